@@ -1,0 +1,156 @@
+/*
+ * tgraph.h -- C ABI of the B200-native BSP graph superstep library (libtgraph.so).
+ *
+ * The library implements the data-parallel hot path of TOTEM (Gharaibeh et al.,
+ * arXiv 1312.3018; "P:n" below = /root/reference/PAPER.md line n): the BSP
+ * superstep over a partitioned CSR graph (§4.1) -- a compute phase per
+ * partition (BFS frontier expansion, PageRank pull-sum, SSSP relaxation, Brandes
+ * BC forward/backward) followed by a communication phase in which each
+ * partition's source-reduced boundary-edge outbox is delivered to the owner
+ * partition's inbox (§4.3.2) -- and the termination vote.
+ *
+ * The calling sequence follows the paper's statement of the problem (Appendix 1,
+ * P:955-971): load an edge list into CSR and partition it (tg_engine_create_*,
+ * P:958-964 graph_initialize + totem_init), run an algorithm with its source or
+ * iteration count, read back per-vertex state in global vertex order
+ * (totem_engine_collect).
+ *
+ * Conventions (all functions):
+ *   - extern "C", plain pointers and sizes, no C++/torch types.
+ *   - Return an int status (tg_status); never throw, never abort.  On a non-zero
+ *     return tg_last_error() gives a thread-local message.
+ *   - Vertex ids are uint32 values in [0, V), V <= 2^31; edge counts uint64.
+ *   - Caller arrays are never retained after a call returns (the library copies
+ *     what it needs).  Output arrays are caller-allocated, length V, indexed by
+ *     GLOBAL vertex id, in host or device memory as `mem` says.
+ *   - An engine is not re-entrant: one call at a time per engine.
+ */
+#ifndef TGRAPH_H
+#define TGRAPH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TG_OK = 0,
+  TG_EINVAL = 2,     /* bad argument: source >= V, id >= V, iterations < 1, a+b+c > 1,
+                        SSSP on an engine built without weights, NULL output, ...    */
+  TG_ECAPACITY = 3,  /* too many partitions / vertices, or does not fit device memory */
+  TG_EIO = 4,        /* reserved for file I/O */
+  TG_EINTERNAL = 5,  /* internal invariant violated (e.g. SSSP distance overflows u32) */
+  TG_ECUDA = 6,      /* CUDA runtime error (message carries cudaGetErrorString)         */
+  TG_ENCCL = 7,      /* NCCL error / NCCL transport unavailable                          */
+} tg_status;
+
+/* Where a caller array lives. */
+typedef enum { TG_MEM_HOST = 0, TG_MEM_DEVICE = 1 } tg_mem;
+
+/* 0xFFFFFFFF: "unreached" for BFS levels and SSSP distances (reading A16). */
+#define TG_INF32 0xFFFFFFFFu
+#define TG_MAX_PARTITIONS 64
+
+const char* tg_version(void);
+/* Message for the last non-OK return on this thread ("" if none). */
+const char* tg_last_error(void);
+
+typedef struct tg_engine tg_engine;
+
+/* Engine attributes (the paper's totem_attr_t, re-aimed at GPUs).
+ *   num_partitions: logical partitions hosted on this process's device, >= 1.
+ *       Vertices are dealt to partitions by the degree-aware serpentine rule
+ *       (reading A23; §6.2): order by out-degree desc,
+ *       id asc; position i -> round r = i/P, j = i%P, partition
+ *       (r even ? j : P-1-j), local id r.  P > 1 on one device exercises the
+ *       full outbox/inbox machinery with device-to-device exchange.
+ *   device: CUDA device ordinal.
+ *   weighted: 1 to keep per-edge SSSP weights (required by tg_sssp).
+ *   build_in_csr: 1 to build the in-edge CSR used by tg_pagerank (pull).
+ *   reserved: must be zero. */
+typedef struct {
+  int num_partitions;
+  int device;
+  int weighted;
+  int build_in_csr;
+  int reserved[4];
+} tg_attr;
+
+/* Build an engine from an explicit directed edge list (duplicates and
+ * self-loops kept).  src/dst/w have length E and live in `mem`; w may be NULL
+ * (unweighted).  Every id must be < V (else TG_EINVAL).  V in [1, 2^31). */
+int tg_engine_create_edges(uint64_t V, uint64_t E, const uint32_t* src, const uint32_t* dst,
+                           const uint32_t* w, int mem, const tg_attr* attr, tg_engine** out);
+
+/* Build an engine from the RMAT stream of inputs/tg_inputs.h, generated on the
+ * device (Table 2: (A,B,C)=(0.57,0.19,0.19), degree 16).  E =
+ * edge_factor * 2^scale; weights drawn from wseed when attr->weighted.
+ * TG_EINVAL if a+b+c > 1, scale outside [1,31] or edge_factor < 1. */
+int tg_engine_create_rmat(int scale, int edge_factor, double a, double b, double c,
+                          uint64_t seed, int scramble, uint64_t wseed, const tg_attr* attr,
+                          tg_engine** out);
+
+void tg_engine_free(tg_engine* eng);
+
+typedef struct {
+  uint64_t V, E;
+  int num_partitions;
+  int weighted, has_in_csr;
+  uint64_t device_bytes;     /* bytes of device memory held by the engine */
+  uint64_t build_ms;         /* wall time of the build, milliseconds       */
+} tg_info;
+int tg_engine_info(const tg_engine* eng, tg_info* info);
+
+/* Per-partition layout (§4.3.1-4.3.2).  slots_to[q] (length P,
+ * nullable) = outbox entries of p destined to q = distinct remote vertices of q
+ * referenced from p (source-side reduction, §3.4). */
+typedef struct {
+  uint64_t Vp, Ep;           /* owned vertices, owned out-edges             */
+  uint64_t Ep_local;         /* out-edges whose target is owned by p        */
+  uint64_t outbox_slots;     /* |V_o| of P:267                              */
+  uint64_t inbox_slots;      /* |V_i| of P:265                              */
+} tg_part_info;
+int tg_engine_partition_info(const tg_engine* eng, int p, tg_part_info* info, uint64_t* slots_to);
+
+/* Run statistics.  device_ms: CUDA-event time on the engine stream from state
+ * initialisation to the final vote (the paper's timed scope; result
+ * collection excluded).  traversed_edges: the paper's TEPS numerator:
+ * BFS/SSSP = sum of out-degrees of reached vertices; BC = 2x that per source;
+ * PageRank = |E| x iterations.  supersteps: BSP rounds executed.
+ * algorithmic_bytes: DESIGN.md §Roofline count for the run.  comm_bytes:
+ * inbox/outbox message bytes moved between partitions.  launches: kernels. */
+typedef struct {
+  double device_ms;
+  uint64_t supersteps;
+  uint64_t traversed_edges;
+  uint64_t algorithmic_bytes;
+  uint64_t comm_bytes;
+  uint64_t launches;
+} tg_stats;
+
+/* Level-synchronous BFS (Fig. 11; App. 1).  levels[v] =
+ * hop distance from source, TG_INF32 if unreached.  stats nullable. */
+int tg_bfs(tg_engine* eng, uint64_t source, uint32_t* levels, int mem, tg_stats* stats);
+
+/* Bellman-Ford SSSP over BSP (Fig. 20).  dist[v] = minimum weight sum,
+ * TG_INF32 if unreached.  TG_EINVAL if the engine has no weights, TG_EINTERNAL
+ * if a distance overflows uint32. */
+int tg_sssp(tg_engine* eng, uint64_t source, uint32_t* dist, int mem, tg_stats* stats);
+
+/* Pull PageRank, `iterations` Jacobi rounds (Fig. 14, readings A1-A8):
+ * r_0 = 1/V; r_{t+1}[v] = (1-d)/V + d * sum_{(u,v)} r_t[u]/outdeg(u).
+ * rank is float32 (4-byte rank).  TG_EINVAL if iterations < 1 or the
+ * engine was built without the in-CSR. */
+int tg_pagerank(tg_engine* eng, int iterations, double damping, float* rank, int mem,
+                tg_stats* stats);
+
+/* Brandes betweenness centrality over k sources (Fig. 18; readings
+ * A9-A14): bc[v] = sum over sources s != v of delta_s(v), fp64, unnormalised,
+ * directed.  sources: host array of k global ids.  bc overwritten. */
+int tg_bc(tg_engine* eng, const uint64_t* sources, int k, double* bc, int mem, tg_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TGRAPH_H */

@@ -1,0 +1,24 @@
+"""B200-native BSP graph superstep engine (TOTEM hot path, arXiv 1312.3018).
+
+Thin ctypes binding of libtgraph.so (include/tgraph.h): argument marshalling
+only -- every step of every algorithm runs in the CUDA kernels of csrc/.  There
+is no CPU fallback: if the library is missing the import fails loudly.
+"""
+from .tgraph import (  # noqa: F401
+    TG_INF32,
+    TG_MEM_DEVICE,
+    TG_MEM_HOST,
+    Engine,
+    Stats,
+    TGraphError,
+    lib,
+    tg_bc,
+    tg_bfs,
+    tg_engine_create_edges,
+    tg_engine_create_rmat,
+    tg_engine_free,
+    tg_engine_info,
+    tg_engine_partition_info,
+    tg_pagerank,
+    tg_sssp,
+)

@@ -1,0 +1,388 @@
+// api.cu -- the extern "C" boundary (include/tgraph.h) plus engine-wide helpers:
+// message exchange between partitions, result collection, statistics.
+#include <cstring>
+#include <functional>
+#include <string>
+
+#include "frontier.cuh"
+
+namespace tg {
+
+static thread_local std::string g_last_error;
+
+Engine::~Engine() {
+  if (stream) cudaStreamSynchronize(stream);
+  parts.clear();
+  rank_of.release();
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (h_counts) cudaFreeHost(h_counts);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+template <typename T>
+static uint64_t b(const DevBuf<T>& d) {
+  return d.bytes();
+}
+
+uint64_t Engine::device_bytes() const {
+  uint64_t t = b(rank_of);
+  for (auto& pp : parts) {
+    const Part& p = *pp;
+    t += b(p.row_off) + b(p.col) + b(p.w) + b(p.global_of) + b(p.tile_vf) + b(p.tile_vl) +
+         b(p.obox_rid) + b(p.ibox_lid) + b(p.in_off) + b(p.in_col) + b(p.in_local) + b(p.in_pos) +
+         b(p.in_slot) + b(p.in_outdeg) + b(p.ibox_inpos);
+  }
+  return t;
+}
+
+void Engine::locate(uint64_t g, int* p, uint32_t* l) const {
+  TG_REQUIRE(g < V, TG_EINVAL, "source vertex " + std::to_string(g) + " >= V");
+  uint32_t i = 0;
+  TG_CK(cudaMemcpy(&i, rank_of.get() + g, 4, cudaMemcpyDeviceToHost));
+  deal(i, P, p, l);
+}
+
+void ensure_frontier_state(Engine& eng) {
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    FrontierState& f = p.fs;
+    const uint64_t nw = std::max<uint64_t>(words_for(p.Vp), 1);
+    if (f.cur.n >= nw && f.counters.n) continue;
+    f.cur.alloc(nw);
+    f.next.alloc(nw);
+    f.visited.alloc(nw);
+    f.vals.alloc(std::max<uint64_t>(p.Vp, 1));
+    const uint64_t sw = std::max<uint64_t>(p.S / 32, 1), iw = std::max<uint64_t>(p.I / 32, 1);
+    f.obox_mark.alloc(sw);
+    f.obox_new.alloc(sw);
+    f.obox_u32.alloc(std::max<uint64_t>(p.S, 1));
+    f.ibox_bits.alloc(iw);
+    f.ibox_u32.alloc(std::max<uint64_t>(p.I, 1));
+    f.counters.alloc(4);
+    p.ts.ensure(p);
+  }
+}
+
+void exchange(Engine& eng, BufOf send, BufOf recv, size_t elem, bool reverse) {
+  // LOCAL transport: every partition lives on this device; the segments are
+  // symmetric by construction, so each (p, q) pair is one D2D copy.
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    for (auto& qq : eng.parts) {
+      Part& q = *qq;
+      if (p.id == q.id) continue;
+      const uint64_t o0 = p.obox_off[q.id], n = p.obox_off[q.id + 1] - o0;  // p -> q segment
+      const uint64_t i0 = q.ibox_off[p.id];
+      if (!n) continue;
+      const uint64_t bytes = elem ? n * elem : n / 8;
+      const uint64_t so = elem ? o0 * elem : o0 / 8, ro = elem ? i0 * elem : i0 / 8;
+      char* ps = static_cast<char*>(reverse ? send(q) : send(p));
+      char* pr = static_cast<char*>(reverse ? recv(p) : recv(q));
+      if (!reverse)
+        TG_CK(cudaMemcpyAsync(pr + ro, ps + so, bytes, cudaMemcpyDeviceToDevice, eng.stream));
+      else
+        TG_CK(cudaMemcpyAsync(pr + so, ps + ro, bytes, cudaMemcpyDeviceToDevice, eng.stream));
+      eng.comm_bytes += bytes;
+    }
+  }
+}
+
+unsigned long long read_counts(Engine& eng, int idx) {
+  const int P = (int)eng.parts.size();
+  for (int i = 0; i < P; ++i)
+    TG_CK(cudaMemcpyAsync(eng.h_counts + i, eng.parts[i]->fs.counters.get() + idx, 8,
+                          cudaMemcpyDeviceToHost, eng.stream));
+  TG_CK(cudaStreamSynchronize(eng.stream));
+  unsigned long long t = 0;
+  for (int i = 0; i < P; ++i) t += eng.h_counts[i];
+  return t;
+}
+
+void time_begin(Engine& eng) { TG_CK(cudaEventRecord(eng.ev0, eng.stream)); }
+double time_end(Engine& eng) {
+  TG_CK(cudaEventRecord(eng.ev1, eng.stream));
+  TG_CK(cudaEventSynchronize(eng.ev1));
+  float ms = 0;
+  TG_CK(cudaEventElapsedTime(&ms, eng.ev0, eng.ev1));
+  return (double)ms;
+}
+
+namespace {
+
+__global__ void k_reached_u32(const uint32_t* vals, const uint64_t* row_off, uint64_t Vp,
+                              unsigned long long* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long s = 0, n = 0;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < Vp; v += stride)
+    if (vals[v] != kInf) {
+      s += row_off[v + 1] - row_off[v];
+      n++;
+    }
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    n += __shfl_down_sync(0xffffffffu, n, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (s) atomicAdd(&out[0], s);
+    if (n) atomicAdd(&out[1], n);
+  }
+}
+
+__global__ void k_reached_bm(const uint32_t* bm, const uint64_t* row_off, uint64_t Vp,
+                             unsigned long long* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long s = 0, n = 0;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < Vp; v += stride)
+    if ((bm[v >> 5] >> (v & 31)) & 1u) {
+      s += row_off[v + 1] - row_off[v];
+      n++;
+    }
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, o);
+    n += __shfl_down_sync(0xffffffffu, n, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (s) atomicAdd(&out[0], s);
+    if (n) atomicAdd(&out[1], n);
+  }
+}
+
+__global__ void k_collect_u32(const uint32_t* vals, const uint32_t* global_of, uint64_t Vp,
+                              uint32_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride)
+    out[global_of[i]] = vals[i];
+}
+
+uint64_t reached(Engine& eng, bool bitmap, uint64_t* nreached) {
+  DevBuf<unsigned long long> acc(2);
+  TG_CK(cudaMemsetAsync(acc.get(), 0, 16, eng.stream));
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    if (!p.Vp) continue;
+    if (bitmap)
+      k_reached_bm<<<grid_for(p.Vp, 256), 256, 0, eng.stream>>>(p.fs.visited.get(), p.row_off.get(),
+                                                                p.Vp, acc.get());
+    else
+      k_reached_u32<<<grid_for(p.Vp, 256), 256, 0, eng.stream>>>(p.fs.vals.get(), p.row_off.get(),
+                                                                 p.Vp, acc.get());
+  }
+  TG_CK(cudaGetLastError());
+  unsigned long long h[2];
+  TG_CK(cudaMemcpyAsync(h, acc.get(), 16, cudaMemcpyDeviceToHost, eng.stream));
+  TG_CK(cudaStreamSynchronize(eng.stream));
+  if (nreached) *nreached = h[1];
+  return h[0];
+}
+
+}  // namespace
+
+uint64_t reached_outdeg_u32(Engine& eng, uint64_t* nreached) { return reached(eng, false, nreached); }
+uint64_t reached_outdeg_bitmap(Engine& eng, uint64_t* nreached) { return reached(eng, true, nreached); }
+
+void collect_u32(Engine& eng, uint32_t* out, int mem) {
+  TG_REQUIRE(out != nullptr, TG_EINVAL, "NULL output array");
+  uint32_t* dout = out;
+  DevBuf<uint32_t> tmp;
+  if (mem == TG_MEM_HOST) {
+    tmp.alloc(eng.V);
+    dout = tmp.get();
+  }
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    if (!p.Vp) continue;
+    k_collect_u32<<<grid_for(p.Vp, 256), 256, 0, eng.stream>>>(p.fs.vals.get(), p.global_of.get(),
+                                                               p.Vp, dout);
+  }
+  TG_CK(cudaGetLastError());
+  if (mem == TG_MEM_HOST)
+    TG_CK(cudaMemcpyAsync(out, dout, eng.V * 4, cudaMemcpyDeviceToHost, eng.stream));
+  TG_CK(cudaStreamSynchronize(eng.stream));
+}
+
+static int guard(const std::function<void()>& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return TG_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host out of memory";
+    return TG_ECAPACITY;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TG_EINTERNAL;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return TG_EINTERNAL;
+  }
+}
+
+static void init_engine(Engine& eng, const tg_attr* attr) {
+  TG_REQUIRE(attr != nullptr, TG_EINVAL, "NULL attr");
+  TG_REQUIRE(attr->num_partitions >= 1, TG_EINVAL, "num_partitions must be >= 1");
+  TG_REQUIRE(attr->num_partitions <= TG_MAX_PARTITIONS, TG_ECAPACITY,
+             "num_partitions > TG_MAX_PARTITIONS");
+  for (int r : attr->reserved) TG_REQUIRE(r == 0, TG_EINVAL, "tg_attr.reserved must be zero");
+  int ndev = 0;
+  TG_CK(cudaGetDeviceCount(&ndev));
+  TG_REQUIRE(attr->device >= 0 && attr->device < ndev, TG_EINVAL, "bad CUDA device ordinal");
+  eng.device = attr->device;
+  TG_CK(cudaSetDevice(eng.device));
+  eng.P = attr->num_partitions;
+  eng.weighted = attr->weighted != 0;
+  eng.has_in = attr->build_in_csr != 0;
+  TG_CK(cudaStreamCreateWithFlags(&eng.stream, cudaStreamNonBlocking));
+  TG_CK(cudaEventCreate(&eng.ev0));
+  TG_CK(cudaEventCreate(&eng.ev1));
+  TG_CK(cudaMallocHost(&eng.h_counts, sizeof(unsigned long long) * TG_MAX_PARTITIONS * 4));
+}
+
+}  // namespace tg
+
+using namespace tg;
+
+extern "C" {
+
+const char* tg_version(void) { return "tgraph 0.1 (sm_100a)"; }
+const char* tg_last_error(void) { return g_last_error.c_str(); }
+
+int tg_engine_create_edges(uint64_t V, uint64_t E, const uint32_t* src, const uint32_t* dst,
+                           const uint32_t* w, int mem, const tg_attr* attr, tg_engine** out) {
+  return guard([&] {
+    TG_REQUIRE(out != nullptr, TG_EINVAL, "NULL out");
+    *out = nullptr;
+    TG_REQUIRE(V >= 1 && V < (1ull << 31), TG_EINVAL, "V must be in [1, 2^31)");
+    TG_REQUIRE(E == 0 || (src && dst), TG_EINVAL, "NULL edge arrays");
+    TG_REQUIRE(mem == TG_MEM_HOST || mem == TG_MEM_DEVICE, TG_EINVAL, "bad mem kind");
+    auto eng = std::make_unique<Engine>();
+    init_engine(*eng, attr);
+    TG_REQUIRE(!eng->weighted || w != nullptr || E == 0, TG_EINVAL,
+               "attr.weighted set but no weight array given");
+    eng->V = V;
+    eng->E = E;
+    DevBuf<uint32_t> ds, dd, dw;
+    EdgeInput in;
+    in.generated = false;
+    if (mem == TG_MEM_HOST && E) {
+      ds.alloc(E);
+      dd.alloc(E);
+      TG_CK(cudaMemcpy(ds.get(), src, E * 4, cudaMemcpyHostToDevice));
+      TG_CK(cudaMemcpy(dd.get(), dst, E * 4, cudaMemcpyHostToDevice));
+      if (w && eng->weighted) {
+        dw.alloc(E);
+        TG_CK(cudaMemcpy(dw.get(), w, E * 4, cudaMemcpyHostToDevice));
+      }
+      in.src = ds.get();
+      in.dst = dd.get();
+      in.w = dw.get();
+    } else {
+      in.src = src;
+      in.dst = dst;
+      in.w = eng->weighted ? w : nullptr;
+    }
+    build_engine(*eng, in);
+    *out = reinterpret_cast<tg_engine*>(eng.release());
+  });
+}
+
+int tg_engine_create_rmat(int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                          int scramble, uint64_t wseed, const tg_attr* attr, tg_engine** out) {
+  return guard([&] {
+    TG_REQUIRE(out != nullptr, TG_EINVAL, "NULL out");
+    *out = nullptr;
+    TG_REQUIRE(scale >= 1 && scale <= 31, TG_EINVAL, "scale must be in [1, 31]");
+    TG_REQUIRE(edge_factor >= 1, TG_EINVAL, "edge_factor must be >= 1");
+    TG_REQUIRE(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0 + 1e-12, TG_EINVAL,
+               "RMAT probabilities: need a, b, c >= 0 and a + b + c <= 1");
+    auto eng = std::make_unique<Engine>();
+    init_engine(*eng, attr);
+    eng->V = 1ull << scale;
+    eng->E = (uint64_t)edge_factor << scale;
+    EdgeInput in;
+    in.generated = true;
+    in.scale = scale;
+    in.a = a;
+    in.b = b;
+    in.c = c;
+    in.seed = seed;
+    in.wseed = wseed;
+    in.scramble = scramble;
+    build_engine(*eng, in);
+    *out = reinterpret_cast<tg_engine*>(eng.release());
+  });
+}
+
+void tg_engine_free(tg_engine* e) {
+  if (!e) return;
+  Engine* eng = reinterpret_cast<Engine*>(e);
+  cudaSetDevice(eng->device);
+  delete eng;
+}
+
+int tg_engine_info(const tg_engine* e, tg_info* info) {
+  return guard([&] {
+    TG_REQUIRE(e && info, TG_EINVAL, "NULL argument");
+    const Engine* eng = reinterpret_cast<const Engine*>(e);
+    info->V = eng->V;
+    info->E = eng->E;
+    info->num_partitions = eng->P;
+    info->weighted = eng->weighted;
+    info->has_in_csr = eng->has_in;
+    info->device_bytes = eng->device_bytes();
+    info->build_ms = eng->build_ms;
+  });
+}
+
+int tg_engine_partition_info(const tg_engine* e, int p, tg_part_info* info, uint64_t* slots_to) {
+  return guard([&] {
+    TG_REQUIRE(e && info, TG_EINVAL, "NULL argument");
+    const Engine* eng = reinterpret_cast<const Engine*>(e);
+    TG_REQUIRE(p >= 0 && p < eng->P, TG_EINVAL, "partition index out of range");
+    const Part& pt = *eng->parts[p];
+    info->Vp = pt.Vp;
+    info->Ep = pt.Ep;
+    info->Ep_local = pt.Ep_local;
+    info->outbox_slots = pt.S_real;
+    info->inbox_slots = pt.I_real;
+    if (slots_to)
+      for (int q = 0; q < eng->P; ++q) slots_to[q] = q < (int)pt.seg_real.size() ? pt.seg_real[q] : 0;
+  });
+}
+
+#define TG_RUN(body)                                                     \
+  return guard([&] {                                                     \
+    TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");                  \
+    Engine& eng = *reinterpret_cast<Engine*>(e);                         \
+    TG_REQUIRE(mem == TG_MEM_HOST || mem == TG_MEM_DEVICE, TG_EINVAL, "bad mem kind"); \
+    TG_CK(cudaSetDevice(eng.device));                                    \
+    if (st) std::memset(st, 0, sizeof(*st));                             \
+    body;                                                                \
+  })
+
+int tg_bfs(tg_engine* e, uint64_t source, uint32_t* levels, int mem, tg_stats* st) {
+  TG_RUN({
+    TG_REQUIRE(levels != nullptr, TG_EINVAL, "NULL levels");
+    run_bfs(eng, source, levels, mem, st);
+  });
+}
+
+int tg_sssp(tg_engine* e, uint64_t source, uint32_t* dist, int mem, tg_stats* st) {
+  TG_RUN({
+    TG_REQUIRE(dist != nullptr, TG_EINVAL, "NULL dist");
+    run_sssp(eng, source, dist, mem, st);
+  });
+}
+
+int tg_pagerank(tg_engine* e, int iterations, double damping, float* rank, int mem, tg_stats* st) {
+  TG_RUN({ run_pagerank(eng, iterations, damping, rank, mem, st); });
+}
+
+int tg_bc(tg_engine* e, const uint64_t* sources, int k, double* bc, int mem, tg_stats* st) {
+  TG_RUN({ run_bc(eng, sources, k, bc, mem, st); });
+}
+
+}  // extern "C"

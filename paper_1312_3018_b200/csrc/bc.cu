@@ -1,0 +1,327 @@
+// bc.cu -- Brandes betweenness centrality as two BSP cycles per source
+// (Fig. 18; readings A9-A14).
+//
+// Forward cycle, superstep L (frontier = level-L bitmap F[L]):
+//   edge (v,t): t unvisited -> sigma[t] += sigma[v] (fp64 atomic add, Fig. 18
+//   line 12) and t joins F[L+1] (lines 7-9).  Remote t: the partial sigma is
+//   summed into t's outbox slot unless the slot was sent at an earlier level
+//   (then t is known to be at level <= L); sigma messages are pushed, the owner
+//   adds those that reach a still-unvisited vertex.  Level bitmaps F[0..maxL]
+//   are kept for the backward cycle.
+// Backward cycle, L = maxL .. 1 (pull):
+//   c[w] = (1 + delta[w]) / sigma[w] for w in F[L+1]; owners publish c of their
+//   boundary vertices to the referencing partitions (ghosts);
+//   delta[v] = sigma[v] * sum_{(v,w), w in F[L+1]} c[w]     (Fig. 18 lines 22-30
+//   with the "1 +" of Brandes' recurrence restored, reading A9);
+//   bc[v] += delta[v]; the source (level 0) is never updated (line 34).
+// The backward sum uses the tile kernel in reduce mode: per-row sums in shared
+// memory, rows that span tiles accumulate with fp64 atomics.
+#include "frontier.cuh"
+
+namespace tg {
+
+namespace {
+
+struct BcFwdOp {
+  using Aux = double;
+  static constexpr bool kReduce = false;
+  const uint32_t* col;
+  const uint32_t* visited;
+  uint32_t* next;
+  double* sigma;
+  const uint32_t* omark;
+  uint32_t* onew;
+  double* osigma;
+  __device__ __forceinline__ Aux aux(uint32_t v) const { return sigma[v]; }
+  __device__ __forceinline__ void edge(uint32_t, const Aux& sv, uint64_t e) const {
+    const uint32_t t = __ldcs(col + e);
+    if (t & kRemote) {
+      const uint32_t s = t & ~kRemote, m = 1u << (s & 31);
+      if (!(omark[s >> 5] & m)) {
+        atomicAdd(&osigma[s], sv);
+        if (!(onew[s >> 5] & m)) atomicOr(&onew[s >> 5], m);
+      }
+    } else {
+      const uint32_t m = 1u << (t & 31);
+      if (!(__ldg(visited + (t >> 5)) & m)) {
+        atomicAdd(&sigma[t], sv);
+        if (!(next[t >> 5] & m)) atomicOr(&next[t >> 5], m);
+      }
+    }
+  }
+};
+
+struct BcBwdOp {
+  using Aux = Empty;
+  static constexpr bool kReduce = true;
+  const uint32_t* col;
+  const uint32_t* succ;  // F[L+1]
+  const double* c;
+  const double* ghost;
+  double* dsum;
+  __device__ __forceinline__ Aux aux(uint32_t) const { return {}; }
+  __device__ __forceinline__ double edge_val(uint32_t, const Aux&, uint64_t e) const {
+    const uint32_t t = __ldcs(col + e);
+    if (t & kRemote) return ghost[t & ~kRemote];
+    return bit_test(succ, t) ? c[t] : 0.0;
+  }
+  __device__ __forceinline__ void vertex_done(uint32_t v, const Aux&, double acc, bool whole) const {
+    if (whole) dsum[v] = acc;
+    else atomicAdd(&dsum[v], acc);
+  }
+};
+
+__global__ void k_bc_seed(uint32_t* bm, uint32_t i, double* sigma) {
+  bm[i >> 5] |= 1u << (i & 31);
+  sigma[i] = 1.0;
+}
+
+__global__ void k_bc_scatter(const double* msg, const uint32_t* lid, uint64_t I, const uint32_t* visited,
+                             double* sigma, uint32_t* next) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < I; j += stride) {
+    const double m = msg[j];
+    if (!(m > 0.0)) continue;
+    const uint32_t v = lid[j];
+    if (bit_test(visited, v)) continue;
+    atomicAdd(&sigma[v], m);
+    bit_set_atomic(next, v);
+  }
+}
+
+__global__ void k_or_clear(uint32_t* mark, uint32_t* nw, uint64_t words) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words; i += stride) {
+    const uint32_t x = nw[i];
+    if (x) {
+      mark[i] |= x;
+      nw[i] = 0;
+    }
+  }
+}
+
+// owner side of the backward pull: c of boundary vertices in F[L+1], else 0
+__global__ void k_bc_pack(const uint32_t* lid, uint64_t I, const uint32_t* succ, const double* c,
+                          double* pack) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < I; j += stride) {
+    const uint32_t v = lid[j];
+    pack[j] = (v != kInf && bit_test(succ, v)) ? c[v] : 0.0;
+  }
+}
+
+// delta, bc and c for the vertices of level L (one warp per bitmap word)
+__global__ void k_bc_level(const uint32_t* F, uint64_t Vp, uint64_t nz_end, const double* sigma,
+                           const double* dsum, double* bc, double* c) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t nwords = words_for(Vp);
+  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < nwords; w += nwarps) {
+    const uint32_t x = F[w];
+    if (!((x >> lane) & 1u)) continue;
+    const uint64_t v = w * 32 + lane;
+    const double sv = sigma[v];
+    const double delta = v < nz_end ? sv * dsum[v] : 0.0;
+    bc[v] += delta;
+    c[v] = (1.0 + delta) / sv;
+  }
+}
+
+__global__ void k_collect_f64(const double* vals, const uint32_t* global_of, uint64_t Vp, double* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride)
+    out[global_of[i]] = vals[i];
+}
+
+void* send_osigma(Part& p) { return p.bcs.obox_sigma.get(); }
+void* recv_isigma(Part& p) { return p.bcs.ibox_sigma.get(); }
+void* send_pack(Part& p) { return p.bcs.ibox_pack.get(); }
+void* recv_ghost(Part& p) { return p.bcs.ghost.get(); }
+
+uint32_t* level_bitmap(Part& p, size_t L) {
+  BCState& b = p.bcs;
+  const uint64_t nw = std::max<uint64_t>(words_for(p.Vp), 1);
+  while (b.level_bm.size() <= L) b.level_bm.emplace_back(nw);
+  return b.level_bm[L].get();
+}
+
+}  // namespace
+
+void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, tg_stats* st) {
+  TG_REQUIRE(k >= 0 && (k == 0 || sources), TG_EINVAL, "tg_bc: bad source list");
+  TG_REQUIRE(out != nullptr, TG_EINVAL, "tg_bc: NULL output");
+  for (int i = 0; i < k; ++i) TG_REQUIRE(sources[i] < eng.V, TG_EINVAL, "tg_bc: source >= V");
+  ensure_frontier_state(eng);
+  cudaStream_t s = eng.stream;
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    BCState& b = p.bcs;
+    const uint64_t Vn = std::max<uint64_t>(p.Vp, 1);
+    if (b.sigma.n < Vn) {
+      b.sigma.alloc(Vn);
+      b.dsum.alloc(Vn);
+      b.c.alloc(Vn);
+      b.bc.alloc(Vn);
+    }
+    if (eng.P > 1 && b.obox_sigma.n < std::max<uint64_t>(p.S, 1)) {
+      b.obox_sigma.alloc(std::max<uint64_t>(p.S, 1));
+      b.ghost.alloc(std::max<uint64_t>(p.S, 1));
+      b.ibox_sigma.alloc(std::max<uint64_t>(p.I, 1));
+      b.ibox_pack.alloc(std::max<uint64_t>(p.I, 1));
+    }
+    TG_CK(cudaMemsetAsync(b.bc.get(), 0, Vn * 8, s));
+  }
+  eng.launches = 0;
+  eng.comm_bytes = 0;
+  double total_ms = 0;
+  uint64_t supersteps = 0, traversed = 0, bytes = 0;
+  for (int si = 0; si < k; ++si) {
+    int ps;
+    uint32_t ls;
+    eng.locate(sources[si], &ps, &ls);
+    time_begin(eng);
+    // ---------------- forward cycle ----------------
+    for (auto& pp : eng.parts) {
+      Part& p = *pp;
+      FrontierState& f = p.fs;
+      BCState& b = p.bcs;
+      const uint64_t nw = words_for(p.Vp);
+      TG_CK(cudaMemsetAsync(b.sigma.get(), 0, p.Vp * 8, s));
+      TG_CK(cudaMemsetAsync(b.dsum.get(), 0, p.Vp * 8, s));
+      TG_CK(cudaMemsetAsync(f.visited.get(), 0, nw * 4, s));
+      uint32_t* F0 = level_bitmap(p, 0);
+      TG_CK(cudaMemsetAsync(F0, 0, nw * 4, s));
+      if (p.S) {
+        TG_CK(cudaMemsetAsync(f.obox_mark.get(), 0, p.S / 8, s));
+        TG_CK(cudaMemsetAsync(f.obox_new.get(), 0, p.S / 8, s));
+        TG_CK(cudaMemsetAsync(b.obox_sigma.get(), 0, p.S * 8, s));
+      }
+      TG_CK(cudaMemsetAsync(f.counters.get(), 0, f.counters.bytes(), s));
+      if (p.id == ps) {
+        k_bc_seed<<<1, 1, 0, s>>>(F0, ls, b.sigma.get());
+        eng.launches++;
+      }
+      launch_advance(eng, p, p.ts, F0, nullptr, f.visited.get(), nullptr, 0, f.counters.get());
+    }
+    uint32_t maxL = 0;
+    for (uint32_t L = 0;; ++L) {
+      for (auto& pp : eng.parts) {
+        Part& p = *pp;
+        FrontierState& f = p.fs;
+        BCState& b = p.bcs;
+        uint32_t* next = level_bitmap(p, L + 1);
+        TG_CK(cudaMemsetAsync(next, 0, words_for(p.Vp) * 4, s));
+        launch_compact(eng, p.ts);
+        BcFwdOp op{p.col.get(), f.visited.get(), next, b.sigma.get(), f.obox_mark.get(),
+                   f.obox_new.get(), b.obox_sigma.get()};
+        launch_expand(eng, p, p.ts, b.level_bm[L].get(), op);
+      }
+      supersteps++;
+      if (eng.P > 1) {
+        exchange(eng, send_osigma, recv_isigma, 8, false);
+        for (auto& pp : eng.parts) {
+          Part& p = *pp;
+          FrontierState& f = p.fs;
+          BCState& b = p.bcs;
+          if (p.S) {
+            k_or_clear<<<grid_for(p.S / 32, 256), 256, 0, s>>>(f.obox_mark.get(), f.obox_new.get(),
+                                                               p.S / 32);
+            TG_CK(cudaMemsetAsync(b.obox_sigma.get(), 0, p.S * 8, s));
+            eng.launches++;
+          }
+          if (p.I) {
+            k_bc_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(b.ibox_sigma.get(), p.ibox_lid.get(), p.I,
+                                                            f.visited.get(), b.sigma.get(),
+                                                            b.level_bm[L + 1].get());
+            eng.launches++;
+          }
+          TG_CK(cudaGetLastError());
+        }
+      }
+      for (auto& pp : eng.parts) {
+        Part& p = *pp;
+        FrontierState& f = p.fs;
+        TG_CK(cudaMemsetAsync(f.counters.get(), 0, 8, s));
+        launch_advance(eng, p, p.ts, p.bcs.level_bm[L + 1].get(), nullptr, f.visited.get(), nullptr,
+                       0, f.counters.get());
+      }
+      if (read_counts(eng, 0) == 0) {
+        maxL = L;  // F[L+1] is empty
+        break;
+      }
+      TG_REQUIRE(L <= eng.V, TG_EINTERNAL, "tg_bc: superstep bound exceeded");
+    }
+    // ---------------- backward cycle ----------------
+    for (uint32_t L = maxL; L >= 1; --L) {
+      if (L < maxL) {
+        if (eng.P > 1) {
+          for (auto& pp : eng.parts) {
+            Part& p = *pp;
+            if (!p.I) continue;
+            k_bc_pack<<<grid_for(p.I, 256), 256, 0, s>>>(p.ibox_lid.get(), p.I,
+                                                         p.bcs.level_bm[L + 1].get(), p.bcs.c.get(),
+                                                         p.bcs.ibox_pack.get());
+            eng.launches++;
+          }
+          TG_CK(cudaGetLastError());
+          exchange(eng, send_pack, recv_ghost, 8, true);
+        }
+        for (auto& pp : eng.parts) {
+          Part& p = *pp;
+          if (!p.ntiles) continue;
+          k_mark_tiles<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
+              p.bcs.level_bm[L].get(), p.Vp, p.row_off.get(), p.ts.bm.get());
+          TG_CK(cudaGetLastError());
+          eng.launches++;
+          launch_compact(eng, p.ts);
+          BcBwdOp op{p.col.get(), p.bcs.level_bm[L + 1].get(), p.bcs.c.get(), p.bcs.ghost.get(),
+                     p.bcs.dsum.get()};
+          launch_expand(eng, p, p.ts, p.bcs.level_bm[L].get(), op);
+        }
+        supersteps++;
+      }
+      for (auto& pp : eng.parts) {
+        Part& p = *pp;
+        if (!p.Vp) continue;
+        k_bc_level<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
+            p.bcs.level_bm[L].get(), p.Vp, p.nz_end, p.bcs.sigma.get(), p.bcs.dsum.get(),
+            p.bcs.bc.get(), p.bcs.c.get());
+        TG_CK(cudaGetLastError());
+        eng.launches++;
+      }
+    }
+    total_ms += time_end(eng);
+    uint64_t nreached = 0;
+    const uint64_t tr = reached_outdeg_bitmap(eng, &nreached);
+    traversed += 2 * tr;
+    // forward: col 4 + visited probe 4 + sigma RMW 8 per edge; backward: col 4 +
+    // successor probe 4 + c gather 8 per edge; per reached vertex offsets 16 x2,
+    // sigma/dsum/bc/c 32
+    bytes += 32 * tr + 64 * nreached;
+  }
+  if (st) {
+    st->device_ms = total_ms;
+    st->supersteps = supersteps;
+    st->traversed_edges = traversed;
+    st->algorithmic_bytes = bytes;
+    st->comm_bytes = eng.comm_bytes;
+    st->launches = eng.launches;
+  }
+  double* dout = out;
+  DevBuf<double> tmp;
+  if (mem == TG_MEM_HOST) {
+    tmp.alloc(eng.V);
+    dout = tmp.get();
+  }
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    if (!p.Vp) continue;
+    k_collect_f64<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.bcs.bc.get(), p.global_of.get(), p.Vp, dout);
+  }
+  TG_CK(cudaGetLastError());
+  if (mem == TG_MEM_HOST)
+    TG_CK(cudaMemcpyAsync(out, dout, eng.V * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace tg

@@ -1,0 +1,587 @@
+// build.cu -- device-side CSR builder and degree-aware partitioner (untimed
+// pre-processing).  Steps:
+//   1. out-degrees of the edge stream (generated on the device from
+//      inputs/tg_inputs.h, or uploaded);
+//   2. degree order: stable radix sort of ~outdeg -> order[i], rank_of[g]
+//      (§6.2 sorts by degree; ties by id, reading A23);
+//   3. per partition p (serpentine deal of the order): local/remote row degrees,
+//      the distinct remote targets (outbox slots, source-side reduction of
+//      PAPER.md:168-182), out-CSR with local-before-remote rows and
+//      kRemote|slot payloads for boundary edges, edge tiles;
+//   4. optional PageRank in-CSR (rows sorted by in-degree; outbox rows appended);
+//   5. inboxes = peers' outbox segments (symmetry).
+// CUB is used for the V-sized sorts/scans of this untimed build only; no
+// library code runs inside a timed algorithm.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <chrono>
+
+#include "engine.cuh"
+#include "tg_inputs.h"
+
+namespace tg {
+
+namespace {
+
+struct EdgeGen {
+  const uint32_t *src, *dst, *w;
+  bool gen;
+  int scale, scramble;
+  tgin_thresholds t;
+  uint64_t seed, wseed;
+  __device__ __forceinline__ void get(uint64_t k, uint32_t& s, uint32_t& d) const {
+    if (gen) {
+      tgin_rmat_edge(scale, t, seed, scramble, k, &s, &d);
+    } else {
+      s = src[k];
+      d = dst[k];
+    }
+  }
+  __device__ __forceinline__ uint32_t weight(uint64_t k) const {
+    return gen ? tgin_weight(wseed, k) : (w ? w[k] : 1u);
+  }
+};
+
+__device__ __forceinline__ void block_add_u64(unsigned long long* dst, unsigned long long v) {
+  // warp reduce then one atomic per warp
+  for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+__global__ void k_outdeg(EdgeGen g, uint64_t E, uint64_t V, uint32_t* outdeg,
+                         unsigned long long* bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < E; k += stride) {
+    uint32_t s, d;
+    g.get(k, s, d);
+    if (s >= V || d >= V) {
+      atomicAdd(bad, 1ull);
+      continue;
+    }
+    atomicAdd(&outdeg[s], 1u);
+  }
+}
+
+__global__ void k_neg_iota(const uint32_t* outdeg, uint64_t V, uint32_t* keys, uint32_t* vals) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V; v += stride) {
+    keys[v] = ~outdeg[v];
+    vals[v] = (uint32_t)v;
+  }
+}
+
+__global__ void k_inverse(const uint32_t* order, uint64_t V, uint32_t* rank_of) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += stride)
+    rank_of[order[i]] = (uint32_t)i;
+}
+
+__global__ void k_global_of(const uint32_t* order, uint64_t Vp, int p, int P, const uint32_t* outdeg,
+                            uint32_t* global_of, unsigned long long* nz) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long cnt = 0;
+  for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < Vp; l += stride) {
+    const uint32_t g = order[undeal((uint32_t)l, p, P)];
+    global_of[l] = g;
+    cnt += outdeg[g] > 0;
+  }
+  block_add_u64(nz, cnt);
+}
+
+__global__ void k_gather_deg(const uint32_t* gof, const uint32_t* od, uint64_t n, uint32_t* o) {
+  const uint64_t st = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l < n; l += st) o[l] = od[gof[l]];
+}
+
+// local / remote row degrees of partition p
+__global__ void k_count(EdgeGen g, uint64_t E, const uint32_t* rank_of, int P, int p,
+                        uint32_t* nloc, uint32_t* nrem, unsigned long long* nremote) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long cnt = 0;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < E; k += stride) {
+    uint32_t s, d, ls, ld;
+    int ps, pd;
+    g.get(k, s, d);
+    deal(rank_of[s], P, &ps, &ls);
+    if (ps != p) continue;
+    deal(rank_of[d], P, &pd, &ld);
+    if (pd == p) {
+      atomicAdd(&nloc[ls], 1u);
+    } else {
+      atomicAdd(&nrem[ls], 1u);
+      cnt++;
+    }
+  }
+  block_add_u64(nremote, cnt);
+}
+
+__global__ void k_collect_keys(EdgeGen g, uint64_t E, const uint32_t* rank_of, int P, int p,
+                               unsigned long long* keys, unsigned long long* counter) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < E; k += stride) {
+    uint32_t s, d, ls, ld;
+    int ps, pd;
+    g.get(k, s, d);
+    deal(rank_of[s], P, &ps, &ls);
+    if (ps != p) continue;
+    deal(rank_of[d], P, &pd, &ld);
+    if (pd == p) continue;
+    keys[atomicAdd(counter, 1ull)] = ((unsigned long long)pd << 32) | ld;
+  }
+}
+
+__global__ void k_deg64(const uint32_t* nloc, const uint32_t* nrem, uint64_t Vp, uint64_t* deg) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t l = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; l <= Vp; l += stride)
+    deg[l] = l < Vp ? (uint64_t)nloc[l] + (nrem ? nrem[l] : 0u) : 0ull;
+}
+
+__global__ void k_seg_count(const unsigned long long* ukeys, uint64_t n, unsigned long long* cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += stride)
+    atomicAdd(&cnt[ukeys[u] >> 32], 1ull);
+}
+
+__global__ void k_place_slots(const unsigned long long* ukeys, uint64_t n, const uint64_t* ustart,
+                              const uint64_t* poff, uint32_t* obox_rid) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n; u += stride) {
+    const unsigned long long key = ukeys[u];
+    const uint32_t q = (uint32_t)(key >> 32);
+    obox_rid[poff[q] + (u - ustart[q])] = (uint32_t)key;
+  }
+}
+
+__device__ __forceinline__ uint64_t lower_bound_u64(const unsigned long long* a, uint64_t n,
+                                                    unsigned long long x) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t m = (lo + hi) >> 1;
+    if (a[m] < x) lo = m + 1;
+    else hi = m;
+  }
+  return lo;
+}
+
+__global__ void k_fill(EdgeGen g, uint64_t E, const uint32_t* rank_of, int P, int p,
+                       const uint64_t* row_off, const uint32_t* nloc, uint32_t* cur_loc,
+                       uint32_t* cur_rem, uint32_t* col, uint32_t* w, bool weighted,
+                       const unsigned long long* ukeys, uint64_t nukeys, const uint64_t* ustart,
+                       const uint64_t* poff) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < E; k += stride) {
+    uint32_t s, d, ls, ld;
+    int ps, pd;
+    g.get(k, s, d);
+    deal(rank_of[s], P, &ps, &ls);
+    if (ps != p) continue;
+    deal(rank_of[d], P, &pd, &ld);
+    uint64_t pos;
+    uint32_t val;
+    if (pd == p) {
+      pos = row_off[ls] + atomicAdd(&cur_loc[ls], 1u);
+      val = ld;
+    } else {
+      pos = row_off[ls] + nloc[ls] + atomicAdd(&cur_rem[ls], 1u);
+      const unsigned long long key = ((unsigned long long)pd << 32) | ld;
+      const uint64_t u = lower_bound_u64(ukeys, nukeys, key);
+      val = kRemote | (uint32_t)(poff[pd] + (u - ustart[pd]));
+    }
+    col[pos] = val;
+    if (weighted) w[pos] = g.weight(k);
+  }
+}
+
+__device__ __forceinline__ uint32_t row_of_edge(const uint64_t* row_off, uint64_t lo, uint64_t hi,
+                                                uint64_t e) {
+  // largest v in [lo, hi] with row_off[v] <= e
+  while (lo < hi) {
+    const uint64_t m = (lo + hi + 1) >> 1;
+    if (row_off[m] <= e) lo = m;
+    else hi = m - 1;
+  }
+  return (uint32_t)lo;
+}
+
+__global__ void k_tiles(const uint64_t* row_off, uint64_t Vp, uint64_t Ep, uint64_t ntiles,
+                        uint32_t* vf, uint32_t* vl) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < ntiles; t += stride) {
+    const uint64_t e0 = t * kTile;
+    const uint64_t e1 = min(e0 + kTile, Ep) - 1;
+    vf[t] = row_of_edge(row_off, 0, Vp - 1, e0);
+    vl[t] = row_of_edge(row_off, 0, Vp - 1, e1);
+  }
+}
+
+// ---- PageRank in-CSR ----
+// Each thread walks edges via the tile metadata to find its source row.
+__global__ void k_in_count(const uint64_t* row_off, const uint32_t* col, uint64_t Ep, uint64_t Vp,
+                           const uint32_t* vf, const uint32_t* vl, uint32_t* indeg) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < Ep; e += stride) {
+    const uint32_t t = col[e];
+    const uint64_t r = (t & kRemote) ? Vp + (t & ~kRemote) : t;
+    atomicAdd(&indeg[r], 1u);
+  }
+}
+
+__global__ void k_scatter_pos(const uint32_t* vals, uint64_t n, uint64_t base, uint32_t* pos_of) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    pos_of[vals[i]] = (uint32_t)(base + i);
+}
+
+__global__ void k_in_deg_sorted(const uint32_t* keys_sorted, uint64_t n, uint64_t base,
+                                uint64_t* deg64, unsigned long long* cls, uint32_t t_cta) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long c_cta = 0, c_warp = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t d = ~keys_sorted[i];
+    deg64[base + i] = d;
+    c_cta += d >= t_cta;
+    c_warp += d >= 32;
+  }
+  block_add_u64(&cls[0], c_cta);
+  block_add_u64(&cls[1], c_warp);
+}
+
+__global__ void k_in_fill(const uint64_t* row_off, const uint32_t* col, uint64_t Ep, uint64_t Vp,
+                          const uint32_t* vf, const uint32_t* vl, const uint32_t* in_pos,
+                          const uint32_t* slot_pos, const uint64_t* in_off, uint32_t* cursor,
+                          uint32_t* in_col) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < Ep; e += stride) {
+    const uint64_t tile = e / kTile;
+    const uint32_t l = row_of_edge(row_off, vf[tile], vl[tile], e);
+    const uint32_t t = col[e];
+    const uint32_t r = (t & kRemote) ? slot_pos[t & ~kRemote] : in_pos[t];
+    const uint64_t pos = in_off[r] + atomicAdd(&cursor[r], 1u);
+    in_col[pos] = in_pos[l];
+  }
+}
+
+__global__ void k_in_outdeg(const uint64_t* row_off, const uint32_t* in_local, uint64_t Vp,
+                            uint32_t* in_outdeg) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride) {
+    const uint32_t l = in_local[i];
+    in_outdeg[i] = (uint32_t)(row_off[l + 1] - row_off[l]);
+  }
+}
+
+__global__ void k_ibox_inpos(const uint32_t* lid, uint64_t n, const uint32_t* in_pos, uint32_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = lid[i] == kInf ? kInf : in_pos[lid[i]];
+}
+
+template <typename T>
+T d2h(const T* p, cudaStream_t s) {
+  T v;
+  TG_CK(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+  return v;
+}
+
+constexpr unsigned kB = 256;
+inline unsigned G(uint64_t n) { return grid_for(n, kB, 148u * 32u); }
+
+// Sort (keys, vals) pairs of u32 by key with CUB; results in *_out.
+void sort_pairs_u32(const uint32_t* kin, uint32_t* kout, const uint32_t* vin, uint32_t* vout,
+                    uint64_t n, cudaStream_t s) {
+  TG_REQUIRE(n < (1ull << 31), TG_ECAPACITY, "sort: more than 2^31 items");
+  size_t tmp = 0;
+  TG_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)n, 0, 32, s));
+  DevBuf<uint8_t> t(tmp ? tmp : 1);
+  TG_CK(cub::DeviceRadixSort::SortPairs(t.get(), tmp, kin, kout, vin, vout, (int)n, 0, 32, s));
+}
+
+void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s) {
+  TG_REQUIRE(n < (1ull << 31), TG_ECAPACITY, "scan: more than 2^31 items");
+  size_t tmp = 0;
+  TG_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int)n, s));
+  DevBuf<uint8_t> t(tmp ? tmp : 1);
+  TG_CK(cub::DeviceScan::ExclusiveSum(t.get(), tmp, in, out, (int)n, s));
+}
+
+constexpr uint32_t kPrCta = 2048;  // in-degree at/above which a PageRank row gets a whole CTA
+
+void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
+                const uint32_t* outdeg) {
+  cudaStream_t s = eng.stream;
+  const int P = eng.P, p = pt.id;
+  const uint64_t Vp = pt.Vp;
+  DevBuf<unsigned long long> cnt(8);
+  TG_CK(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+
+  pt.global_of.alloc(std::max<uint64_t>(Vp, 1));
+  k_global_of<<<G(Vp), kB, 0, s>>>(order, Vp, p, P, outdeg, pt.global_of.get(), cnt.get() + 0);
+  TG_CK(cudaGetLastError());
+  pt.nz_end = d2h(cnt.get() + 0, s);
+
+  DevBuf<uint32_t> nloc(std::max<uint64_t>(Vp, 1)), nrem;
+  TG_CK(cudaMemsetAsync(nloc.get(), 0, nloc.bytes(), s));
+  uint64_t nremote = 0;
+  if (P > 1) {
+    nrem.alloc(std::max<uint64_t>(Vp, 1));
+    TG_CK(cudaMemsetAsync(nrem.get(), 0, nrem.bytes(), s));
+    k_count<<<G(eng.E), kB, 0, s>>>(g, eng.E, eng.rank_of.get(), P, p, nloc.get(), nrem.get(),
+                                    cnt.get() + 1);
+    TG_CK(cudaGetLastError());
+    nremote = d2h(cnt.get() + 1, s);
+  } else {
+    // single partition: every edge is local, row degree = out-degree
+    k_gather_deg<<<G(Vp), kB, 0, s>>>(pt.global_of.get(), outdeg, Vp, nloc.get());
+    TG_CK(cudaGetLastError());
+  }
+
+  // row offsets
+  {
+    DevBuf<uint64_t> deg(Vp + 1);
+    k_deg64<<<G(Vp + 1), kB, 0, s>>>(nloc.get(), P > 1 ? nrem.get() : nullptr, Vp, deg.get());
+    TG_CK(cudaGetLastError());
+    pt.row_off.alloc(Vp + 1);
+    exclusive_scan_u64(deg.get(), pt.row_off.get(), Vp + 1, s);
+  }
+  pt.Ep = d2h(pt.row_off.get() + Vp, s);
+  pt.Ep_local = pt.Ep - nremote;
+
+  // outbox slots: distinct (q, remote local id), sorted
+  DevBuf<unsigned long long> ukeys;
+  std::vector<uint64_t> ustart(P + 1, 0);
+  pt.obox_off.assign(P + 1, 0);
+  DevBuf<uint64_t> d_ustart(P + 1), d_poff(P + 1);
+  if (nremote) {
+    DevBuf<unsigned long long> keys(nremote), keys2(nremote);
+    TG_CK(cudaMemsetAsync(cnt.get() + 2, 0, sizeof(unsigned long long), s));
+    k_collect_keys<<<G(eng.E), kB, 0, s>>>(g, eng.E, eng.rank_of.get(), P, p, keys.get(),
+                                           cnt.get() + 2);
+    TG_CK(cudaGetLastError());
+    TG_REQUIRE(nremote < (1ull << 31), TG_ECAPACITY, "too many boundary edges in a partition");
+    size_t tmp = 0;
+    TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.get(), keys2.get(), (int)nremote, 0,
+                                         64, s));
+    {
+      DevBuf<uint8_t> t(tmp ? tmp : 1);
+      TG_CK(cub::DeviceRadixSort::SortKeys(t.get(), tmp, keys.get(), keys2.get(), (int)nremote, 0,
+                                           64, s));
+    }
+    // unique into keys (reuse buffer)
+    DevBuf<unsigned long long> nsel(1);
+    tmp = 0;
+    TG_CK(cub::DeviceSelect::Unique(nullptr, tmp, keys2.get(), keys.get(), nsel.get(),
+                                    (int)nremote, s));
+    {
+      DevBuf<uint8_t> t(tmp ? tmp : 1);
+      TG_CK(cub::DeviceSelect::Unique(t.get(), tmp, keys2.get(), keys.get(), nsel.get(),
+                                      (int)nremote, s));
+    }
+    pt.S_real = d2h(nsel.get(), s);
+    ukeys.alloc(pt.S_real);
+    TG_CK(cudaMemcpyAsync(ukeys.get(), keys.get(), pt.S_real * 8, cudaMemcpyDeviceToDevice, s));
+    DevBuf<unsigned long long> seg(P);
+    TG_CK(cudaMemsetAsync(seg.get(), 0, seg.bytes(), s));
+    k_seg_count<<<G(pt.S_real), kB, 0, s>>>(ukeys.get(), pt.S_real, seg.get());
+    TG_CK(cudaGetLastError());
+    std::vector<unsigned long long> hseg(P);
+    TG_CK(cudaMemcpyAsync(hseg.data(), seg.get(), P * 8, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaStreamSynchronize(s));
+    pt.seg_real.assign(hseg.begin(), hseg.end());
+    for (int q = 0; q < P; ++q) {
+      ustart[q + 1] = ustart[q] + hseg[q];
+      pt.obox_off[q + 1] = pt.obox_off[q] + ((hseg[q] + 31) / 32) * 32;
+    }
+  }
+  pt.S = pt.obox_off[P];
+  TG_CK(cudaMemcpyAsync(d_ustart.get(), ustart.data(), (P + 1) * 8, cudaMemcpyHostToDevice, s));
+  TG_CK(cudaMemcpyAsync(d_poff.get(), pt.obox_off.data(), (P + 1) * 8, cudaMemcpyHostToDevice, s));
+  pt.obox_rid.alloc(std::max<uint64_t>(pt.S, 1));
+  TG_CK(cudaMemsetAsync(pt.obox_rid.get(), 0xFF, pt.obox_rid.bytes(), s));
+  if (pt.S_real) {
+    k_place_slots<<<G(pt.S_real), kB, 0, s>>>(ukeys.get(), pt.S_real, d_ustart.get(), d_poff.get(),
+                                               pt.obox_rid.get());
+    TG_CK(cudaGetLastError());
+  }
+
+  // out-CSR fill
+  pt.col.alloc(std::max<uint64_t>(pt.Ep, 1));
+  if (eng.weighted) pt.w.alloc(std::max<uint64_t>(pt.Ep, 1));
+  {
+    DevBuf<uint32_t> cur_loc(std::max<uint64_t>(Vp, 1)), cur_rem(std::max<uint64_t>(Vp, 1));
+    TG_CK(cudaMemsetAsync(cur_loc.get(), 0, cur_loc.bytes(), s));
+    TG_CK(cudaMemsetAsync(cur_rem.get(), 0, cur_rem.bytes(), s));
+    k_fill<<<G(eng.E), kB, 0, s>>>(g, eng.E, eng.rank_of.get(), P, p, pt.row_off.get(), nloc.get(),
+                                   cur_loc.get(), cur_rem.get(), pt.col.get(), pt.w.get(),
+                                   eng.weighted, ukeys.get(), pt.S_real, d_ustart.get(),
+                                   d_poff.get());
+    TG_CK(cudaGetLastError());
+  }
+  nloc.release();
+  nrem.release();
+  ukeys.release();
+
+  // tiles
+  pt.ntiles = (pt.Ep + kTile - 1) / kTile;
+  pt.tile_vf.alloc(std::max<uint64_t>(pt.ntiles, 1));
+  pt.tile_vl.alloc(std::max<uint64_t>(pt.ntiles, 1));
+  if (pt.ntiles) {
+    k_tiles<<<G(pt.ntiles), kB, 0, s>>>(pt.row_off.get(), Vp, pt.Ep, pt.ntiles, pt.tile_vf.get(),
+                                        pt.tile_vl.get());
+    TG_CK(cudaGetLastError());
+  }
+
+  // PageRank in-CSR
+  if (eng.has_in) {
+    pt.has_in = true;
+    const uint64_t R = Vp + pt.S;
+    DevBuf<uint32_t> indeg(std::max<uint64_t>(R, 1));
+    TG_CK(cudaMemsetAsync(indeg.get(), 0, indeg.bytes(), s));
+    if (pt.Ep) {
+      k_in_count<<<G(pt.Ep), kB, 0, s>>>(pt.row_off.get(), pt.col.get(), pt.Ep, Vp,
+                                         pt.tile_vf.get(), pt.tile_vl.get(), indeg.get());
+      TG_CK(cudaGetLastError());
+    }
+    DevBuf<uint32_t> keys(std::max<uint64_t>(R, 1)), keys_out(std::max<uint64_t>(R, 1));
+    DevBuf<uint32_t> vals(std::max<uint64_t>(R, 1));
+    pt.in_local.alloc(std::max<uint64_t>(Vp, 1));
+    pt.in_pos.alloc(std::max<uint64_t>(Vp, 1));
+    pt.in_slot.alloc(std::max<uint64_t>(pt.S, 1));
+    DevBuf<uint32_t> slot_pos(std::max<uint64_t>(pt.S, 1));
+    // keys = ~indeg, vals = iota (per range)
+    k_neg_iota<<<G(Vp), kB, 0, s>>>(indeg.get(), Vp, keys.get(), vals.get());
+    if (pt.S) k_neg_iota<<<G(pt.S), kB, 0, s>>>(indeg.get() + Vp, pt.S, keys.get() + Vp, vals.get() + Vp);
+    TG_CK(cudaGetLastError());
+    if (Vp) sort_pairs_u32(keys.get(), keys_out.get(), vals.get(), pt.in_local.get(), Vp, s);
+    if (pt.S)
+      sort_pairs_u32(keys.get() + Vp, keys_out.get() + Vp, vals.get() + Vp, pt.in_slot.get(), pt.S, s);
+    k_scatter_pos<<<G(Vp), kB, 0, s>>>(pt.in_local.get(), Vp, 0, pt.in_pos.get());
+    if (pt.S) k_scatter_pos<<<G(pt.S), kB, 0, s>>>(pt.in_slot.get(), pt.S, Vp, slot_pos.get());
+    TG_CK(cudaGetLastError());
+    DevBuf<uint64_t> deg64(R + 1);
+    TG_CK(cudaMemsetAsync(deg64.get(), 0, deg64.bytes(), s));
+    DevBuf<unsigned long long> cls(4);
+    TG_CK(cudaMemsetAsync(cls.get(), 0, cls.bytes(), s));
+    k_in_deg_sorted<<<G(Vp), kB, 0, s>>>(keys_out.get(), Vp, 0, deg64.get(), cls.get(), kPrCta);
+    if (pt.S)
+      k_in_deg_sorted<<<G(pt.S), kB, 0, s>>>(keys_out.get() + Vp, pt.S, Vp, deg64.get(),
+                                             cls.get() + 2, kPrCta);
+    TG_CK(cudaGetLastError());
+    unsigned long long hc[4];
+    TG_CK(cudaMemcpyAsync(hc, cls.get(), sizeof(hc), cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaStreamSynchronize(s));
+    pt.loc_cta = hc[0];
+    pt.loc_warp = hc[1];
+    pt.box_cta = hc[2];
+    pt.box_warp = hc[3];
+    pt.in_off.alloc(R + 1);
+    exclusive_scan_u64(deg64.get(), pt.in_off.get(), R + 1, s);
+    deg64.release();
+    keys.release();
+    keys_out.release();
+    pt.in_col.alloc(std::max<uint64_t>(pt.Ep, 1));
+    TG_CK(cudaMemsetAsync(indeg.get(), 0, indeg.bytes(), s));  // reuse as cursor
+    if (pt.Ep) {
+      k_in_fill<<<G(pt.Ep), kB, 0, s>>>(pt.row_off.get(), pt.col.get(), pt.Ep, Vp, pt.tile_vf.get(),
+                                        pt.tile_vl.get(), pt.in_pos.get(), slot_pos.get(),
+                                        pt.in_off.get(), indeg.get(), pt.in_col.get());
+      TG_CK(cudaGetLastError());
+    }
+    pt.in_outdeg.alloc(std::max<uint64_t>(Vp, 1));
+    k_in_outdeg<<<G(Vp), kB, 0, s>>>(pt.row_off.get(), pt.in_local.get(), Vp, pt.in_outdeg.get());
+    TG_CK(cudaGetLastError());
+  }
+  TG_CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+void build_engine(Engine& eng, const EdgeInput& in) {
+  auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t s = eng.stream;
+  EdgeGen g{};
+  g.src = in.src;
+  g.dst = in.dst;
+  g.w = in.w;
+  g.gen = in.generated;
+  g.scale = in.scale;
+  g.scramble = in.scramble;
+  g.t = tgin_make_thresholds(in.a, in.b, in.c);
+  g.seed = in.seed;
+  g.wseed = in.wseed;
+  const uint64_t V = eng.V;
+
+  DevBuf<uint32_t> outdeg(V);
+  DevBuf<unsigned long long> bad(1);
+  TG_CK(cudaMemsetAsync(outdeg.get(), 0, outdeg.bytes(), s));
+  TG_CK(cudaMemsetAsync(bad.get(), 0, bad.bytes(), s));
+  if (eng.E) {
+    k_outdeg<<<G(eng.E), kB, 0, s>>>(g, eng.E, V, outdeg.get(), bad.get());
+    TG_CK(cudaGetLastError());
+  }
+  TG_REQUIRE(d2h(bad.get(), s) == 0, TG_EINVAL, "edge endpoint id >= V");
+
+  DevBuf<uint32_t> order(V);
+  {
+    DevBuf<uint32_t> keys(V), keys_out(V), vals(V);
+    k_neg_iota<<<G(V), kB, 0, s>>>(outdeg.get(), V, keys.get(), vals.get());
+    TG_CK(cudaGetLastError());
+    sort_pairs_u32(keys.get(), keys_out.get(), vals.get(), order.get(), V, s);
+  }
+  eng.rank_of.alloc(V);
+  k_inverse<<<G(V), kB, 0, s>>>(order.get(), V, eng.rank_of.get());
+  TG_CK(cudaGetLastError());
+
+  eng.parts.clear();
+  for (int p = 0; p < eng.P; ++p) {
+    auto pt = std::make_unique<Part>();
+    pt->id = p;
+    pt->Vp = part_size(V, p, eng.P);
+    eng.parts.push_back(std::move(pt));
+  }
+  for (auto& pt : eng.parts) build_part(eng, *pt, g, order.get(), outdeg.get());
+
+  // inboxes: q's inbox from p mirrors p's outbox segment for q
+  for (auto& qt : eng.parts) {
+    const int q = qt->id;
+    qt->ibox_off.assign(eng.P + 1, 0);
+    for (int p = 0; p < eng.P; ++p) {
+      const Part& pp = *eng.parts[p];
+      qt->ibox_off[p + 1] = qt->ibox_off[p] + (p == q ? 0 : pp.obox_off[q + 1] - pp.obox_off[q]);
+    }
+    qt->I = qt->ibox_off[eng.P];
+    qt->ibox_lid.alloc(std::max<uint64_t>(qt->I, 1));
+    for (int p = 0; p < eng.P; ++p) {
+      if (p == q) continue;
+      const Part& pp = *eng.parts[p];
+      const uint64_t n = pp.obox_off[q + 1] - pp.obox_off[q];
+      if (n)
+        TG_CK(cudaMemcpyAsync(qt->ibox_lid.get() + qt->ibox_off[p], pp.obox_rid.get() + pp.obox_off[q],
+                              n * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    if (qt->has_in) {
+      qt->ibox_inpos.alloc(std::max<uint64_t>(qt->I, 1));
+      if (qt->I) {
+        k_ibox_inpos<<<G(qt->I), kB, 0, s>>>(qt->ibox_lid.get(), qt->I, qt->in_pos.get(),
+                                             qt->ibox_inpos.get());
+        TG_CK(cudaGetLastError());
+      }
+    }
+  }
+  for (auto& pt : eng.parts) {
+    if (pt->seg_real.empty()) pt->seg_real.assign(eng.P, 0);
+  }
+  for (auto& qt : eng.parts) {
+    uint64_t real = 0;
+    for (auto& o : eng.parts)
+      if (o->id != qt->id) real += o->seg_real[qt->id];
+    qt->I_real = real;
+  }
+  TG_CK(cudaStreamSynchronize(s));
+  eng.build_ms = (uint64_t)std::chrono::duration_cast<std::chrono::milliseconds>(
+                     std::chrono::steady_clock::now() - t0)
+                     .count();
+}
+
+}  // namespace tg

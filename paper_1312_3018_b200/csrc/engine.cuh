@@ -1,0 +1,175 @@
+// engine.cuh -- device-resident partitioned graph and per-algorithm state.
+//
+// Layout (§4.3.1-4.3.2):
+//   * every partition p owns Vp vertices with dense local ids 0..Vp-1 ordered by
+//     out-degree descending (so degree classes are contiguous id ranges and
+//     zero-degree vertices form the tail [nz_end, Vp));
+//   * out-CSR row_off (u64) / col (u32): per row the LOCAL targets first, then
+//     the remote ones; a remote entry is kRemote | outbox slot (the
+//     paper's partition-tagged E entry pointing into the outbox);
+//   * outbox: one slot per distinct (p, remote vertex) pair -- the source-side
+//     reduction of P:168-182 is structural.  Slots are grouped by owner q,
+//     sorted by the owner's local id, each segment padded to a multiple of 32
+//     so bitmap words never straddle two peers;
+//   * inbox of q from p = p's outbox segment for q (symmetric): only the
+//     message arrays move between partitions;
+//   * edge tiles: the edge array is cut into tiles of kTile edges; tile t knows
+//     the first/last row it touches, so a frontier kernel is load balanced over
+//     edges whatever the degree skew (hubs span many tiles);
+//   * PageRank in-CSR in its own "in-order" index space (rows sorted by
+//     in-degree): rows [0,Vp) are local vertices, rows [Vp,Vp+S) are outbox
+//     slots (their sums are the partition's partial-sum messages).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace tg {
+
+constexpr uint32_t kTile = 2048;        // edges per frontier tile
+constexpr uint32_t kTileThreads = 512;  // CTA size of the tile kernels
+
+// Degree-aware serpentine deal (reading A23): order position i -> (part, local).
+__host__ __device__ __forceinline__ void deal(uint64_t i, int P, int* p, uint32_t* l) {
+  const uint64_t r = i / (uint64_t)P, j = i % (uint64_t)P;
+  *p = (int)((r & 1) ? (uint64_t)P - 1 - j : j);
+  *l = (uint32_t)r;
+}
+__host__ __device__ __forceinline__ uint64_t undeal(uint32_t l, int p, int P) {
+  const uint64_t j = (l & 1) ? (uint64_t)(P - 1 - p) : (uint64_t)p;
+  return (uint64_t)l * (uint64_t)P + j;
+}
+inline uint64_t part_size(uint64_t V, int p, int P) {
+  const uint64_t R = V / (uint64_t)P, rem = V % (uint64_t)P;
+  if (!rem) return R;
+  const uint64_t j = (R & 1) ? (uint64_t)(P - 1 - p) : (uint64_t)p;
+  return R + (j < rem ? 1 : 0);
+}
+
+// Per-partition tile scheduling scratch (frontier.cu)
+struct Part;
+struct TileSched {
+  DevBuf<uint32_t> bm;    // bitmap over tiles
+  DevBuf<uint32_t> list;  // compacted active tiles
+  DevBuf<unsigned long long> count;
+  uint64_t nwords = 0;
+  void ensure(const Part& p);
+};
+
+struct PRState {  // PageRank (in-order space)
+  DevBuf<float> contrib[2];
+  DevBuf<float> rank;
+  DevBuf<double> acc;
+  DevBuf<double> obox;  // partial sums per outbox slot
+  DevBuf<double> ibox;  // received partial sums
+};
+
+struct FrontierState {  // BFS / SSSP / BC-forward
+  DevBuf<uint32_t> cur, next, visited;            // bitmaps over local ids
+  DevBuf<uint32_t> vals;                          // BFS level or SSSP dist (u32, Vp)
+  DevBuf<uint32_t> obox_mark, obox_new;           // bitmaps over outbox slots
+  DevBuf<uint32_t> obox_u32;                      // SSSP min-combined distances
+  DevBuf<uint32_t> ibox_bits;                     // BFS/BC inbox bitmap
+  DevBuf<uint32_t> ibox_u32;                      // SSSP inbox distances
+  DevBuf<unsigned long long> counters;            // [0] frontier count, [1] flags
+};
+
+struct BCState {
+  DevBuf<double> sigma, dsum, c, bc;
+  DevBuf<double> obox_sigma, ibox_sigma;  // forward partial sigma sums
+  DevBuf<double> ibox_pack, ghost;        // backward pull: owner-packed c, sender's ghosts
+  std::vector<DevBuf<uint32_t>> level_bm; // frontier bitmap per level
+};
+
+struct Part {
+  int id = 0;
+  uint64_t Vp = 0, Ep = 0, Ep_local = 0;
+  uint64_t nz_end = 0;  // local ids >= nz_end have out-degree 0
+  DevBuf<uint64_t> row_off;
+  DevBuf<uint32_t> col, w, global_of;
+  // tiles
+  uint64_t ntiles = 0;
+  DevBuf<uint32_t> tile_vf, tile_vl;  // first / last row touched by tile t
+  // outbox / inbox (padded segments)
+  std::vector<uint64_t> obox_off, ibox_off;  // P+1 each (host)
+  uint64_t S = 0, I = 0;                     // padded totals
+  uint64_t S_real = 0, I_real = 0;
+  DevBuf<uint32_t> obox_rid;  // owner's local id per slot (kInf = padding)
+  DevBuf<uint32_t> ibox_lid;  // local id per inbox entry (kInf = padding)
+  // PageRank in-CSR
+  bool has_in = false;
+  DevBuf<uint64_t> in_off;          // Vp + S + 1
+  DevBuf<uint32_t> in_col;          // in-order position of the local source
+  DevBuf<uint32_t> in_local;        // in-order position -> local id (Vp)
+  DevBuf<uint32_t> in_pos;          // local id -> in-order position (Vp)
+  DevBuf<uint32_t> in_slot;         // outbox row r (0..S) -> slot
+  DevBuf<uint32_t> in_outdeg;       // out-degree of the vertex at in-position (Vp)
+  DevBuf<uint32_t> ibox_inpos;      // inbox entry -> in-order position (I)
+  uint64_t loc_cta = 0, loc_warp = 0;  // class ends of local rows
+  uint64_t box_cta = 0, box_warp = 0;  // class ends of outbox rows (relative)
+  std::vector<uint64_t> seg_real;  // real (unpadded) outbox slots per peer
+  // algorithm state (lazily allocated)
+  TileSched ts;
+  FrontierState fs;
+  PRState pr;
+  BCState bcs;
+};
+
+struct Engine {
+  int device = 0;
+  int P = 1;
+  uint64_t V = 0, E = 0;
+  bool weighted = false, has_in = false;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DevBuf<uint32_t> rank_of;  // global id -> degree-order position
+  std::vector<std::unique_ptr<Part>> parts;
+  uint64_t build_ms = 0;
+  uint64_t launches = 0;     // kernels launched by the current run
+  uint64_t comm_bytes = 0;   // message bytes exchanged by the current run
+  unsigned long long* h_counts = nullptr;  // pinned host scratch (TG_MAX_PARTITIONS * 4)
+  ~Engine();
+  uint64_t device_bytes() const;
+  // global id -> (partition, local id); one 4-byte D2H read
+  void locate(uint64_t g, int* p, uint32_t* l) const;
+};
+
+// Implemented in build.cu
+struct EdgeInput {
+  bool generated = false;
+  const uint32_t *src = nullptr, *dst = nullptr, *w = nullptr;  // device pointers
+  int scale = 0;
+  double a = 0, b = 0, c = 0;
+  uint64_t seed = 0, wseed = 0;
+  int scramble = 1;
+};
+void build_engine(Engine& eng, const EdgeInput& in);
+
+// Implemented per algorithm TU
+void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st);
+void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st);
+void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stats* st);
+void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, tg_stats* st);
+
+// Helpers shared by the algorithm TUs (api.cu)
+// Message exchange between partitions (the communication phase).
+// forward (push): p's outbox segment for q -> q's inbox segment from p.
+// reverse (pull): q's inbox segment from p -> p's outbox segment for q.
+// send/recv return the base pointer of the per-partition array; elem = bytes
+// per slot, or 0 for a bitmap (one bit per slot, segments are 32-aligned).
+using BufOf = void* (*)(Part&);
+void exchange(Engine& eng, BufOf send, BufOf recv, size_t elem, bool reverse);
+// sum of out-degrees over reached vertices (vals != INF, or visited bits);
+// *nreached (nullable) receives the number of reached vertices
+uint64_t reached_outdeg_u32(Engine& eng, uint64_t* nreached = nullptr);
+uint64_t reached_outdeg_bitmap(Engine& eng, uint64_t* nreached = nullptr);
+void collect_u32(Engine& eng, uint32_t* out, int mem);  // fs.vals -> out[global]
+void ensure_frontier_state(Engine& eng);
+// read the per-partition counters[idx] (one sync) and return their sum
+unsigned long long read_counts(Engine& eng, int idx);
+void time_begin(Engine& eng);
+double time_end(Engine& eng);  // ms since time_begin (CUDA events)
+
+}  // namespace tg

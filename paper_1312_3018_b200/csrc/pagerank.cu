@@ -1,0 +1,257 @@
+// pagerank.cu -- pull PageRank over BSP rounds (Fig. 14;
+// readings A1-A8 in DESIGN.md).  Iteration t on partition p, in the in-order
+// index space (rows sorted by in-degree, so each degree class is a contiguous
+// row range and gets its own kernel shape):
+//   pull    : sum_e contrib[in_col[e]] over the row's in-edges from LOCAL
+//             sources, accumulated in fp64 (contrib = rank/outdeg stored fp32,
+//             the paper's 4-byte rank).  Rows [Vp, Vp+S) are outbox
+//             slots: their sums are this partition's source-reduced partial
+//             sums for remote vertices ("the 'rank' sum in PageRank").
+//   P == 1  : fused finalize: rank = (1-d)/V + d*sum, next contrib = rank/outdeg.
+//   P > 1   : outbox partial sums -> owners' inboxes (full buffer),
+//             scatter-add into acc, then finalize.
+// No vote: a fixed number of rounds.
+#include "frontier.cuh"
+
+namespace tg {
+
+namespace {
+
+constexpr unsigned kCtaThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+struct PullOut {
+  bool fused;
+  uint64_t Vp;
+  double base, d;
+  double* acc;               // !fused: local rows
+  double* obox;              // outbox partial sums (slot-indexed)
+  const uint32_t* in_slot;   // outbox row -> slot
+  float* rank;               // fused
+  float* contrib_next;       // fused
+  const uint32_t* outdeg;    // fused
+  __device__ __forceinline__ void put(uint64_t r, double sum) const {
+    if (r < Vp) {
+      if (fused) {
+        const double rk = base + d * sum;
+        rank[r] = (float)rk;
+        const uint32_t od = outdeg[r];
+        contrib_next[r] = od ? (float)(rk / (double)od) : 0.0f;
+      } else {
+        acc[r] = sum;
+      }
+    } else {
+      obox[in_slot[r - Vp]] = sum;
+    }
+  }
+};
+
+// one CTA per row (in-degree >= kPrCta)
+__global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off, const uint32_t* in_col,
+                                                          const float* contrib, uint64_t r0,
+                                                          PullOut o) {
+  __shared__ double s_part[kCtaThreads / 32];
+  const uint64_t r = r0 + blockIdx.x;
+  const uint64_t b = in_off[r], e = in_off[r + 1];
+  double sum = 0.0;
+  for (uint64_t i = b + threadIdx.x; i < e; i += kCtaThreads) sum += (double)__ldg(contrib + __ldcs(in_col + i));
+  sum = warp_sum(sum);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < kCtaThreads / 32 ? s_part[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) o.put(r, v);
+  }
+}
+
+// one warp per row (32 <= in-degree < kPrCta)
+__global__ void __launch_bounds__(256) k_pull_warp(const uint64_t* in_off, const uint32_t* in_col,
+                                                   const float* contrib, uint64_t r0, uint64_t r1,
+                                                   PullOut o) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t r = r0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); r < r1;
+       r += nwarps) {
+    const uint64_t b = in_off[r], e = in_off[r + 1];
+    double sum = 0.0;
+    for (uint64_t i = b + lane; i < e; i += 32) sum += (double)__ldg(contrib + __ldcs(in_col + i));
+    sum = warp_sum(sum);
+    if (lane == 0) o.put(r, sum);
+  }
+}
+
+// one thread per row (in-degree < 32, including 0)
+__global__ void __launch_bounds__(256) k_pull_thread(const uint64_t* in_off, const uint32_t* in_col,
+                                                     const float* contrib, uint64_t r0, uint64_t r1,
+                                                     PullOut o) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < r1; r += stride) {
+    const uint64_t b = in_off[r], e = in_off[r + 1];
+    double sum = 0.0;
+    for (uint64_t i = b; i < e; ++i) sum += (double)__ldg(contrib + __ldcs(in_col + i));
+    o.put(r, sum);
+  }
+}
+
+__global__ void k_pr_init(const uint32_t* outdeg, uint64_t Vp, double r0, float* contrib, float* rank) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride) {
+    const uint32_t od = outdeg[i];
+    contrib[i] = od ? (float)(r0 / (double)od) : 0.0f;
+    rank[i] = (float)r0;
+  }
+}
+
+__global__ void k_pr_scatter(const double* msg, const uint32_t* inpos, uint64_t I, double* acc) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < I; j += stride) {
+    const uint32_t r = inpos[j];
+    if (r != kInf) atomicAdd(&acc[r], msg[j]);
+  }
+}
+
+__global__ void k_pr_finalize(const double* acc, const uint32_t* outdeg, uint64_t Vp, double base,
+                              double d, float* rank, float* contrib_next) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride) {
+    const double rk = base + d * acc[i];
+    rank[i] = (float)rk;
+    const uint32_t od = outdeg[i];
+    contrib_next[i] = od ? (float)(rk / (double)od) : 0.0f;
+  }
+}
+
+__global__ void k_pr_collect(const float* rank, const uint32_t* in_local, const uint32_t* global_of,
+                             uint64_t Vp, float* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride)
+    out[global_of[in_local[i]]] = rank[i];
+}
+
+void launch_pull_range(Engine& eng, Part& p, const float* contrib, uint64_t r0, uint64_t cta_end,
+                       uint64_t warp_end, uint64_t r1, const PullOut& o) {
+  cudaStream_t s = eng.stream;
+  if (cta_end > r0) {
+    k_pull_cta<<<(unsigned)(cta_end - r0), kCtaThreads, 0, s>>>(p.in_off.get(), p.in_col.get(),
+                                                                contrib, r0, o);
+    eng.launches++;
+  }
+  if (warp_end > cta_end) {
+    k_pull_warp<<<grid_for((warp_end - cta_end) * 32, 256, 148u * 16u), 256, 0, s>>>(
+        p.in_off.get(), p.in_col.get(), contrib, cta_end, warp_end, o);
+    eng.launches++;
+  }
+  if (r1 > warp_end) {
+    k_pull_thread<<<grid_for(r1 - warp_end, 256, 148u * 16u), 256, 0, s>>>(
+        p.in_off.get(), p.in_col.get(), contrib, warp_end, r1, o);
+    eng.launches++;
+  }
+  TG_CK(cudaGetLastError());
+}
+
+void* send_obox(Part& p) { return p.pr.obox.get(); }
+void* recv_ibox(Part& p) { return p.pr.ibox.get(); }
+
+}  // namespace
+
+void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stats* st) {
+  TG_REQUIRE(iters >= 1, TG_EINVAL, "tg_pagerank: iterations must be >= 1");
+  TG_REQUIRE(eng.has_in, TG_EINVAL, "tg_pagerank: engine built without the in-CSR");
+  TG_REQUIRE(out != nullptr, TG_EINVAL, "tg_pagerank: NULL output");
+  cudaStream_t s = eng.stream;
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    PRState& r = p.pr;
+    const uint64_t Vn = std::max<uint64_t>(p.Vp, 1);
+    if (r.rank.n < Vn) {
+      r.contrib[0].alloc(Vn);
+      r.contrib[1].alloc(Vn);
+      r.rank.alloc(Vn);
+      if (eng.P > 1) {
+        r.acc.alloc(Vn);
+        r.obox.alloc(std::max<uint64_t>(p.S, 1));
+        r.ibox.alloc(std::max<uint64_t>(p.I, 1));
+      }
+    }
+  }
+  eng.launches = 0;
+  eng.comm_bytes = 0;
+  const double base = (1.0 - d) / (double)eng.V, r0 = 1.0 / (double)eng.V;
+  time_begin(eng);
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    if (!p.Vp) continue;
+    k_pr_init<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.in_outdeg.get(), p.Vp, r0, p.pr.contrib[0].get(),
+                                                  p.pr.rank.get());
+    eng.launches++;
+  }
+  int cur = 0;
+  for (int it = 0; it < iters; ++it) {
+    for (auto& pp : eng.parts) {
+      Part& p = *pp;
+      PRState& r = p.pr;
+      PullOut o{eng.P == 1, p.Vp, base, d, r.acc.get(), r.obox.get(), p.in_slot.get(), r.rank.get(),
+                r.contrib[cur ^ 1].get(), p.in_outdeg.get()};
+      launch_pull_range(eng, p, r.contrib[cur].get(), 0, p.loc_cta, p.loc_warp, p.Vp, o);
+      if (p.S)
+        launch_pull_range(eng, p, r.contrib[cur].get(), p.Vp, p.Vp + p.box_cta, p.Vp + p.box_warp,
+                          p.Vp + p.S, o);
+    }
+    if (eng.P > 1) {
+      exchange(eng, send_obox, recv_ibox, 8, false);
+      for (auto& pp : eng.parts) {
+        Part& p = *pp;
+        PRState& r = p.pr;
+        if (p.I) {
+          k_pr_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(r.ibox.get(), p.ibox_inpos.get(), p.I,
+                                                          r.acc.get());
+          eng.launches++;
+        }
+        if (p.Vp) {
+          k_pr_finalize<<<grid_for(p.Vp, 256), 256, 0, s>>>(r.acc.get(), p.in_outdeg.get(), p.Vp,
+                                                            base, d, r.rank.get(),
+                                                            r.contrib[cur ^ 1].get());
+          eng.launches++;
+        }
+        TG_CK(cudaGetLastError());
+      }
+    }
+    cur ^= 1;
+  }
+  const double ms = time_end(eng);
+  if (st) {
+    st->device_ms = ms;
+    st->supersteps = (uint64_t)iters;
+    st->traversed_edges = eng.E * (uint64_t)iters;
+    // per iteration: 8 B per edge (in_col + contrib gather) + 20 B per vertex
+    // (in_off 8, outdeg 4, rank 4, contrib 4) -- DESIGN.md "Roofline"
+    st->algorithmic_bytes = (8 * eng.E + 20 * eng.V) * (uint64_t)iters;
+    st->comm_bytes = eng.comm_bytes;
+    st->launches = eng.launches;
+  }
+  // collect rank -> out[global]
+  float* dout = out;
+  DevBuf<float> tmp;
+  if (mem == TG_MEM_HOST) {
+    tmp.alloc(eng.V);
+    dout = tmp.get();
+  }
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    if (!p.Vp) continue;
+    k_pr_collect<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.pr.rank.get(), p.in_local.get(),
+                                                     p.global_of.get(), p.Vp, dout);
+  }
+  TG_CK(cudaGetLastError());
+  if (mem == TG_MEM_HOST)
+    TG_CK(cudaMemcpyAsync(out, dout, eng.V * sizeof(float), cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+}
+
+}  // namespace tg

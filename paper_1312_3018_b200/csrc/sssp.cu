@@ -1,0 +1,147 @@
+// sssp.cu -- Bellman-Ford SSSP over BSP supersteps (Fig. 20).
+// Per superstep and partition:
+//   compute : every edge (v,t,w) of an active v: nd = dist[v] + w; local t:
+//             atomicMin(dist[t], nd) and activate t on improvement (Fig. 20
+//             lines 7-12); remote t: atomicMin into its outbox slot (the
+//             min-combiner of P:182).  nd is formed in 64 bits; a value that
+//             does not fit u32 raises the overflow flag (TG_EINTERNAL).
+//   communicate: the full outbox value array (full buffer every
+//             superstep; min-combine makes re-sending idempotent).
+//   scatter : dist[v] = min(dist[v], msg), activate on improvement.
+//   advance : next-active bitmap -> vote count.
+// The paper's same-superstep re-activation changes the number of
+// supersteps, never the fixed point; it is not used here (A19).
+#include "frontier.cuh"
+
+namespace tg {
+
+namespace {
+
+struct SsspOp {
+  using Aux = uint32_t;
+  static constexpr bool kReduce = false;
+  const uint32_t* col;
+  const uint32_t* w;
+  uint32_t* dist;
+  uint32_t* next;
+  uint32_t* obox;
+  unsigned long long* overflow;
+  __device__ __forceinline__ Aux aux(uint32_t v) const { return dist[v]; }
+  __device__ __forceinline__ void edge(uint32_t, const Aux& dv, uint64_t e) const {
+    const uint32_t t = __ldcs(col + e);
+    const uint64_t nd64 = (uint64_t)dv + __ldcs(w + e);
+    if (nd64 >= (uint64_t)kInf) {
+      *overflow = 1ull;
+      return;
+    }
+    const uint32_t nd = (uint32_t)nd64;
+    if (t & kRemote) {
+      const uint32_t s = t & ~kRemote;
+      if (nd < obox[s]) atomicMin(&obox[s], nd);
+    } else if (nd < dist[t]) {
+      const uint32_t old = atomicMin(&dist[t], nd);
+      if (nd < old) {
+        const uint32_t m = 1u << (t & 31);
+        if (!(next[t >> 5] & m)) atomicOr(&next[t >> 5], m);
+      }
+    }
+  }
+};
+
+__global__ void k_sssp_scatter(const uint32_t* msg, const uint32_t* lid, uint64_t I, uint32_t* dist,
+                               uint32_t* next) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < I; j += stride) {
+    const uint32_t m = msg[j];
+    if (m == kInf) continue;
+    const uint32_t v = lid[j];
+    if (m < dist[v]) {
+      const uint32_t old = atomicMin(&dist[v], m);
+      if (m < old) bit_set_atomic(next, v);
+    }
+  }
+}
+
+void* send_obox(Part& p) { return p.fs.obox_u32.get(); }
+void* recv_ibox(Part& p) { return p.fs.ibox_u32.get(); }
+
+}  // namespace
+
+void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st) {
+  TG_REQUIRE(eng.weighted, TG_EINVAL, "tg_sssp: engine was built without edge weights");
+  int ps;
+  uint32_t ls;
+  eng.locate(source, &ps, &ls);
+  ensure_frontier_state(eng);
+  eng.launches = 0;
+  eng.comm_bytes = 0;
+  cudaStream_t s = eng.stream;
+  time_begin(eng);
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
+    FrontierState& f = p.fs;
+    const uint64_t nw = words_for(p.Vp);
+    TG_CK(cudaMemsetAsync(f.vals.get(), 0xFF, p.Vp * 4, s));
+    TG_CK(cudaMemsetAsync(f.cur.get(), 0, nw * 4, s));
+    TG_CK(cudaMemsetAsync(f.next.get(), 0, nw * 4, s));
+    if (p.S) TG_CK(cudaMemsetAsync(f.obox_u32.get(), 0xFF, p.S * 4, s));
+    TG_CK(cudaMemsetAsync(f.counters.get(), 0, f.counters.bytes(), s));
+    if (p.id == ps) {
+      k_seed<<<1, 1, 0, s>>>(f.next.get(), ls, f.vals.get(), 0);
+      eng.launches++;
+    }
+    launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get(),
+                   f.counters.get() + 2);
+    std::swap(f.cur, f.next);
+  }
+  uint64_t supersteps = 0;
+  for (;;) {
+    for (auto& pp : eng.parts) {
+      Part& p = *pp;
+      FrontierState& f = p.fs;
+      launch_compact(eng, p.ts);
+      SsspOp op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
+                f.counters.get() + 1};
+      launch_expand(eng, p, p.ts, f.cur.get(), op);
+    }
+    supersteps++;
+    if (eng.P > 1) {
+      exchange(eng, send_obox, recv_ibox, 4, false);
+      for (auto& pp : eng.parts) {
+        Part& p = *pp;
+        if (!p.I) continue;
+        k_sssp_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(p.fs.ibox_u32.get(), p.ibox_lid.get(), p.I,
+                                                          p.fs.vals.get(), p.fs.next.get());
+        TG_CK(cudaGetLastError());
+        eng.launches++;
+      }
+    }
+    for (auto& pp : eng.parts) {
+      Part& p = *pp;
+      FrontierState& f = p.fs;
+      TG_CK(cudaMemsetAsync(f.counters.get(), 0, 8, s));
+      launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get(),
+                     f.counters.get() + 2);
+      std::swap(f.cur, f.next);
+    }
+    if (read_counts(eng, 0) == 0) break;
+    TG_REQUIRE(supersteps <= eng.V + 1, TG_EINTERNAL, "tg_sssp: superstep bound exceeded");
+  }
+  const double ms = time_end(eng);
+  TG_REQUIRE(read_counts(eng, 1) == 0, TG_EINTERNAL, "tg_sssp: distance overflows uint32");
+  if (st) {
+    uint64_t nreached = 0;
+    st->device_ms = ms;
+    st->supersteps = supersteps;
+    st->traversed_edges = reached_outdeg_u32(eng, &nreached);
+    // relaxed edges R = sum of out-degrees of every activation (counters[2]):
+    // 12 B per relaxation (col + w + dist probe), 20 B per activation row.
+    const uint64_t R = read_counts(eng, 2);
+    st->algorithmic_bytes = 12 * R + 20 * nreached;
+    st->comm_bytes = eng.comm_bytes;
+    st->launches = eng.launches;
+  }
+  collect_u32(eng, out, mem);
+}
+
+}  // namespace tg

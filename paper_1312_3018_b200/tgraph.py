@@ -1,0 +1,243 @@
+"""ctypes binding of libtgraph.so -- same names as include/tgraph.h.
+
+Arrays: numpy arrays are host memory (TG_MEM_HOST); torch CUDA tensors are
+device memory (TG_MEM_DEVICE, passed by data_ptr()).  Nothing here computes:
+each function marshals arguments, calls the C ABI and raises TGraphError on a
+non-zero status with tg_last_error().
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtgraph.so")
+
+TG_OK, TG_EINVAL, TG_ECAPACITY, TG_EIO, TG_EINTERNAL, TG_ECUDA, TG_ENCCL = 0, 2, 3, 4, 5, 6, 7
+TG_MEM_HOST, TG_MEM_DEVICE = 0, 1
+TG_INF32 = 0xFFFFFFFF
+
+
+class TGraphError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[tg status {code}] {msg}")
+        self.code = code
+
+
+class tg_attr(C.Structure):
+    _fields_ = [("num_partitions", C.c_int), ("device", C.c_int), ("weighted", C.c_int),
+                ("build_in_csr", C.c_int), ("reserved", C.c_int * 4)]
+
+
+class tg_info(C.Structure):
+    _fields_ = [("V", C.c_uint64), ("E", C.c_uint64), ("num_partitions", C.c_int),
+                ("weighted", C.c_int), ("has_in_csr", C.c_int), ("device_bytes", C.c_uint64),
+                ("build_ms", C.c_uint64)]
+
+
+class tg_part_info(C.Structure):
+    _fields_ = [("Vp", C.c_uint64), ("Ep", C.c_uint64), ("Ep_local", C.c_uint64),
+                ("outbox_slots", C.c_uint64), ("inbox_slots", C.c_uint64)]
+
+
+class tg_stats(C.Structure):
+    _fields_ = [("device_ms", C.c_double), ("supersteps", C.c_uint64),
+                ("traversed_edges", C.c_uint64), ("algorithmic_bytes", C.c_uint64),
+                ("comm_bytes", C.c_uint64), ("launches", C.c_uint64)]
+
+
+@dataclass
+class Stats:
+    device_ms: float
+    supersteps: int
+    traversed_edges: int
+    algorithmic_bytes: int
+    comm_bytes: int
+    launches: int
+
+    @staticmethod
+    def of(s: tg_stats) -> "Stats":
+        return Stats(s.device_ms, s.supersteps, s.traversed_edges, s.algorithmic_bytes,
+                     s.comm_bytes, s.launches)
+
+
+_LIB = None
+
+
+def lib():
+    """Load libtgraph.so (built in-tree by __graft_entry__.build())."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                              "g.build()'` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        p, u64, i32, dbl = C.c_void_p, C.c_uint64, C.c_int, C.c_double
+        L.tg_version.restype = C.c_char_p
+        L.tg_last_error.restype = C.c_char_p
+        L.tg_engine_create_edges.argtypes = [u64, u64, p, p, p, i32, C.POINTER(tg_attr), C.POINTER(p)]
+        L.tg_engine_create_rmat.argtypes = [i32, i32, dbl, dbl, dbl, u64, i32, u64,
+                                            C.POINTER(tg_attr), C.POINTER(p)]
+        L.tg_engine_free.argtypes = [p]
+        L.tg_engine_free.restype = None
+        L.tg_engine_info.argtypes = [p, C.POINTER(tg_info)]
+        L.tg_engine_partition_info.argtypes = [p, i32, C.POINTER(tg_part_info), p]
+        L.tg_bfs.argtypes = [p, u64, p, i32, C.POINTER(tg_stats)]
+        L.tg_sssp.argtypes = [p, u64, p, i32, C.POINTER(tg_stats)]
+        L.tg_pagerank.argtypes = [p, i32, dbl, p, i32, C.POINTER(tg_stats)]
+        L.tg_bc.argtypes = [p, p, i32, p, i32, C.POINTER(tg_stats)]
+        for f in ("tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
+                  "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc"):
+            getattr(L, f).restype = i32
+        _LIB = L
+    return _LIB
+
+
+def _check(rc: int) -> None:
+    if rc != TG_OK:
+        raise TGraphError(rc, lib().tg_last_error().decode())
+
+
+def _arr(a, dtype):
+    """-> (pointer, mem kind, keepalive)."""
+    if a is None:
+        return None, TG_MEM_HOST, None
+    if hasattr(a, "data_ptr") and getattr(a, "is_cuda", False):
+        return C.c_void_p(a.data_ptr()), TG_MEM_DEVICE, a
+    arr = np.ascontiguousarray(a, dtype)
+    return arr.ctypes.data_as(C.c_void_p), TG_MEM_HOST, arr
+
+
+def _attr(partitions, device, weighted, in_csr) -> tg_attr:
+    at = tg_attr()
+    at.num_partitions, at.device, at.weighted, at.build_in_csr = partitions, device, int(weighted), int(in_csr)
+    return at
+
+
+def tg_engine_create_edges(V, src, dst, w=None, partitions=1, device=0, weighted=None, in_csr=True):
+    ps, ms, k1 = _arr(src, np.uint32)
+    pd, md, k2 = _arr(dst, np.uint32)
+    pw, mw, k3 = _arr(w, np.uint32)
+    E = len(src)
+    if E and ms != md:
+        raise ValueError("src and dst must live in the same memory")
+    if weighted is None:
+        weighted = w is not None
+    at = _attr(partitions, device, weighted, in_csr)
+    h = C.c_void_p()
+    _check(lib().tg_engine_create_edges(V, E, ps, pd, pw, ms, C.byref(at), C.byref(h)))
+    return h
+
+
+def tg_engine_create_rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, scramble=True,
+                          wseed=2, partitions=1, device=0, weighted=True, in_csr=True):
+    at = _attr(partitions, device, weighted, in_csr)
+    h = C.c_void_p()
+    _check(lib().tg_engine_create_rmat(scale, edge_factor, a, b, c, seed, int(scramble), wseed,
+                                       C.byref(at), C.byref(h)))
+    return h
+
+
+def tg_engine_free(h) -> None:
+    lib().tg_engine_free(h)
+
+
+def tg_engine_info(h) -> dict:
+    i = tg_info()
+    _check(lib().tg_engine_info(h, C.byref(i)))
+    return {f: getattr(i, f) for f, _ in tg_info._fields_}
+
+
+def tg_engine_partition_info(h, p: int, P: int) -> dict:
+    i = tg_part_info()
+    slots = np.zeros(P, np.uint64)
+    _check(lib().tg_engine_partition_info(h, p, C.byref(i), slots.ctypes.data_as(C.c_void_p)))
+    d = {f: getattr(i, f) for f, _ in tg_part_info._fields_}
+    d["slots_to"] = slots
+    return d
+
+
+def _out(out, V, dtype):
+    if out is None:
+        out = np.empty(V, dtype)
+    ptr, mem, keep = _arr(out, dtype) if not isinstance(out, np.ndarray) else (
+        out.ctypes.data_as(C.c_void_p), TG_MEM_HOST, out)
+    if isinstance(out, np.ndarray) and (out.dtype != dtype or not out.flags.c_contiguous or len(out) < V):
+        raise ValueError(f"output must be a contiguous {dtype} array of length >= V")
+    return out, ptr, mem
+
+
+def tg_bfs(h, V, source, out=None):
+    out, ptr, mem = _out(out, V, np.uint32)
+    st = tg_stats()
+    _check(lib().tg_bfs(h, source, ptr, mem, C.byref(st)))
+    return out, Stats.of(st)
+
+
+def tg_sssp(h, V, source, out=None):
+    out, ptr, mem = _out(out, V, np.uint32)
+    st = tg_stats()
+    _check(lib().tg_sssp(h, source, ptr, mem, C.byref(st)))
+    return out, Stats.of(st)
+
+
+def tg_pagerank(h, V, iterations=5, damping=0.85, out=None):
+    out, ptr, mem = _out(out, V, np.float32)
+    st = tg_stats()
+    _check(lib().tg_pagerank(h, iterations, damping, ptr, mem, C.byref(st)))
+    return out, Stats.of(st)
+
+
+def tg_bc(h, V, sources, out=None):
+    out, ptr, mem = _out(out, V, np.float64)
+    s = np.ascontiguousarray(sources, np.uint64)
+    st = tg_stats()
+    _check(lib().tg_bc(h, s.ctypes.data_as(C.c_void_p), len(s), ptr, mem, C.byref(st)))
+    return out, Stats.of(st)
+
+
+class Engine:
+    """Owning handle: a partitioned, device-resident graph."""
+
+    def __init__(self, handle):
+        self.h = handle
+        inf = tg_engine_info(handle)
+        self.V, self.E, self.P = inf["V"], inf["E"], inf["num_partitions"]
+        self.info = inf
+
+    @classmethod
+    def from_edges(cls, V, src, dst, w=None, **kw) -> "Engine":
+        return cls(tg_engine_create_edges(V, src, dst, w, **kw))
+
+    @classmethod
+    def rmat(cls, scale, **kw) -> "Engine":
+        return cls(tg_engine_create_rmat(scale, **kw))
+
+    def close(self):
+        if self.h:
+            tg_engine_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def partition_info(self, p):
+        return tg_engine_partition_info(self.h, p, self.P)
+
+    def bfs(self, source, out=None):
+        return tg_bfs(self.h, self.V, source, out)
+
+    def sssp(self, source, out=None):
+        return tg_sssp(self.h, self.V, source, out)
+
+    def pagerank(self, iterations=5, damping=0.85, out=None):
+        return tg_pagerank(self.h, self.V, iterations, damping, out)
+
+    def bc(self, sources, out=None):
+        return tg_bc(self.h, self.V, sources, out)

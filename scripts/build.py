@@ -76,7 +76,7 @@ def build_tgraph(force: bool = False) -> str:
            "-Xptxas", "-v", "--expt-relaxed-constexpr",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(ROOT, "inputs"),
            "-o", TGRAPH_SO, *cu]
-    if inc:
+    if inc and os.environ.get("TG_WITH_NCCL"):
         cmd += ["-DTG_HAVE_NCCL=1", "-I", inc, "-L", lib, "-l:libnccl.so.2",
                 "-Xlinker", "-rpath=" + lib]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True)

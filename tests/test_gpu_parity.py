@@ -1,0 +1,254 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bars (BASELINE.json north_star): BFS levels and SSSP
+distances bit-exact; PageRank within 1e-5 relative per vertex; BC within 1e-4
+relative per vertex."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+PR_RTOL = 1e-5
+BC_RTOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def tg():
+    import paper_1312_3018_b200 as tg
+
+    tg.lib()
+    return tg
+
+
+def assert_pr(gpu, ref):
+    rel = np.abs(gpu.astype(np.float64) - ref) / np.abs(ref)
+    assert rel.max() <= PR_RTOL, f"PageRank max rel err {rel.max():.3e} at {rel.argmax()}"
+
+
+def assert_bc(gpu, ref):
+    scale = max(1.0, float(np.abs(ref).max()))
+    err = np.abs(gpu - ref)
+    ok = err <= BC_RTOL * np.abs(ref) + 1e-12 * scale
+    assert ok.all(), f"BC mismatch at {np.where(~ok)[0][:5]}: {gpu[~ok][:5]} vs {ref[~ok][:5]}"
+
+
+def both(tg, V, src, dst, w=None, P=1):
+    G = oracle.Graph(V, src, dst, w)
+    eng = tg.Engine.from_edges(V, np.asarray(src, np.uint32), np.asarray(dst, np.uint32),
+                               None if w is None else np.asarray(w, np.uint32), partitions=P,
+                               weighted=w is not None)
+    return G, eng
+
+
+def check_all(tg, G, eng, bfs_src=(), sssp_src=(), pr_T=(5,), bc_src=()):
+    for s in bfs_src:
+        lv, st = eng.bfs(int(s))
+        assert np.array_equal(lv, G.bfs(int(s))), f"BFS mismatch from {s}"
+    for s in sssp_src:
+        d, _ = eng.sssp(int(s))
+        assert np.array_equal(d, G.sssp(int(s))), f"SSSP mismatch from {s}"
+    for T in pr_T:
+        r, _ = eng.pagerank(T)
+        assert_pr(r, G.pagerank(T))
+    if len(bc_src):
+        b, _ = eng.bc(np.asarray(bc_src, np.uint64))
+        assert_bc(b, G.bc(bc_src))
+
+
+# ------------------------------------------------------------ SPEC worked examples
+@pytest.mark.parametrize("P", [1, 2])
+def test_golden(tg, P):
+    g = GOLD["bfs_path_split"]
+    G, eng = both(tg, g["V"], g["src"], g["dst"], P=P)
+    assert eng.bfs(g["source"])[0].tolist() == g["levels"], g["cite"]
+    g = GOLD["bfs_isolated_source"]
+    G, eng = both(tg, g["V"], g["src"], g["dst"], P=P)
+    assert eng.bfs(g["source"])[0].tolist() == g["levels"], g["cite"]
+    g = GOLD["sssp_triangle"]
+    G, eng = both(tg, g["V"], g["src"], g["dst"], g["w"], P=P)
+    assert eng.sssp(g["source"])[0].tolist() == g["dist"], g["cite"]
+    g = GOLD["pagerank_two_cycle"]
+    G, eng = both(tg, g["V"], g["src"], g["dst"], P=P)
+    assert np.allclose(eng.pagerank(g["T"], g["d"])[0], g["rank"], rtol=1e-6), g["cite"]
+    g = GOLD["bc_undirected_path"]
+    G, eng = both(tg, g["V"], g["src"], g["dst"], P=P)
+    assert np.allclose(eng.bc(g["sources"])[0], g["bc"], rtol=1e-12), g["cite"]
+    if P == 1:
+        g = GOLD["pagerank_isolated"]
+        G, eng = both(tg, g["V"], g["src"], g["dst"], P=P)
+        assert np.allclose(eng.pagerank(g["T"], g["d"])[0], g["rank"], rtol=1e-6), g["cite"]
+
+
+# ------------------------------------------------------------ C1: RMAT-10, 2 partitions
+def test_c1_rmat10_two_partitions(tg):
+    scale = 10
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    eng_dev = tg.Engine.rmat(scale, partitions=2)             # edges generated on the device
+    eng_up = tg.Engine.from_edges(V, src, dst, w, partitions=2)  # uploaded host edges
+    deg = G.out_degree()
+    sources = np.where(deg > 0)[0]
+    for eng in (eng_dev, eng_up):
+        for s in sources:                       # every source with out-degree >= 1 (8(d) C1)
+            assert np.array_equal(eng.bfs(int(s))[0], G.bfs(int(s))), s
+        for T in (5, 20):
+            assert_pr(eng.pagerank(T)[0], G.pagerank(T))
+        for s in sources[::64]:
+            assert np.array_equal(eng.sssp(int(s))[0], G.sssp(int(s)))
+        bs = inputs.list_sources(src, 4)
+        assert_bc(eng.bc(bs)[0], G.bc(bs))
+
+
+def test_c1_partition_layout_matches_oracle(tg):
+    """Structural parity of the partitioner: per-partition |V_p| and the
+    source-reduced outbox sizes equal the oracle's degree partition + beta."""
+    scale = 10
+    src, dst, _ = inputs.rmat_edges(scale)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst)
+    for P in (2, 3, 4):
+        part, _ = G.partition(P)
+        br, bd, slots = oracle.beta(V, src, dst, part, P)
+        eng = tg.Engine.from_edges(V, src, dst, partitions=P)
+        tot_slots = 0
+        for p in range(P):
+            pi = eng.partition_info(p)
+            assert pi["Vp"] == int((part == p).sum())
+            assert pi["Ep"] == int((part[src] == p).sum())
+            assert pi["Ep_local"] == int(((part[src] == p) & (part[dst] == p)).sum())
+            assert np.array_equal(pi["slots_to"], slots[p]), (P, p)
+            assert pi["inbox_slots"] == int(slots[:, p].sum())
+            tot_slots += pi["outbox_slots"]
+        assert np.isclose(tot_slots / len(src), bd)
+
+
+# ------------------------------------------------------------ partition invariance
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_partition_invariance_rmat12(tg, P):
+    scale = 12
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    eng = tg.Engine.from_edges(V, src, dst, w, partitions=P)
+    srcs = inputs.list_sources(src, 6)
+    check_all(tg, G, eng, bfs_src=srcs, sssp_src=srcs[:3], pr_T=(5,), bc_src=srcs[:4])
+
+
+# ------------------------------------------------------------ adversarial shapes
+@pytest.mark.parametrize("P", [1, 2])
+def test_hub_of_degree_2_20(tg, P):
+    k = 1 << 20
+    V = k + 2
+    src = np.concatenate([np.zeros(k, np.uint32), np.arange(1, 200, dtype=np.uint32)])
+    dst = np.concatenate([np.arange(1, k + 1, dtype=np.uint32), np.full(199, k + 1, np.uint32)])
+    w = (np.arange(len(src)) % 63 + 1).astype(np.uint32)
+    G, eng = both(tg, V, src, dst, w, P)
+    check_all(tg, G, eng, bfs_src=[0, 5], sssp_src=[0], pr_T=(3,), bc_src=[0, 7])
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_long_path_many_supersteps(tg, P):
+    n = 3000
+    src = np.arange(n - 1, dtype=np.uint32)
+    dst = src + 1
+    w = np.full(n - 1, 63, np.uint32)
+    G, eng = both(tg, n, src, dst, w, P)
+    lv, st = eng.bfs(0)
+    assert st.supersteps == n and np.array_equal(lv, G.bfs(0))
+    check_all(tg, G, eng, sssp_src=[0, 1500], pr_T=(4,), bc_src=[0, 10])
+
+
+@pytest.mark.parametrize("P", [1, 2])
+def test_multigraph_selfloops_disconnected_isolated(tg, P):
+    rng = np.random.default_rng(11)
+    n = 5000
+    src = rng.integers(0, n // 2, 40000).astype(np.uint32)   # upper half: isolated vertices
+    dst = rng.integers(0, n // 2, 40000).astype(np.uint32)
+    src = np.concatenate([src, src[:5000], np.arange(100, dtype=np.uint32)])  # duplicates
+    dst = np.concatenate([dst, dst[:5000], np.arange(100, dtype=np.uint32)])  # + self loops
+    w = rng.integers(1, 64, len(src)).astype(np.uint32)
+    G, eng = both(tg, n, src, dst, w, P)
+    check_all(tg, G, eng, bfs_src=[0, 3, n - 1], sssp_src=[0, n - 1], pr_T=(5,),
+              bc_src=[0, 1, n - 1])
+
+
+def test_uniform_degree_cycle_and_empty_graph(tg):
+    n = 10007
+    src = np.arange(n, dtype=np.uint32)
+    dst = ((src.astype(np.int64) * 7 + 1) % n).astype(np.uint32)
+    G, eng = both(tg, n, src, dst, np.ones(n, np.uint32), 2)
+    check_all(tg, G, eng, bfs_src=[0], sssp_src=[5], pr_T=(5,), bc_src=[0])
+    G, eng = both(tg, 7, [], [], None, 1)
+    lv, _ = eng.bfs(3)
+    assert lv.tolist() == [0xFFFFFFFF] * 3 + [0] + [0xFFFFFFFF] * 3
+    r, _ = eng.pagerank(2)
+    assert np.allclose(r, 0.15 / 7, rtol=1e-6)
+
+
+def test_errors(tg):
+    src, dst, _ = inputs.rmat_edges(8)
+    eng = tg.Engine.from_edges(256, src, dst)
+    with pytest.raises(tg.TGraphError) as e:
+        eng.bfs(256)                       # source >= V
+    assert e.value.code == 2
+    with pytest.raises(tg.TGraphError) as e:
+        eng.sssp(0)                        # unweighted engine
+    assert e.value.code == 2
+    with pytest.raises(tg.TGraphError) as e:
+        eng.pagerank(0)                    # iterations < 1
+    assert e.value.code == 2
+    with pytest.raises(tg.TGraphError):
+        tg.Engine.from_edges(10, [0, 11], [1, 2])  # id >= V
+
+
+def test_device_outputs(tg):
+    import torch
+
+    scale = 10
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    eng = tg.Engine.rmat(scale)
+    s = int(inputs.rmat_sources(scale, 1)[0])
+    lv = torch.empty(V, dtype=torch.int32, device="cuda")
+    eng.bfs(s, out=lv)
+    assert np.array_equal(lv.cpu().numpy().view(np.uint32), G.bfs(s))
+    r = torch.empty(V, dtype=torch.float32, device="cuda")
+    eng.pagerank(5, out=r)
+    assert_pr(r.cpu().numpy(), G.pagerank(5))
+
+
+# ------------------------------------------------------------ C2: RMAT-22, 1 GPU
+@pytest.fixture(scope="module")
+def c2(tg):
+    scale = 22
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    G = oracle.Graph(1 << scale, src, dst, w)
+    del src, dst, w
+    eng = tg.Engine.rmat(scale)          # device-side generation of the same stream
+    return scale, G, eng
+
+
+def test_c2_bfs_sssp(c2):
+    scale, G, eng = c2
+    srcs = inputs.rmat_sources(scale, 8)
+    for s in srcs:
+        lv, st = eng.bfs(int(s))
+        assert np.array_equal(lv, G.bfs(int(s))), s
+        assert st.traversed_edges == int(G.out_degree()[lv != 0xFFFFFFFF].sum())
+    for s in srcs[:3]:
+        assert np.array_equal(eng.sssp(int(s))[0], G.sssp(int(s))), s
+
+
+def test_c2_pagerank_bc(c2):
+    scale, G, eng = c2
+    assert_pr(eng.pagerank(5)[0], G.pagerank(5))
+    bs = inputs.rmat_sources(scale, 2)
+    assert_bc(eng.bc(bs)[0], G.bc(bs))
