@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""bench.py -- the TOTEM BSP superstep hot path on B200 (BASELINE.json metric).
+
+One "step" = one pass of every hot-path row of SURVEY.md 8(a) over the
+resident RMAT graph: BFS from source j, Bellman-Ford SSSP from source j,
+PageRank (5 Jacobi rounds, the paper's Fig. 16 protocol) and Brandes BC from
+source j.  The workload at N=1 is RMAT-28 (edge factor 16, 2^32 edges), the
+configuration BASELINE.json's metric is quoted on; it fits one B200.
+
+value  = traversed edges of the whole step (the paper's TEPS numerators,
+         PAPER.md:336: BFS/SSSP sum of reached out-degrees, BC 2x that,
+         PageRank |E| per round) / device time of the step, in GTEPS,
+         outputs written to device memory.  Device time = sum of the CUDA-event
+         intervals the library records on its own stream around each algorithm
+         (state init .. final vote), bracketed by barrier + synchronize.
+e2e    = same metric through the same C-ABI calls with HOST output buffers
+         (pinned), device->host copies of every result inside the timed region.
+roofline = the dominant kernel from the library's CUDA-event kernel ledger.
+cpu_baseline = the CPU oracle (single thread) on a bounded RMAT-22 sample.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BFS/SSSP/BC GTEPS and PageRank edges/s/iter, RMAT-28 at 1/2/4/8 B200"
+UNIT = "GTEPS"
+PR_ITERS = 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tgraph", choices=["tgraph", "reference"])
+    ap.add_argument("--scale", type=int, default=28)
+    ap.add_argument("--cpu-scale", type=int, default=22, help="RMAT scale of the oracle sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--out", default=None, help="also write the JSON line to this file")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes per kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        return json.load(open(p))
+    return {}
+
+
+# ----------------------------------------------------------------- oracle legs
+def oracle_sample(scale: int, n_src: int = 1, reps_bfs: int = 2):
+    """The CPU oracle, as it stands, on an RMAT sample of the same family.
+    Returns (traversed_edges, seconds, description)."""
+    import inputs
+    import oracle
+
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    G = oracle.Graph(1 << scale, src, dst, w)
+    deg = G.out_degree()
+    srcs = inputs.rmat_sources(scale, max(n_src, reps_bfs))
+    total_e, total_s = 0, 0.0
+    for s in srcs[:reps_bfs]:
+        t0 = time.perf_counter()
+        lv = G.bfs(int(s))
+        total_s += time.perf_counter() - t0
+        total_e += int(deg[lv != 0xFFFFFFFF].sum())
+    for s in srcs[:n_src]:
+        t0 = time.perf_counter()
+        d = G.sssp(int(s))
+        total_s += time.perf_counter() - t0
+        total_e += int(deg[d != 0xFFFFFFFF].sum())
+    t0 = time.perf_counter()
+    G.pagerank(PR_ITERS)
+    total_s += time.perf_counter() - t0
+    total_e += G.E * PR_ITERS
+    for s in srcs[:n_src]:
+        lv = G.bfs(int(s))
+        t0 = time.perf_counter()
+        G.bc([int(s)])
+        total_s += time.perf_counter() - t0
+        total_e += 2 * int(deg[lv != 0xFFFFFFFF].sum())
+    desc = (f"oracle/oracle.c single-threaded on RMAT-{scale} (same generator, edge factor 16): "
+            f"BFS x{reps_bfs}, SSSP x{n_src}, PageRank {PR_ITERS} rounds, BC x{n_src}")
+    return total_e, total_s, desc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import inputs
+    import oracle
+
+    scale = 20  # bounded sample per step: a few seconds of single-thread oracle work
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    G = oracle.Graph(1 << scale, src, dst, w)
+    deg = G.out_degree()
+    srcs = inputs.rmat_sources(scale, args.warmup + args.steps)
+
+    def step(j):
+        s = int(srcs[j])
+        e = 0
+        lv = G.bfs(s)
+        e += int(deg[lv != 0xFFFFFFFF].sum())
+        d = G.sssp(s)
+        e += int(deg[d != 0xFFFFFFFF].sum())
+        G.pagerank(PR_ITERS)
+        e += G.E * PR_ITERS
+        G.bc([s])
+        e += 2 * int(deg[lv != 0xFFFFFFFF].sum())
+        return e
+
+    for j in range(args.warmup):
+        step(j)
+    t0 = time.perf_counter()
+    tot = 0
+    for j in range(args.steps):
+        tot += step(args.warmup + j)
+    sec = time.perf_counter() - t0
+    val = tot / sec / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64",
+        "data": "synthetic",
+        "config": {"workload": f"RMAT-{scale} sample of the RMAT-{args.scale} workload "
+                               "(BFS + SSSP + PageRank x5 + BC per step)", "scale": scale,
+                   "edge_factor": 16},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"RMAT-{scale}, one source per step, single thread"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+
+    import inputs
+    import paper_1312_3018_b200 as tg
+
+    scale = args.scale
+    V, E = 1 << scale, 16 << scale
+    t_build = time.perf_counter()
+    eng = tg.Engine.rmat(scale, edge_factor=16, seed=inputs.GRAPH_SEED, wseed=inputs.WEIGHT_SEED,
+                         partitions=1, device=dev, weighted=True, in_csr=True)
+    build_s = time.perf_counter() - t_build
+    srcs = inputs.rmat_sources(scale, args.warmup + 2 * args.steps + 1)
+
+    lv_d = torch.empty(V, dtype=torch.int32, device="cuda")
+    ds_d = torch.empty(V, dtype=torch.int32, device="cuda")
+    pr_d = torch.empty(V, dtype=torch.float32, device="cuda")
+    bc_d = torch.empty(V, dtype=torch.float64, device="cuda")
+
+    def step(j, outs):
+        s = int(srcs[j])
+        rs = [eng.bfs(s, out=outs[0])[1], eng.sssp(s, out=outs[1])[1],
+              eng.pagerank(PR_ITERS, out=outs[2])[1], eng.bc([s], out=outs[3])[1]]
+        return rs
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    for j in range(args.warmup):
+        step(j, (lv_d, ds_d, pr_d, bc_d))
+
+    # ---- device-resident timed region (value) ----
+    eng.set_profiling(True)
+    per_alg = {"bfs": [0, 0.0], "sssp": [0, 0.0], "pagerank": [0, 0.0], "bc": [0, 0.0]}
+    launches = 0
+    barrier()
+    with ClockSampler(dev) as clk:
+        dev_ms = 0.0
+        for j in range(args.steps):
+            rs = step(args.warmup + j, (lv_d, ds_d, pr_d, bc_d))
+            for name, r in zip(per_alg, rs):
+                per_alg[name][0] += r.traversed_edges
+                per_alg[name][1] += r.device_ms
+                dev_ms += r.device_ms
+                launches += r.launches
+        barrier()
+    kstats = eng.kernel_stats()
+    eng.set_profiling(False)
+    traversed = sum(v[0] for v in per_alg.values())
+    ms_step = dev_ms / args.steps
+    if dist:
+        t = torch.tensor([ms_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+        tt = torch.tensor([traversed], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt)
+        traversed_all = float(tt.item())
+    else:
+        traversed_all = float(traversed)
+    value = traversed_all / (ms_step * args.steps * 1e-3) / 1e9
+
+    # ---- end to end through the C ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        lv_h = torch.empty(V, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        ds_h = torch.empty(V, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        pr_h = torch.empty(V, dtype=torch.float32, pin_memory=True).numpy()
+        bc_h = torch.empty(V, dtype=torch.float64, pin_memory=True).numpy()
+        barrier()
+        t0 = time.perf_counter()
+        tr = 0
+        for j in range(args.steps):
+            rs = step(args.warmup + args.steps + j, (lv_h, ds_h, pr_h, bc_h))
+            tr += sum(r.traversed_edges for r in rs)
+        barrier()
+        sec = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([sec], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sec = float(t.item())
+            tt = torch.tensor([tr], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt)
+            tr = float(tt.item())
+        e2e = {"value": tr / sec / 1e9, "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": V * (4 + 4 + 4 + 8),
+               "note": "step inputs are source ids passed by value; the graph stays resident "
+                       "in HBM; every per-vertex result is copied to pinned host memory"}
+
+    # ---- roofline of the dominant kernel ----
+    peak, peak_src = measured_peak()
+    dom = max(kstats, key=lambda k: kstats[k]["ms"])
+    ks = kstats[dom]
+    achieved = ks["algorithmic_bytes"] / (ks["ms"] * 1e-3) / 1e9 if ks["ms"] > 0 else 0.0
+    tot_ms = sum(v["ms"] for v in kstats.values())
+    traffic = ncu_traffic().get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": ks["algorithmic_bytes"] / max(ks["launches"], 1),
+                "avg_launch_ms": ks["ms"] / max(ks["launches"], 1), "peak_source": peak_src,
+                "share_of_kernel_time": ks["ms"] / tot_ms if tot_ms else None}
+    kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
+                   "GBps": (v["algorithmic_bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] else None}
+               for k, v in kstats.items() if v["launches"]}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        e, s, desc = oracle_sample(args.cpu_scale)
+        cpu = {"value": e / s / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
+               "seconds": s}
+
+    info = eng.info
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32+f64", "data": "synthetic",
+        "config": {
+            "workload": f"RMAT-{scale} (A,B,C)=(0.57,0.19,0.19) edge factor 16: BFS + SSSP + "
+                        f"PageRank x{PR_ITERS} + BC, one source per step",
+            "scale": scale, "vertices": V, "edges": E, "partitions_per_gpu": 1,
+            "parallelism": "single" if world == 1 else f"replicas{world}",
+            "l2": "inputs larger than L2 (graph %.1f GB >> 126 MB L2)" % (info["device_bytes"] / 1e9),
+            "build_s": round(build_s, 2)},
+        "per_algorithm_gteps": {k: (v[0] / (v[1] * 1e-3) / 1e9 if v[1] else None)
+                                for k, v in per_alg.items()},
+        "per_algorithm_ms_per_step": {k: v[1] / args.steps for k, v in per_alg.items()},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "kernels": kernels,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            with open(args.out, "w") as f:
+                f.write(s + "\n")
+    eng.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

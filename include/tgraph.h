@@ -150,6 +150,34 @@ int tg_pagerank(tg_engine* eng, int iterations, double damping, float* rank, int
  * directed.  sources: host array of k global ids.  bc overwritten. */
 int tg_bc(tg_engine* eng, const uint64_t* sources, int k, double* bc, int mem, tg_stats* stats);
 
+/* ---- kernel ledger (measurement) --------------------------------------------
+ * With profiling on, the library brackets each hot kernel launch with CUDA
+ * events on the engine stream (the stream the kernel runs on) and accumulates,
+ * per kernel id: launches, summed event time and the ALGORITHMIC bytes the
+ * launch had to move (per-edge and per-vertex figures x
+ * the edges / vertices that launch processed).  Off by default. */
+typedef enum {
+  TG_K_BFS_EXPAND = 0,   /* BFS frontier expansion (edge tiles)           */
+  TG_K_SSSP_EXPAND = 1,  /* SSSP relaxation (edge tiles)                  */
+  TG_K_BCF_EXPAND = 2,   /* BC forward: BFS + sigma (edge tiles)          */
+  TG_K_BCB_EXPAND = 3,   /* BC backward: dependency pull (edge tiles)     */
+  TG_K_PR_PULL = 4,      /* PageRank pull-sum, all degree classes, 1 iter */
+  TG_K_ADVANCE = 5,      /* frontier advance / vote count                 */
+  TG_K_COMPACT = 6,      /* active-tile compaction                        */
+  TG_K_EXCHANGE = 7,     /* inter-partition message exchange + scatter    */
+  TG_K_COUNT = 8
+} tg_kernel_id;
+
+typedef struct {
+  uint64_t launches;
+  double ms;                 /* summed CUDA-event time                        */
+  double algorithmic_bytes;  /* summed algorithmic bytes of those launches    */
+} tg_kernel_stat;
+
+int tg_engine_set_profiling(tg_engine* eng, int on);   /* also resets the ledger */
+int tg_engine_kernel_stat(const tg_engine* eng, int kernel_id, tg_kernel_stat* out);
+const char* tg_kernel_name(int kernel_id);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,12 @@ Engine::~Engine() {
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (h_counts) cudaFreeHost(h_counts);
+  for (auto& p : pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  if (prof_open) cudaEventDestroy(prof_open);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -99,13 +105,73 @@ unsigned long long read_counts(Engine& eng, int idx) {
   return t;
 }
 
+Vote read_vote(Engine& eng) {
+  const int P = (int)eng.parts.size();
+  for (int i = 0; i < P; ++i)
+    TG_CK(cudaMemcpyAsync(eng.h_counts + 2 * i, eng.parts[i]->fs.counters.get(), 16,
+                          cudaMemcpyDeviceToHost, eng.stream));
+  TG_CK(cudaStreamSynchronize(eng.stream));
+  Vote v;
+  for (int i = 0; i < P; ++i) {
+    v.count += eng.h_counts[2 * i];
+    v.edges += eng.h_counts[2 * i + 1];
+  }
+  return v;
+}
+
+void reset_vote(Engine& eng) {
+  for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get(), 0, 16, eng.stream));
+}
+
 void time_begin(Engine& eng) { TG_CK(cudaEventRecord(eng.ev0, eng.stream)); }
 double time_end(Engine& eng) {
   TG_CK(cudaEventRecord(eng.ev1, eng.stream));
   TG_CK(cudaEventSynchronize(eng.ev1));
   float ms = 0;
   TG_CK(cudaEventElapsedTime(&ms, eng.ev0, eng.ev1));
+  eng.prof_flush();
   return (double)ms;
+}
+
+static cudaEvent_t pool_get(Engine& eng) {
+  if (!eng.ev_pool.empty()) {
+    cudaEvent_t e = eng.ev_pool.back();
+    eng.ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  TG_CK(cudaEventCreate(&e));
+  return e;
+}
+
+void Engine::prof_begin(int kid) {
+  if (!prof) return;
+  prof_open = pool_get(*this);
+  prof_open_kid = kid;
+  TG_CK(cudaEventRecord(prof_open, stream));
+}
+
+void Engine::prof_end(int kid) {
+  if (!prof || !prof_open || prof_open_kid != kid) return;
+  cudaEvent_t b = pool_get(*this);
+  TG_CK(cudaEventRecord(b, stream));
+  pending.push_back({kid, prof_open, b});
+  prof_open = nullptr;
+  prof_open_kid = -1;
+}
+
+void Engine::prof_flush() {
+  if (pending.empty()) return;
+  TG_CK(cudaStreamSynchronize(stream));
+  for (auto& p : pending) {
+    float ms = 0;
+    TG_CK(cudaEventElapsedTime(&ms, p.a, p.b));
+    kstat[p.kid].launches++;
+    kstat[p.kid].ms += ms;
+    ev_pool.push_back(p.a);
+    ev_pool.push_back(p.b);
+  }
+  pending.clear();
 }
 
 namespace {
@@ -383,6 +449,32 @@ int tg_pagerank(tg_engine* e, int iterations, double damping, float* rank, int m
 
 int tg_bc(tg_engine* e, const uint64_t* sources, int k, double* bc, int mem, tg_stats* st) {
   TG_RUN({ run_bc(eng, sources, k, bc, mem, st); });
+}
+
+int tg_engine_set_profiling(tg_engine* e, int on) {
+  return guard([&] {
+    TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");
+    Engine& eng = *reinterpret_cast<Engine*>(e);
+    TG_CK(cudaSetDevice(eng.device));
+    eng.prof_flush();
+    eng.prof = on != 0;
+    for (auto& k : eng.kstat) k = tg_kernel_stat{};
+  });
+}
+
+int tg_engine_kernel_stat(const tg_engine* e, int kid, tg_kernel_stat* out) {
+  return guard([&] {
+    TG_REQUIRE(e && out, TG_EINVAL, "NULL argument");
+    TG_REQUIRE(kid >= 0 && kid < TG_K_COUNT, TG_EINVAL, "kernel id out of range");
+    *out = reinterpret_cast<const Engine*>(e)->kstat[kid];
+  });
+}
+
+const char* tg_kernel_name(int kid) {
+  static const char* names[TG_K_COUNT] = {"bfs_expand",  "sssp_expand", "bc_fwd_expand",
+                                          "bc_bwd_expand", "pr_pull",   "advance",
+                                          "tile_compact", "exchange_scatter"};
+  return (kid >= 0 && kid < TG_K_COUNT) ? names[kid] : "?";
 }
 
 }  // extern "C"

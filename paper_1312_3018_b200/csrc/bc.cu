@@ -174,7 +174,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
   eng.launches = 0;
   eng.comm_bytes = 0;
   double total_ms = 0;
-  uint64_t supersteps = 0, traversed = 0, bytes = 0;
+  uint64_t supersteps = 0, traversed = 0, bytes = 0, bm_bytes = 0;
+  for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   for (int si = 0; si < k; ++si) {
     int ps;
     uint32_t ls;
@@ -196,7 +197,6 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         TG_CK(cudaMemsetAsync(f.obox_new.get(), 0, p.S / 8, s));
         TG_CK(cudaMemsetAsync(b.obox_sigma.get(), 0, p.S * 8, s));
       }
-      TG_CK(cudaMemsetAsync(f.counters.get(), 0, f.counters.bytes(), s));
       if (p.id == ps) {
         k_bc_seed<<<1, 1, 0, s>>>(F0, ls, b.sigma.get());
         eng.launches++;
@@ -204,7 +204,9 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       launch_advance(eng, p, p.ts, F0, nullptr, f.visited.get(), nullptr, 0, f.counters.get());
     }
     uint32_t maxL = 0;
+    std::vector<uint64_t> lvl_count{1}, lvl_edges;  // |F[L]| and edges of F[L] rows
     for (uint32_t L = 0;; ++L) {
+      reset_vote(eng);
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         FrontierState& f = p.fs;
@@ -214,10 +216,11 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         launch_compact(eng, p.ts);
         BcFwdOp op{p.col.get(), f.visited.get(), next, b.sigma.get(), f.obox_mark.get(),
                    f.obox_new.get(), b.obox_sigma.get()};
-        launch_expand(eng, p, p.ts, b.level_bm[L].get(), op);
+        launch_expand(eng, p, p.ts, b.level_bm[L].get(), op, TG_K_BCF_EXPAND, f.counters.get() + 1);
       }
       supersteps++;
       if (eng.P > 1) {
+        eng.prof_begin(TG_K_EXCHANGE);
         exchange(eng, send_osigma, recv_isigma, 8, false);
         for (auto& pp : eng.parts) {
           Part& p = *pp;
@@ -237,15 +240,22 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           }
           TG_CK(cudaGetLastError());
         }
+        eng.prof_end(TG_K_EXCHANGE);
       }
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         FrontierState& f = p.fs;
-        TG_CK(cudaMemsetAsync(f.counters.get(), 0, 8, s));
         launch_advance(eng, p, p.ts, p.bcs.level_bm[L + 1].get(), nullptr, f.visited.get(), nullptr,
                        0, f.counters.get());
       }
-      if (read_counts(eng, 0) == 0) {
+      const Vote v = read_vote(eng);
+      // forward expand: col 4 per edge; offsets 16 + sigma[v] 8 per frontier
+      // vertex; sigma[t] 8 per newly reached vertex; 3 bitmap passes
+      eng.prof_bytes(TG_K_BCF_EXPAND,
+                     4.0 * v.edges + 24.0 * lvl_count[L] + 8.0 * v.count + 3.0 * bm_bytes);
+      lvl_edges.push_back(v.edges);
+      lvl_count.push_back(v.count);
+      if (v.count == 0) {
         maxL = L;  // F[L+1] is empty
         break;
       }
@@ -276,8 +286,12 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           launch_compact(eng, p.ts);
           BcBwdOp op{p.col.get(), p.bcs.level_bm[L + 1].get(), p.bcs.c.get(), p.bcs.ghost.get(),
                      p.bcs.dsum.get()};
-          launch_expand(eng, p, p.ts, p.bcs.level_bm[L].get(), op);
+          launch_expand(eng, p, p.ts, p.bcs.level_bm[L].get(), op, TG_K_BCB_EXPAND, nullptr);
         }
+        // backward expand: col 4 per edge; c 8 per successor (read once);
+        // offsets 16 + dsum 8 per level-L vertex; level + successor bitmaps
+        eng.prof_bytes(TG_K_BCB_EXPAND, 4.0 * lvl_edges[L] + 8.0 * lvl_count[L + 1] +
+                                            24.0 * lvl_count[L] + 2.0 * bm_bytes);
         supersteps++;
       }
       for (auto& pp : eng.parts) {

@@ -60,6 +60,7 @@ void* recv_ibits(Part& p) { return p.fs.ibox_bits.get(); }
 }  // namespace
 
 void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st) {
+  TG_REQUIRE(out != nullptr, TG_EINVAL, "tg_bfs: NULL levels");
   int ps;
   uint32_t ls;
   eng.locate(source, &ps, &ls);
@@ -67,7 +68,10 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
   eng.launches = 0;
   eng.comm_bytes = 0;
   cudaStream_t s = eng.stream;
+  uint64_t bm_bytes = 0;  // one pass over every partition's vertex bitmap
+  for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   time_begin(eng);
+  reset_vote(eng);
   for (auto& pp : eng.parts) {
     Part& p = *pp;
     FrontierState& f = p.fs;
@@ -80,7 +84,6 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
       TG_CK(cudaMemsetAsync(f.obox_mark.get(), 0, p.S / 8, s));
       TG_CK(cudaMemsetAsync(f.obox_new.get(), 0, p.S / 8, s));
     }
-    TG_CK(cudaMemsetAsync(f.counters.get(), 0, f.counters.bytes(), s));
     if (p.id == ps) {
       k_seed<<<1, 1, 0, s>>>(f.next.get(), ls, nullptr, 0);
       eng.launches++;
@@ -89,17 +92,19 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
                    f.counters.get());
     std::swap(f.cur, f.next);
   }
-  uint64_t supersteps = 0;
+  uint64_t supersteps = 0, frontier = 1, edges_total = 0;
   for (uint32_t L = 0;; ++L) {
+    reset_vote(eng);
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
       BfsOp op{p.col.get(), f.visited.get(), f.next.get(), f.obox_mark.get(), f.obox_new.get()};
-      launch_expand(eng, p, p.ts, f.cur.get(), op);
+      launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_BFS_EXPAND, f.counters.get() + 1);
     }
     supersteps++;
     if (eng.P > 1) {
+      eng.prof_begin(TG_K_EXCHANGE);
       exchange(eng, send_onew, recv_ibits, 0, false);
       for (auto& pp : eng.parts) {
         Part& p = *pp;
@@ -112,16 +117,22 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
           eng.launches++;
         }
       }
+      eng.prof_end(TG_K_EXCHANGE);
     }
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       FrontierState& f = p.fs;
-      TG_CK(cudaMemsetAsync(f.counters.get(), 0, 8, s));
       launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), f.visited.get(), f.vals.get(), L + 1,
                      f.counters.get());
       std::swap(f.cur, f.next);
     }
-    if (read_counts(eng, 0) == 0) break;  // termination vote
+    const Vote v = read_vote(eng);
+    // expand: 4 B col per edge, 16 B row offsets per frontier vertex, frontier +
+    // visited + next bitmaps one pass each
+    eng.prof_bytes(TG_K_BFS_EXPAND, 4.0 * v.edges + 16.0 * frontier + 3.0 * bm_bytes);
+    edges_total += v.edges;
+    frontier = v.count;
+    if (v.count == 0) break;  // termination vote
     TG_REQUIRE(supersteps <= eng.V + 1, TG_EINTERNAL, "tg_bfs: superstep bound exceeded");
   }
   const double ms = time_end(eng);
@@ -130,12 +141,11 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
     st->supersteps = supersteps;
     uint64_t nreached = 0;
     st->traversed_edges = reached_outdeg_u32(eng, &nreached);
-    // algorithmic bytes: 4 B per traversed edge (col),
-    // 16 B row offsets + 4 B level write per reached vertex, three bitmap
-    // passes (frontier, next, visited) per superstep.
-    uint64_t bm = 0;
-    for (auto& pp : eng.parts) bm += words_for(pp->Vp) * 4 * 3 * (supersteps + 1);
-    st->algorithmic_bytes = 4 * st->traversed_edges + 20 * nreached + bm;
+    TG_REQUIRE(st->traversed_edges == edges_total, TG_EINTERNAL,
+               "tg_bfs: expanded edges != sum of reached out-degrees");
+    // 4 B per traversed edge (col), 16 B row offsets + 4 B level write per
+    // reached vertex, three bitmap passes (frontier, next, visited) per superstep.
+    st->algorithmic_bytes = 4 * st->traversed_edges + 20 * nreached + 3 * bm_bytes * (supersteps + 1);
     st->comm_bytes = eng.comm_bytes;
     st->launches = eng.launches;
   }

@@ -130,6 +130,21 @@ struct Engine {
   uint64_t launches = 0;     // kernels launched by the current run
   uint64_t comm_bytes = 0;   // message bytes exchanged by the current run
   unsigned long long* h_counts = nullptr;  // pinned host scratch (TG_MAX_PARTITIONS * 4)
+  // kernel ledger (tg_engine_set_profiling)
+  bool prof = false;
+  tg_kernel_stat kstat[TG_K_COUNT] = {};
+  struct Pending {
+    int kid;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t prof_open = nullptr;
+  int prof_open_kid = -1;
+  void prof_begin(int kid);             // no-op unless prof
+  void prof_end(int kid);
+  void prof_bytes(int kid, double bytes) { if (prof) kstat[kid].algorithmic_bytes += bytes; }
+  void prof_flush();                    // sync + accumulate pending pairs
   ~Engine();
   uint64_t device_bytes() const;
   // global id -> (partition, local id); one 4-byte D2H read
@@ -169,6 +184,14 @@ void collect_u32(Engine& eng, uint32_t* out, int mem);  // fs.vals -> out[global
 void ensure_frontier_state(Engine& eng);
 // read the per-partition counters[idx] (one sync) and return their sum
 unsigned long long read_counts(Engine& eng, int idx);
+// counters layout: [0] new-frontier count (advance), [1] edges processed by the
+// superstep's expand, [2] error flags, [3] spare.  One sync for all partitions.
+struct Vote {
+  unsigned long long count = 0, edges = 0;
+};
+Vote read_vote(Engine& eng);
+// zero counters[0..1] of every partition (start of a superstep)
+void reset_vote(Engine& eng);
 void time_begin(Engine& eng);
 double time_end(Engine& eng);  // ms since time_begin (CUDA events)
 

@@ -116,8 +116,11 @@ void launch_compact(Engine& eng, TileSched& ts) {
   TG_CK(cudaMemsetAsync(ts.count.get(), 0, sizeof(unsigned long long), eng.stream));
   if (!ts.nwords) return;
   const unsigned blocks = grid_for(ts.nwords, 256, 148u * 8u);
+  eng.prof_begin(TG_K_COMPACT);
   k_tile_compact<<<blocks, 256, 0, eng.stream>>>(ts.bm.get(), ts.nwords, ts.list.get(),
                                                  ts.count.get());
+  eng.prof_end(TG_K_COMPACT);
+  eng.prof_bytes(TG_K_COMPACT, 4.0 * ts.nwords);
   TG_CK(cudaGetLastError());
   eng.launches++;
 }
@@ -128,8 +131,12 @@ void launch_advance(Engine& eng, Part& p, TileSched& ts, uint32_t* next, uint32_
   if (!p.Vp) return;
   const uint64_t nwords = words_for(p.Vp);
   const unsigned blocks = grid_for(nwords * 32, 256, 148u * 16u);
+  eng.prof_begin(TG_K_ADVANCE);
   k_advance<<<blocks, 256, 0, eng.stream>>>(next, cur_old, visited, vals, level_val, p.Vp,
                                             p.row_off.get(), ts.bm.get(), count, degsum);
+  eng.prof_end(TG_K_ADVANCE);
+  // next read + cur_old clear + visited RMW, one pass each
+  eng.prof_bytes(TG_K_ADVANCE, 4.0 * nwords * (1 + (cur_old ? 1 : 0) + (visited ? 2 : 0)));
   TG_CK(cudaGetLastError());
   eng.launches++;
 }

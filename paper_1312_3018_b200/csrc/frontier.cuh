@@ -61,6 +61,7 @@ struct TileArgs {
   const unsigned long long* tile_count;
   uint64_t Ep;
   const uint32_t* frontier;  // bitmap of active rows
+  unsigned long long* edges; // += edges processed (one atomic per tile)
 };
 
 template <class Op>
@@ -163,7 +164,10 @@ __global__ void __launch_bounds__(kTileThreads) k_tile_expand(TileArgs a, Op op)
         ex += len[q];
       }
     }
-    if (tid == 0) S.pre[A] = W;
+    if (tid == 0) {
+      S.pre[A] = W;
+      if (a.edges) atomicAdd(a.edges, (unsigned long long)W);
+    }
     __syncthreads();
     // 4. warp w walks flattened edges [j0, j1) in 32-edge steps
     {
@@ -248,10 +252,11 @@ void launch_advance(Engine& eng, Part& p, TileSched& ts, uint32_t* next, uint32_
 unsigned expand_grid();
 
 template <class Op>
-void launch_expand(Engine& eng, Part& p, TileSched& ts, const uint32_t* frontier, const Op& op) {
+void launch_expand(Engine& eng, Part& p, TileSched& ts, const uint32_t* frontier, const Op& op,
+                   int kid, unsigned long long* edges) {
   if (!p.ntiles) return;
   TileArgs a{p.row_off.get(), p.tile_vf.get(), p.tile_vl.get(), ts.list.get(), ts.count.get(),
-             p.Ep, frontier};
+             p.Ep, frontier, edges};
   const size_t smem = sizeof(TileSmem<Op>);
   static bool configured = false;
   if (!configured) {
@@ -259,7 +264,9 @@ void launch_expand(Engine& eng, Part& p, TileSched& ts, const uint32_t* frontier
                                (int)smem));
     configured = true;
   }
+  eng.prof_begin(kid);
   k_tile_expand<Op><<<expand_grid(), kTileThreads, smem, eng.stream>>>(a, op);
+  eng.prof_end(kid);
   TG_CK(cudaGetLastError());
   eng.launches++;
 }

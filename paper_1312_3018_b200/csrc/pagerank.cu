@@ -193,6 +193,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   }
   int cur = 0;
   for (int it = 0; it < iters; ++it) {
+    eng.prof_begin(TG_K_PR_PULL);
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       PRState& r = p.pr;
@@ -203,6 +204,10 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
         launch_pull_range(eng, p, r.contrib[cur].get(), p.Vp, p.Vp + p.box_cta, p.Vp + p.box_warp,
                           p.Vp + p.S, o);
     }
+    eng.prof_end(TG_K_PR_PULL);
+    // pull: in_col 4 + contrib gather 4 per edge; in_off 8 + outdeg 4 + rank 4 +
+    // next contrib 4 per row
+    eng.prof_bytes(TG_K_PR_PULL, 8.0 * eng.E + 20.0 * eng.V);
     if (eng.P > 1) {
       exchange(eng, send_obox, recv_ibox, 8, false);
       for (auto& pp : eng.parts) {

@@ -68,6 +68,7 @@ void* recv_ibox(Part& p) { return p.fs.ibox_u32.get(); }
 }  // namespace
 
 void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st) {
+  TG_REQUIRE(out != nullptr, TG_EINVAL, "tg_sssp: NULL dist");
   TG_REQUIRE(eng.weighted, TG_EINVAL, "tg_sssp: engine was built without edge weights");
   int ps;
   uint32_t ls;
@@ -76,7 +77,10 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   eng.launches = 0;
   eng.comm_bytes = 0;
   cudaStream_t s = eng.stream;
+  uint64_t bm_bytes = 0;
+  for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   time_begin(eng);
+  for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get(), 0, 32, s));
   for (auto& pp : eng.parts) {
     Part& p = *pp;
     FrontierState& f = p.fs;
@@ -85,27 +89,27 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     TG_CK(cudaMemsetAsync(f.cur.get(), 0, nw * 4, s));
     TG_CK(cudaMemsetAsync(f.next.get(), 0, nw * 4, s));
     if (p.S) TG_CK(cudaMemsetAsync(f.obox_u32.get(), 0xFF, p.S * 4, s));
-    TG_CK(cudaMemsetAsync(f.counters.get(), 0, f.counters.bytes(), s));
     if (p.id == ps) {
       k_seed<<<1, 1, 0, s>>>(f.next.get(), ls, f.vals.get(), 0);
       eng.launches++;
     }
-    launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get(),
-                   f.counters.get() + 2);
+    launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get());
     std::swap(f.cur, f.next);
   }
-  uint64_t supersteps = 0;
+  uint64_t supersteps = 0, frontier = 1, relax = 0, activations = 1;
   for (;;) {
+    reset_vote(eng);
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
       SsspOp op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
-                f.counters.get() + 1};
-      launch_expand(eng, p, p.ts, f.cur.get(), op);
+                f.counters.get() + 2};
+      launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
     }
     supersteps++;
     if (eng.P > 1) {
+      eng.prof_begin(TG_K_EXCHANGE);
       exchange(eng, send_obox, recv_ibox, 4, false);
       for (auto& pp : eng.parts) {
         Part& p = *pp;
@@ -115,29 +119,32 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
         TG_CK(cudaGetLastError());
         eng.launches++;
       }
+      eng.prof_end(TG_K_EXCHANGE);
     }
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       FrontierState& f = p.fs;
-      TG_CK(cudaMemsetAsync(f.counters.get(), 0, 8, s));
-      launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get(),
-                     f.counters.get() + 2);
+      launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get());
       std::swap(f.cur, f.next);
     }
-    if (read_counts(eng, 0) == 0) break;
+    const Vote v = read_vote(eng);
+    // relaxation: col 4 + w 4 + dist[t] 4 per edge; offsets 16 + dist[v] 4 per
+    // active vertex; active + next bitmaps one pass each
+    eng.prof_bytes(TG_K_SSSP_EXPAND, 12.0 * v.edges + 20.0 * frontier + 2.0 * bm_bytes);
+    relax += v.edges;
+    frontier = v.count;
+    activations += v.count;
+    if (v.count == 0) break;
     TG_REQUIRE(supersteps <= eng.V + 1, TG_EINTERNAL, "tg_sssp: superstep bound exceeded");
   }
   const double ms = time_end(eng);
-  TG_REQUIRE(read_counts(eng, 1) == 0, TG_EINTERNAL, "tg_sssp: distance overflows uint32");
+  TG_REQUIRE(read_counts(eng, 2) == 0, TG_EINTERNAL, "tg_sssp: distance overflows uint32");
   if (st) {
     uint64_t nreached = 0;
     st->device_ms = ms;
     st->supersteps = supersteps;
     st->traversed_edges = reached_outdeg_u32(eng, &nreached);
-    // relaxed edges R = sum of out-degrees of every activation (counters[2]):
-    // 12 B per relaxation (col + w + dist probe), 20 B per activation row.
-    const uint64_t R = read_counts(eng, 2);
-    st->algorithmic_bytes = 12 * R + 20 * nreached;
+    st->algorithmic_bytes = 12 * relax + 20 * activations + 2 * bm_bytes * supersteps;
     st->comm_bytes = eng.comm_bytes;
     st->launches = eng.launches;
   }

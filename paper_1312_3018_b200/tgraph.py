@@ -49,6 +49,13 @@ class tg_stats(C.Structure):
                 ("comm_bytes", C.c_uint64), ("launches", C.c_uint64)]
 
 
+class tg_kernel_stat(C.Structure):
+    _fields_ = [("launches", C.c_uint64), ("ms", C.c_double), ("algorithmic_bytes", C.c_double)]
+
+
+TG_K_COUNT = 8
+
+
 @dataclass
 class Stats:
     device_ms: float
@@ -89,8 +96,13 @@ def lib():
         L.tg_sssp.argtypes = [p, u64, p, i32, C.POINTER(tg_stats)]
         L.tg_pagerank.argtypes = [p, i32, dbl, p, i32, C.POINTER(tg_stats)]
         L.tg_bc.argtypes = [p, p, i32, p, i32, C.POINTER(tg_stats)]
+        L.tg_engine_set_profiling.argtypes = [p, i32]
+        L.tg_engine_kernel_stat.argtypes = [p, i32, C.POINTER(tg_kernel_stat)]
+        L.tg_kernel_name.argtypes = [i32]
+        L.tg_kernel_name.restype = C.c_char_p
         for f in ("tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
-                  "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc"):
+                  "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc",
+                  "tg_engine_set_profiling", "tg_engine_kernel_stat"):
             getattr(L, f).restype = i32
         _LIB = L
     return _LIB
@@ -199,6 +211,21 @@ def tg_bc(h, V, sources, out=None):
     return out, Stats.of(st)
 
 
+def tg_engine_set_profiling(h, on: bool) -> None:
+    _check(lib().tg_engine_set_profiling(h, int(on)))
+
+
+def tg_engine_kernel_stats(h) -> dict:
+    """{kernel name: {launches, ms, algorithmic_bytes}} from the engine's ledger."""
+    out = {}
+    for kid in range(TG_K_COUNT):
+        s = tg_kernel_stat()
+        _check(lib().tg_engine_kernel_stat(h, kid, C.byref(s)))
+        out[lib().tg_kernel_name(kid).decode()] = {
+            "launches": s.launches, "ms": s.ms, "algorithmic_bytes": s.algorithmic_bytes}
+    return out
+
+
 class Engine:
     """Owning handle: a partitioned, device-resident graph."""
 
@@ -241,3 +268,9 @@ class Engine:
 
     def bc(self, sources, out=None):
         return tg_bc(self.h, self.V, sources, out)
+
+    def set_profiling(self, on=True):
+        tg_engine_set_profiling(self.h, on)
+
+    def kernel_stats(self):
+        return tg_engine_kernel_stats(self.h)
