@@ -33,7 +33,7 @@ struct BcFwdOp {
   uint32_t* onew;
   double* osigma;
   __device__ __forceinline__ Aux aux(uint32_t v) const { return sigma[v]; }
-  __device__ __forceinline__ void edge(uint32_t, const Aux& sv, uint64_t e) const {
+  __device__ __forceinline__ void edge(const Aux& sv, uint64_t e) const {
     const uint32_t t = __ldcs(col + e);
     if (t & kRemote) {
       const uint32_t s = t & ~kRemote, m = 1u << (s & 31);
@@ -60,12 +60,12 @@ struct BcBwdOp {
   const double* ghost;
   double* dsum;
   __device__ __forceinline__ Aux aux(uint32_t) const { return {}; }
-  __device__ __forceinline__ double edge_val(uint32_t, const Aux&, uint64_t e) const {
+  __device__ __forceinline__ double edge_val(uint64_t e) const {
     const uint32_t t = __ldcs(col + e);
     if (t & kRemote) return ghost[t & ~kRemote];
     return bit_test(succ, t) ? c[t] : 0.0;
   }
-  __device__ __forceinline__ void vertex_done(uint32_t v, const Aux&, double acc, bool whole) const {
+  __device__ __forceinline__ void vertex_done(uint32_t v, double acc, bool whole) const {
     if (whole) dsum[v] = acc;
     else atomicAdd(&dsum[v], acc);
   }

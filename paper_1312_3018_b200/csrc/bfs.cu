@@ -29,7 +29,7 @@ struct BfsOp {
   uint32_t* omark;
   uint32_t* onew;
   __device__ __forceinline__ Aux aux(uint32_t) const { return {}; }
-  __device__ __forceinline__ void edge(uint32_t, const Aux&, uint64_t e) const {
+  __device__ __forceinline__ void edge(const Aux&, uint64_t e) const {
     const uint32_t t = __ldcs(col + e);
     if (t & kRemote) {
       const uint32_t s = t & ~kRemote, m = 1u << (s & 31);

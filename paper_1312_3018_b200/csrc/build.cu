@@ -308,6 +308,84 @@ void exclusive_scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStrea
 
 constexpr uint32_t kPrCta = 2048;  // in-degree at/above which a PageRank row gets a whole CTA
 
+// first row r with row_off[r] >= target (chunk split points for the row sort)
+__global__ void k_split_rows(const uint64_t* row_off, uint64_t nrows, uint64_t step, uint64_t nsplit,
+                             uint64_t* out) {
+  const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (k > nsplit) return;
+  const uint64_t target = k * step;
+  uint64_t lo = 0, hi = nrows;
+  while (lo < hi) {
+    const uint64_t m = (lo + hi) >> 1;
+    if (row_off[m] < target) lo = m + 1;
+    else hi = m;
+  }
+  out[k] = k == nsplit ? nrows : lo;
+}
+
+__global__ void k_rel_offsets(const uint64_t* row_off, uint64_t r0, uint64_t n, uint32_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t base = row_off[r0];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n; i += stride)
+    out[i] = (uint32_t)(row_off[r0 + i] - base);
+}
+
+// Sort the entries of every CSR row ascending (values travel with their keys).
+// Local targets (< kRemote) therefore stay before remote ones, and the
+// lanes of a warp that gather neighbour state touch ascending addresses.
+void sort_rows(const uint64_t* row_off, uint64_t nrows, uint32_t* keys, uint32_t* vals,
+               cudaStream_t s) {
+  if (!nrows) return;
+  uint64_t E = 0;
+  TG_CK(cudaMemcpyAsync(&E, row_off + nrows, 8, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+  if (E < 2) return;
+  const uint64_t step = 1ull << 30;
+  const uint64_t nsplit = (E + step - 1) / step;
+  DevBuf<uint64_t> splits(nsplit + 1);
+  k_split_rows<<<(unsigned)((nsplit + 256) / 256), 256, 0, s>>>(row_off, nrows, step, nsplit,
+                                                                 splits.get());
+  TG_CK(cudaGetLastError());
+  std::vector<uint64_t> hs(nsplit + 1);
+  TG_CK(cudaMemcpyAsync(hs.data(), splits.get(), (nsplit + 1) * 8, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+  hs[0] = 0;
+  std::vector<uint64_t> ho(2);
+  for (uint64_t c = 0; c < nsplit; ++c) {
+    const uint64_t r0 = hs[c], r1 = std::max(hs[c + 1], r0);
+    if (r1 <= r0) continue;
+    uint64_t e0, e1;
+    TG_CK(cudaMemcpyAsync(&e0, row_off + r0, 8, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaMemcpyAsync(&e1, row_off + r1, 8, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaStreamSynchronize(s));
+    const uint64_t n = e1 - e0, nseg = r1 - r0;
+    if (n < 2) continue;
+    TG_REQUIRE(n < (1ull << 31) && nseg < (1ull << 31), TG_ECAPACITY, "row sort chunk too large");
+    DevBuf<uint32_t> off(nseg + 1), kout(n), vout(vals ? n : 0);
+    k_rel_offsets<<<G(nseg + 1), kB, 0, s>>>(row_off, r0, nseg, off.get());
+    TG_CK(cudaGetLastError());
+    size_t tmp = 0;
+    if (vals) {
+      TG_CK(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, keys + e0, kout.get(), vals + e0,
+                                                vout.get(), (int)n, (int)nseg, off.get(),
+                                                off.get() + 1, s));
+      DevBuf<uint8_t> t(tmp ? tmp : 1);
+      TG_CK(cub::DeviceSegmentedSort::SortPairs(t.get(), tmp, keys + e0, kout.get(), vals + e0,
+                                                vout.get(), (int)n, (int)nseg, off.get(),
+                                                off.get() + 1, s));
+      TG_CK(cudaMemcpyAsync(vals + e0, vout.get(), n * 4, cudaMemcpyDeviceToDevice, s));
+    } else {
+      TG_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, keys + e0, kout.get(), (int)n,
+                                               (int)nseg, off.get(), off.get() + 1, s));
+      DevBuf<uint8_t> t(tmp ? tmp : 1);
+      TG_CK(cub::DeviceSegmentedSort::SortKeys(t.get(), tmp, keys + e0, kout.get(), (int)n,
+                                               (int)nseg, off.get(), off.get() + 1, s));
+    }
+    TG_CK(cudaMemcpyAsync(keys + e0, kout.get(), n * 4, cudaMemcpyDeviceToDevice, s));
+    TG_CK(cudaStreamSynchronize(s));
+  }
+}
+
 void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
                 const uint32_t* outdeg) {
   cudaStream_t s = eng.stream;
@@ -421,6 +499,7 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
   nloc.release();
   nrem.release();
   ukeys.release();
+  sort_rows(pt.row_off.get(), Vp, pt.col.get(), eng.weighted ? pt.w.get() : nullptr, s);
 
   // tiles
   pt.ntiles = (pt.Ep + kTile - 1) / kTile;
@@ -488,6 +567,9 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
                                         pt.in_off.get(), indeg.get(), pt.in_col.get());
       TG_CK(cudaGetLastError());
     }
+    indeg.release();
+    slot_pos.release();
+    sort_rows(pt.in_off.get(), R, pt.in_col.get(), nullptr, s);
     pt.in_outdeg.alloc(std::max<uint64_t>(Vp, 1));
     k_in_outdeg<<<G(Vp), kB, 0, s>>>(pt.row_off.get(), pt.in_local.get(), Vp, pt.in_outdeg.get());
     TG_CK(cudaGetLastError());

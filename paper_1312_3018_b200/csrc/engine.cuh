@@ -28,8 +28,7 @@
 
 namespace tg {
 
-constexpr uint32_t kTile = 2048;        // edges per frontier tile
-constexpr uint32_t kTileThreads = 512;  // CTA size of the tile kernels
+constexpr uint32_t kTile = 1024;  // edges per frontier tile (one warp task)
 
 // Degree-aware serpentine deal (reading A23): order position i -> (part, local).
 __host__ __device__ __forceinline__ void deal(uint64_t i, int P, int* p, uint32_t* l) {

@@ -109,7 +109,7 @@ unsigned expand_grid() {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
-  return (unsigned)g_num_sms * 3u;  // persistent: 3 resident CTAs of 512 threads per SM
+  return (unsigned)g_num_sms * 8u;  // persistent: 8 resident CTAs of 256 threads per SM
 }
 
 void launch_compact(Engine& eng, TileSched& ts) {

@@ -27,7 +27,7 @@ struct SsspOp {
   uint32_t* obox;
   unsigned long long* overflow;
   __device__ __forceinline__ Aux aux(uint32_t v) const { return dist[v]; }
-  __device__ __forceinline__ void edge(uint32_t, const Aux& dv, uint64_t e) const {
+  __device__ __forceinline__ void edge(const Aux& dv, uint64_t e) const {
     const uint32_t t = __ldcs(col + e);
     const uint64_t nd64 = (uint64_t)dv + __ldcs(w + e);
     if (nd64 >= (uint64_t)kInf) {
