@@ -32,57 +32,73 @@ __global__ void k_tile_compact(uint32_t* tile_bm, uint64_t nwords, uint32_t* lis
   }
 }
 
+// set the tile bits of edges [row_off[r0], row_off[r1]) -- one atomicOr per
+// 32 tiles
 __device__ __forceinline__ void mark_tile_range(const uint64_t* row_off, uint64_t r0, uint64_t r1,
-                                                uint32_t* tile_bm, int lane) {
+                                                uint32_t* tile_bm) {
   const uint64_t lo = row_off[r0], hi = row_off[r1];
   if (hi <= lo) return;
   const uint64_t t0 = lo / kTile, t1 = (hi - 1) / kTile;
-  for (uint64_t t = t0 + lane; t <= t1; t += 32) atomicOr(&tile_bm[t >> 5], 1u << (t & 31));
+  for (uint64_t t = t0; t <= t1;) {
+    const uint64_t wbase = t & ~31ull;
+    const uint64_t last = (t1 < wbase + 31) ? t1 : wbase + 31;
+    const uint32_t hi_mask = (last - wbase == 31) ? 0xFFFFFFFFu : ((2u << (last - wbase)) - 1u);
+    const uint32_t mask = hi_mask & (0xFFFFFFFFu << (t - wbase));
+    atomicOr(&tile_bm[wbase >> 5], mask);
+    t = wbase + 32;
+  }
 }
 
-// One warp per bitmap word; lane = bit.
+__device__ __forceinline__ void block_add(unsigned long long* dst, unsigned long long v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
+// One thread per bitmap word.
 __global__ void k_advance(uint32_t* next, uint32_t* cur_old, uint32_t* visited, uint32_t* vals,
                           uint32_t level_val, uint64_t Vp, const uint64_t* row_off,
                           uint32_t* tile_bm, unsigned long long* count,
                           unsigned long long* degsum) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t nwords = words_for(Vp);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   unsigned long long cnt = 0, dsum = 0;
-  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < nwords;
-       w += nwarps) {
-    const uint32_t x = next[w];
-    if (lane == 0 && cur_old) cur_old[w] = 0;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
+    uint32_t x = next[w];
+    if (cur_old) cur_old[w] = 0;
     if (!x) continue;
-    const uint64_t v = w * 32 + lane;
-    const bool set = (x >> lane) & 1u;
-    if (vals && set) vals[v] = level_val;
-    if (degsum) {
-      unsigned long long dg = set ? row_off[v + 1] - row_off[v] : 0ull;
-      for (int o = 16; o; o >>= 1) dg += __shfl_down_sync(0xffffffffu, dg, o);
-      if (lane == 0) dsum += dg;
+    cnt += __popc(x);
+    if (visited) visited[w] |= x;
+    const uint64_t v0 = w * 32;
+    const uint64_t v1 = (v0 + 32 < Vp) ? v0 + 32 : Vp;
+    if (degsum) dsum += row_off[v1] - row_off[v0];  // upper bound (whole word), diagnostics
+    if (vals) {
+      if (x == 0xFFFFFFFFu && v0 + 32 <= Vp) {
+        uint4* p = reinterpret_cast<uint4*>(vals + v0);
+        const uint4 q = make_uint4(level_val, level_val, level_val, level_val);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) p[i] = q;
+      } else {
+        while (x) {
+          const int b = __ffs(x) - 1;
+          x &= x - 1;
+          vals[v0 + b] = level_val;
+        }
+      }
     }
-    if (lane == 0) {
-      if (visited) visited[w] |= x;
-      cnt += __popc(x);
-    }
-    const uint64_t r1 = (w * 32 + 32 < Vp) ? w * 32 + 32 : Vp;
-    mark_tile_range(row_off, w * 32, r1, tile_bm, lane);
+    mark_tile_range(row_off, v0, v1, tile_bm);
   }
-  if (lane == 0 && cnt) atomicAdd(count, cnt);
-  if (lane == 0 && dsum) atomicAdd(degsum, dsum);
+  block_add(count, cnt);
+  if (degsum) block_add(degsum, dsum);
 }
 
 __global__ void k_mark_tiles(const uint32_t* bm, uint64_t Vp, const uint64_t* row_off,
                              uint32_t* tile_bm) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t nwords = words_for(Vp);
-  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < nwords;
-       w += nwarps) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
     if (!bm[w]) continue;
-    const uint64_t r1 = (w * 32 + 32 < Vp) ? w * 32 + 32 : Vp;
-    mark_tile_range(row_off, w * 32, r1, tile_bm, lane);
+    const uint64_t v0 = w * 32, v1 = (v0 + 32 < Vp) ? v0 + 32 : Vp;
+    mark_tile_range(row_off, v0, v1, tile_bm);
   }
 }
 
@@ -130,7 +146,7 @@ void launch_advance(Engine& eng, Part& p, TileSched& ts, uint32_t* next, uint32_
                     unsigned long long* count, unsigned long long* degsum) {
   if (!p.Vp) return;
   const uint64_t nwords = words_for(p.Vp);
-  const unsigned blocks = grid_for(nwords * 32, 256, 148u * 16u);
+  const unsigned blocks = grid_for(nwords, 256, 148u * 16u);
   eng.prof_begin(TG_K_ADVANCE);
   k_advance<<<blocks, 256, 0, eng.stream>>>(next, cur_old, visited, vals, level_val, p.Vp,
                                             p.row_off.get(), ts.bm.get(), count, degsum);

@@ -25,6 +25,25 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
+// sum of contrib[in_col[i]] for i = i0, i0+step, ... < e; four independent
+// column loads then four independent gathers per iteration (memory-level
+// parallelism for the dependent load chain), fp64 accumulation.
+__device__ __forceinline__ double gather_sum(const uint32_t* __restrict__ in_col,
+                                             const float* __restrict__ contrib, uint64_t i,
+                                             uint64_t e, uint32_t step) {
+  double s0 = 0.0, s1 = 0.0;
+  for (; i + 3ull * step < e; i += 4ull * step) {
+    const uint32_t c0 = __ldcs(in_col + i), c1 = __ldcs(in_col + i + step);
+    const uint32_t c2 = __ldcs(in_col + i + 2ull * step), c3 = __ldcs(in_col + i + 3ull * step);
+    const float f0 = __ldg(contrib + c0), f1 = __ldg(contrib + c1);
+    const float f2 = __ldg(contrib + c2), f3 = __ldg(contrib + c3);
+    s0 += (double)f0 + (double)f1;
+    s1 += (double)f2 + (double)f3;
+  }
+  for (; i < e; i += step) s0 += (double)__ldg(contrib + __ldcs(in_col + i));
+  return s0 + s1;
+}
+
 struct PullOut {
   bool fused;
   uint64_t Vp;
@@ -58,8 +77,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off
   __shared__ double s_part[kCtaThreads / 32];
   const uint64_t r = r0 + blockIdx.x;
   const uint64_t b = in_off[r], e = in_off[r + 1];
-  double sum = 0.0;
-  for (uint64_t i = b + threadIdx.x; i < e; i += kCtaThreads) sum += (double)__ldg(contrib + __ldcs(in_col + i));
+  double sum = gather_sum(in_col, contrib, b + threadIdx.x, e, kCtaThreads);
   sum = warp_sum(sum);
   if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = sum;
   __syncthreads();
@@ -79,8 +97,7 @@ __global__ void __launch_bounds__(256) k_pull_warp(const uint64_t* in_off, const
   for (uint64_t r = r0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); r < r1;
        r += nwarps) {
     const uint64_t b = in_off[r], e = in_off[r + 1];
-    double sum = 0.0;
-    for (uint64_t i = b + lane; i < e; i += 32) sum += (double)__ldg(contrib + __ldcs(in_col + i));
+    double sum = gather_sum(in_col, contrib, b + lane, e, 32);
     sum = warp_sum(sum);
     if (lane == 0) o.put(r, sum);
   }
@@ -93,9 +110,7 @@ __global__ void __launch_bounds__(256) k_pull_thread(const uint64_t* in_off, con
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < r1; r += stride) {
     const uint64_t b = in_off[r], e = in_off[r + 1];
-    double sum = 0.0;
-    for (uint64_t i = b; i < e; ++i) sum += (double)__ldg(contrib + __ldcs(in_col + i));
-    o.put(r, sum);
+    o.put(r, gather_sum(in_col, contrib, b, e, 1));
   }
 }
 
