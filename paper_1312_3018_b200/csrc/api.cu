@@ -133,6 +133,25 @@ double time_end(Engine& eng) {
   return (double)ms;
 }
 
+void Engine::l2_window(const void* p, size_t bytes) {
+  if (!l2_enabled || !l2_persist || !l2_max_window) return;
+  cudaStreamAttrValue v{};
+  if (p && bytes) {
+    // the hottest prefix only (hubs first), sized to the set-aside: hitRatio 1
+    size_t win = bytes < l2_max_window ? bytes : l2_max_window;
+    win = win < l2_persist ? win : l2_persist;
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(p);
+    v.accessPolicyWindow.num_bytes = win;
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  } else {
+    v.accessPolicyWindow.num_bytes = 0;
+  }
+  TG_CK(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v));
+  if (!(p && bytes)) TG_CK(cudaCtxResetPersistingL2Cache());
+}
+
 static cudaEvent_t pool_get(Engine& eng) {
   if (!eng.ev_pool.empty()) {
     cudaEvent_t e = eng.ev_pool.back();
@@ -305,6 +324,22 @@ static void init_engine(Engine& eng, const tg_attr* attr) {
   TG_CK(cudaEventCreate(&eng.ev0));
   TG_CK(cudaEventCreate(&eng.ev1));
   TG_CK(cudaMallocHost(&eng.h_counts, sizeof(unsigned long long) * TG_MAX_PARTITIONS * 4));
+  // L2 set-aside for persisting accesses: measured slower on RMAT-28 (the
+  // set-aside starves the rest of the working set), so opt-in only
+  // (TG_L2_WINDOW=1).
+  const char* on = std::getenv("TG_L2_WINDOW");
+  eng.l2_enabled = on && on[0] == '1';
+  int maxp = 0, maxw = 0;
+  cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, eng.device);
+  cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, eng.device);
+  if (eng.l2_enabled && maxp > 0 && maxw > 0) {
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) == cudaSuccess) {
+      eng.l2_persist = (size_t)maxp;
+      eng.l2_max_window = (size_t)maxw;
+    } else {
+      cudaGetLastError();
+    }
+  }
 }
 
 }  // namespace tg

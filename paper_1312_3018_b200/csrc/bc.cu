@@ -180,6 +180,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     int ps;
     uint32_t ls;
     eng.locate(sources[si], &ps, &ls);
+    if (eng.P == 1) eng.l2_window(eng.parts[0]->bcs.sigma.get(), eng.parts[0]->Vp * 8);
     time_begin(eng);
     // ---------------- forward cycle ----------------
     for (auto& pp : eng.parts) {
@@ -262,6 +263,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       TG_REQUIRE(L <= eng.V, TG_EINTERNAL, "tg_bc: superstep bound exceeded");
     }
     // ---------------- backward cycle ----------------
+    if (eng.P == 1) eng.l2_window(eng.parts[0]->bcs.c.get(), eng.parts[0]->Vp * 8);
     for (uint32_t L = maxL; L >= 1; --L) {
       if (L < maxL) {
         if (eng.P > 1) {
@@ -305,6 +307,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       }
     }
     total_ms += time_end(eng);
+    eng.l2_window(nullptr, 0);
     uint64_t nreached = 0;
     const uint64_t tr = reached_outdeg_bitmap(eng, &nreached);
     traversed += 2 * tr;

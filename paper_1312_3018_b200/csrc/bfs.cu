@@ -70,6 +70,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
   cudaStream_t s = eng.stream;
   uint64_t bm_bytes = 0;  // one pass over every partition's vertex bitmap
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
+  if (eng.P == 1) eng.l2_window(eng.parts[0]->fs.visited.get(), words_for(eng.parts[0]->Vp) * 4);
   time_begin(eng);
   reset_vote(eng);
   for (auto& pp : eng.parts) {
@@ -136,6 +137,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
     TG_REQUIRE(supersteps <= eng.V + 1, TG_EINTERNAL, "tg_bfs: superstep bound exceeded");
   }
   const double ms = time_end(eng);
+  eng.l2_window(nullptr, 0);
   if (st) {
     st->device_ms = ms;
     st->supersteps = supersteps;

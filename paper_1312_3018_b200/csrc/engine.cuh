@@ -144,6 +144,11 @@ struct Engine {
   void prof_end(int kid);
   void prof_bytes(int kid, double bytes) { if (prof) kstat[kid].algorithmic_bytes += bytes; }
   void prof_flush();                    // sync + accumulate pending pairs
+  // L2 residency control: the hot prefix of the array a kernel gathers from
+  // (degree-sorted ids put hubs first) is marked persisting in the 126 MB L2.
+  size_t l2_persist = 0, l2_max_window = 0;
+  bool l2_enabled = true;
+  void l2_window(const void* p, size_t bytes);  // bytes == 0 clears the window
   ~Engine();
   uint64_t device_bytes() const;
   // global id -> (partition, local id); one 4-byte D2H read

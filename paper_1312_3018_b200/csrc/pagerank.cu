@@ -214,6 +214,9 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       PRState& r = p.pr;
       PullOut o{eng.P == 1, p.Vp, base, d, r.acc.get(), r.obox.get(), p.in_slot.get(), r.rank.get(),
                 r.contrib[cur ^ 1].get(), p.in_outdeg.get()};
+      // hubs are the first in-order positions: keep the hot prefix of the
+      // gathered contribution array resident in L2
+      if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));
       launch_pull_range(eng, p, r.contrib[cur].get(), 0, p.loc_cta, p.loc_warp, p.Vp, o);
       if (p.S)
         launch_pull_range(eng, p, r.contrib[cur].get(), p.Vp, p.Vp + p.box_cta, p.Vp + p.box_warp,
@@ -245,6 +248,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
     cur ^= 1;
   }
   const double ms = time_end(eng);
+  eng.l2_window(nullptr, 0);
   if (st) {
     st->device_ms = ms;
     st->supersteps = (uint64_t)iters;

@@ -79,6 +79,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   cudaStream_t s = eng.stream;
   uint64_t bm_bytes = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
+  if (eng.P == 1) eng.l2_window(eng.parts[0]->fs.vals.get(), eng.parts[0]->Vp * 4);
   time_begin(eng);
   for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get(), 0, 32, s));
   for (auto& pp : eng.parts) {
@@ -138,6 +139,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     TG_REQUIRE(supersteps <= eng.V + 1, TG_EINTERNAL, "tg_sssp: superstep bound exceeded");
   }
   const double ms = time_end(eng);
+  eng.l2_window(nullptr, 0);
   TG_REQUIRE(read_counts(eng, 2) == 0, TG_EINTERNAL, "tg_sssp: distance overflows uint32");
   if (st) {
     uint64_t nreached = 0;
