@@ -36,8 +36,8 @@ uint64_t Engine::device_bytes() const {
   for (auto& pp : parts) {
     const Part& p = *pp;
     t += b(p.row_off) + b(p.col) + b(p.w) + b(p.global_of) + b(p.tile_vf) + b(p.tile_vl) +
-         b(p.obox_rid) + b(p.ibox_lid) + b(p.in_off) + b(p.in_col) + b(p.in_local) + b(p.in_pos) +
-         b(p.in_slot) + b(p.in_outdeg) + b(p.ibox_inpos);
+         b(p.obox_rid) + b(p.ibox_lid) + b(p.in_off) + b(p.in_col) + b(p.outdeg) + b(p.pr_cta) +
+         b(p.pr_warp) + b(p.in_tile_vf) + b(p.in_tile_vl);
   }
   return t;
 }
@@ -65,8 +65,9 @@ void ensure_frontier_state(Engine& eng) {
     f.obox_u32.alloc(std::max<uint64_t>(p.S, 1));
     f.ibox_bits.alloc(iw);
     f.ibox_u32.alloc(std::max<uint64_t>(p.I, 1));
-    f.counters.alloc(4);
-    p.ts.ensure(p);
+    f.counters.alloc(8);
+    p.ts.ensure(p.ntiles);
+    if (p.in_ntiles) p.ts_in.ensure(p.in_ntiles);
   }
 }
 
@@ -108,19 +109,21 @@ unsigned long long read_counts(Engine& eng, int idx) {
 Vote read_vote(Engine& eng) {
   const int P = (int)eng.parts.size();
   for (int i = 0; i < P; ++i)
-    TG_CK(cudaMemcpyAsync(eng.h_counts + 2 * i, eng.parts[i]->fs.counters.get(), 16,
+    TG_CK(cudaMemcpyAsync(eng.h_counts + 4 * i, eng.parts[i]->fs.counters.get(), 32,
                           cudaMemcpyDeviceToHost, eng.stream));
   TG_CK(cudaStreamSynchronize(eng.stream));
   Vote v;
   for (int i = 0; i < P; ++i) {
-    v.count += eng.h_counts[2 * i];
-    v.edges += eng.h_counts[2 * i + 1];
+    v.count += eng.h_counts[4 * i];
+    v.edges += eng.h_counts[4 * i + 1];
+    v.degsum += eng.h_counts[4 * i + 2];
+    v.indegsum += eng.h_counts[4 * i + 3];
   }
   return v;
 }
 
 void reset_vote(Engine& eng) {
-  for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get(), 0, 16, eng.stream));
+  for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get(), 0, 32, eng.stream));
 }
 
 void time_begin(Engine& eng) { TG_CK(cudaEventRecord(eng.ev0, eng.stream)); }

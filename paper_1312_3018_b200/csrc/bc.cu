@@ -16,6 +16,8 @@
 //   bc[v] += delta[v]; the source (level 0) is never updated (line 34).
 // The backward sum uses the tile kernel in reduce mode: per-row sums in shared
 // memory, rows that span tiles accumulate with fp64 atomics.
+#include <cstdio>
+
 #include "frontier.cuh"
 
 namespace tg {
@@ -68,6 +70,56 @@ struct BcBwdOp {
   __device__ __forceinline__ void vertex_done(uint32_t v, double acc, bool whole) const {
     if (whole) dsum[v] = acc;
     else atomicAdd(&dsum[v], acc);
+  }
+};
+
+// Pull forward superstep for dense levels (direction optimization): every
+// unvisited v sums sigma over its in-neighbours in F[L]; a non-zero sum puts v
+// in F[L+1].  No atomics: the warp owns its word of F[L+1] and each lane its
+// sigma[v].  Same sigma as the push form (integer-valued fp64 sums are exact).
+__global__ void __launch_bounds__(256) k_bc_pull(const uint64_t* in_off, const uint32_t* in_col,
+                                                 const uint32_t* F, const uint32_t* visited,
+                                                 double* sigma, uint32_t* next, uint64_t Vp,
+                                                 unsigned long long* edges) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t nwords = words_for(Vp);
+  unsigned long long cnt = 0;
+  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < nwords; w += nwarps) {
+    const uint32_t vis = visited[w];
+    const uint64_t v = w * 32 + lane;
+    const bool cand = v < Vp && !((vis >> lane) & 1u);
+    if (!__ballot_sync(0xffffffffu, cand)) continue;
+    double s = 0.0;
+    if (cand) {
+      const uint64_t b = in_off[v], e = in_off[v + 1];
+      cnt += e - b;
+      for (uint64_t i = b; i < e; ++i) {
+        const uint32_t u = __ldg(in_col + i);
+        if ((__ldg(F + (u >> 5)) >> (u & 31)) & 1u) s += sigma[u];
+      }
+      if (s > 0.0) sigma[v] = s;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, s > 0.0);
+    if (lane == 0 && m) next[w] = m;
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  if (lane == 0 && cnt) atomicAdd(edges, cnt);
+}
+
+// Backward push over the in-CSR (direction-optimized backward level): for each
+// w in F[L+1] (Aux = c[w]) and in-edge (v, w) with v in F[L]: dsum[v] += c[w].
+struct BcBwdPushOp {
+  using Aux = double;
+  static constexpr bool kReduce = false;
+  const uint32_t* in_col;
+  const uint32_t* FL;
+  const double* c;
+  double* dsum;
+  __device__ __forceinline__ Aux aux(uint32_t w) const { return c[w]; }
+  __device__ __forceinline__ void edge(const Aux& cw, uint64_t e) const {
+    const uint32_t v = __ldcs(in_col + e);
+    if (bit_test(FL, v)) atomicAdd(&dsum[v], cw);
   }
 };
 
@@ -174,6 +226,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
   eng.launches = 0;
   eng.comm_bytes = 0;
   double total_ms = 0;
+  const DirectionPolicy dir = direction_policy(eng);
   uint64_t supersteps = 0, traversed = 0, bytes = 0, bm_bytes = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   for (int si = 0; si < k; ++si) {
@@ -202,12 +255,21 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         k_bc_seed<<<1, 1, 0, s>>>(F0, ls, b.sigma.get());
         eng.launches++;
       }
-      launch_advance(eng, p, p.ts, F0, nullptr, f.visited.get(), nullptr, 0, f.counters.get());
+      launch_advance(eng, p, p.ts, F0, nullptr, f.visited.get(), nullptr, 0, f.counters.get(),
+                     f.counters.get() + 2, f.counters.get() + 3);
     }
     uint32_t maxL = 0;
-    std::vector<uint64_t> lvl_count{1}, lvl_edges;  // |F[L]| and edges of F[L] rows
+    uint64_t reached = 1;
+    std::vector<uint64_t> lvl_count{1};  // |F[L]|
+    const Vote v0 = read_vote(eng);
+    uint64_t mf = v0.degsum, explored = mf;
+    std::vector<uint64_t> lvl_out{v0.degsum}, lvl_in{v0.indegsum};  // degree sums of F[L]
+    bool was_pull = false;
     for (uint32_t L = 0;; ++L) {
       reset_vote(eng);
+      const bool pull = dir.bottom_up(eng, lvl_count[L], mf, eng.E - std::min(explored, eng.E),
+                                      was_pull, dir.bc_alpha);
+      was_pull = pull;
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         FrontierState& f = p.fs;
@@ -215,9 +277,20 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         uint32_t* next = level_bitmap(p, L + 1);
         TG_CK(cudaMemsetAsync(next, 0, words_for(p.Vp) * 4, s));
         launch_compact(eng, p.ts);
-        BcFwdOp op{p.col.get(), f.visited.get(), next, b.sigma.get(), f.obox_mark.get(),
-                   f.obox_new.get(), b.obox_sigma.get()};
-        launch_expand(eng, p, p.ts, b.level_bm[L].get(), op, TG_K_BCF_EXPAND, f.counters.get() + 1);
+        if (pull) {
+          eng.prof_begin(TG_K_BCF_EXPAND);
+          k_bc_pull<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
+              p.in_off.get(), p.in_col.get(), b.level_bm[L].get(), f.visited.get(), b.sigma.get(),
+              next, p.Vp, f.counters.get() + 1);
+          eng.prof_end(TG_K_BCF_EXPAND);
+          TG_CK(cudaGetLastError());
+          eng.launches++;
+        } else {
+          BcFwdOp op{p.col.get(), f.visited.get(), next, b.sigma.get(), f.obox_mark.get(),
+                     f.obox_new.get(), b.obox_sigma.get()};
+          launch_expand(eng, p, p.ts, b.level_bm[L].get(), op, TG_K_BCF_EXPAND,
+                        f.counters.get() + 1);
+        }
       }
       supersteps++;
       if (eng.P > 1) {
@@ -247,14 +320,28 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         Part& p = *pp;
         FrontierState& f = p.fs;
         launch_advance(eng, p, p.ts, p.bcs.level_bm[L + 1].get(), nullptr, f.visited.get(), nullptr,
-                       0, f.counters.get());
+                       0, f.counters.get(), f.counters.get() + 2, f.counters.get() + 3);
       }
       const Vote v = read_vote(eng);
-      // forward expand: col 4 per edge; offsets 16 + sigma[v] 8 per frontier
-      // vertex; sigma[t] 8 per newly reached vertex; 3 bitmap passes
-      eng.prof_bytes(TG_K_BCF_EXPAND,
-                     4.0 * v.edges + 24.0 * lvl_count[L] + 8.0 * v.count + 3.0 * bm_bytes);
-      lvl_edges.push_back(v.edges);
+      mf = v.degsum;
+      explored += mf;
+      lvl_out.push_back(v.degsum);
+      lvl_in.push_back(v.indegsum);
+      if (dir.trace)
+        std::fprintf(stderr, "[tg bc] L=%u %s frontier=%llu edges=%llu next=%llu\n", L,
+                     pull ? "pull" : "push", (unsigned long long)lvl_count[L],
+                     (unsigned long long)v.edges, (unsigned long long)v.count);
+      // push: col 4 per edge; offsets 16 + sigma[v] 8 per frontier vertex;
+      // sigma[t] 8 per newly reached vertex; 3 bitmap passes.  pull: in_col 4
+      // per examined in-edge; in-offsets 16 per unvisited vertex; sigma 8 per
+      // newly reached vertex; 3 bitmap passes
+      if (pull)
+        eng.prof_bytes(TG_K_BCF_EXPAND, 4.0 * v.edges + 16.0 * (eng.V - reached) + 8.0 * v.count +
+                                            3.0 * bm_bytes);
+      else
+        eng.prof_bytes(TG_K_BCF_EXPAND,
+                       4.0 * v.edges + 24.0 * lvl_count[L] + 8.0 * v.count + 3.0 * bm_bytes);
+      reached += v.count;
       lvl_count.push_back(v.count);
       if (v.count == 0) {
         maxL = L;  // F[L+1] is empty
@@ -264,6 +351,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     }
     // ---------------- backward cycle ----------------
     if (eng.P == 1) eng.l2_window(eng.parts[0]->bcs.c.get(), eng.parts[0]->Vp * 8);
+    reset_vote(eng);  // counters[1] accumulates the backward edges
     for (uint32_t L = maxL; L >= 1; --L) {
       if (L < maxL) {
         if (eng.P > 1) {
@@ -278,22 +366,37 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           TG_CK(cudaGetLastError());
           exchange(eng, send_pack, recv_ghost, 8, true);
         }
+        // direction per level: pull over the out-edges of F[L] (cost ~ their
+        // count) or push c[w] over the in-edges of F[L+1] (fp64 atomics, ~2x
+        // per edge) -- whichever touches fewer edges
+        const bool push = eng.P == 1 && dir.mode != 1 && eng.parts[0]->in_ntiles &&
+                          (dir.mode == 2 || 2 * lvl_in[L + 1] < lvl_out[L]);
         for (auto& pp : eng.parts) {
           Part& p = *pp;
-          if (!p.ntiles) continue;
-          k_mark_tiles<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
-              p.bcs.level_bm[L].get(), p.Vp, p.row_off.get(), p.ts.bm.get());
-          TG_CK(cudaGetLastError());
-          eng.launches++;
-          launch_compact(eng, p.ts);
-          BcBwdOp op{p.col.get(), p.bcs.level_bm[L + 1].get(), p.bcs.c.get(), p.bcs.ghost.get(),
-                     p.bcs.dsum.get()};
-          launch_expand(eng, p, p.ts, p.bcs.level_bm[L].get(), op, TG_K_BCB_EXPAND, nullptr);
+          if (push) {
+            launch_mark_tiles(eng, in_tiles(p), p.Vp, p.bcs.level_bm[L + 1].get(), p.ts_in);
+            launch_compact(eng, p.ts_in);
+            BcBwdPushOp op{p.in_col.get(), p.bcs.level_bm[L].get(), p.bcs.c.get(), p.bcs.dsum.get()};
+            launch_expand_on(eng, in_tiles(p), p.ts_in, p.bcs.level_bm[L + 1].get(), op,
+                             TG_K_BCB_EXPAND, p.fs.counters.get() + 1);
+          } else {
+            if (!p.ntiles) continue;
+            launch_mark_tiles(eng, out_tiles(p), p.Vp, p.bcs.level_bm[L].get(), p.ts);
+            launch_compact(eng, p.ts);
+            BcBwdOp op{p.col.get(), p.bcs.level_bm[L + 1].get(), p.bcs.c.get(), p.bcs.ghost.get(),
+                       p.bcs.dsum.get()};
+            launch_expand(eng, p, p.ts, p.bcs.level_bm[L].get(), op, TG_K_BCB_EXPAND,
+                          p.fs.counters.get() + 1);
+          }
         }
-        // backward expand: col 4 per edge; c 8 per successor (read once);
-        // offsets 16 + dsum 8 per level-L vertex; level + successor bitmaps
-        eng.prof_bytes(TG_K_BCB_EXPAND, 4.0 * lvl_edges[L] + 8.0 * lvl_count[L + 1] +
-                                            24.0 * lvl_count[L] + 2.0 * bm_bytes);
+        if (dir.trace)
+          std::fprintf(stderr, "[tg bc-bwd] L=%u %s out(F[L])=%llu in(F[L+1])=%llu\n", L,
+                       push ? "push" : "pull", (unsigned long long)lvl_out[L],
+                       (unsigned long long)lvl_in[L + 1]);
+        // backward expand: c 8 per successor (read once); offsets 16 + dsum 8
+        // per level-L vertex; level + successor bitmaps (+ 4 B per edge below)
+        eng.prof_bytes(TG_K_BCB_EXPAND,
+                       8.0 * lvl_count[L + 1] + 24.0 * lvl_count[L] + 2.0 * bm_bytes);
         supersteps++;
       }
       for (auto& pp : eng.parts) {
@@ -308,6 +411,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     }
     total_ms += time_end(eng);
     eng.l2_window(nullptr, 0);
+    eng.prof_bytes(TG_K_BCB_EXPAND, 4.0 * read_vote(eng).edges);
     uint64_t nreached = 0;
     const uint64_t tr = reached_outdeg_bitmap(eng, &nreached);
     traversed += 2 * tr;

@@ -14,6 +14,8 @@
 //             (totem_engine_scatter_inbox_min).
 //   advance : next bitmap -> level[v] = L+1, visited |= next, vote count
 //             (termination when every partition's count is 0).
+#include <cstdio>
+
 #include "frontier.cuh"
 
 namespace tg {
@@ -54,6 +56,42 @@ __global__ void k_bfs_scatter(const uint32_t* ibits, const uint32_t* lid, uint64
   }
 }
 
+// Bottom-up superstep (direction-optimizing BFS):
+// every unvisited vertex scans its in-edges until it finds a parent in the
+// current frontier.  One warp per visited-bitmap word, one lane per vertex; the
+// warp owns its word of `next`, so no atomics.  Same levels as top-down.
+__global__ void __launch_bounds__(256) k_bfs_bottom_up(const uint64_t* in_off,
+                                                       const uint32_t* in_col, const uint32_t* cur,
+                                                       const uint32_t* visited, uint32_t* next,
+                                                       uint64_t Vp, unsigned long long* edges) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t nwords = words_for(Vp);
+  unsigned long long cnt = 0;
+  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < nwords; w += nwarps) {
+    const uint32_t vis = visited[w];
+    const uint64_t v = w * 32 + lane;
+    const bool cand = v < Vp && !((vis >> lane) & 1u);
+    if (!__ballot_sync(0xffffffffu, cand)) continue;
+    bool found = false;
+    if (cand) {
+      const uint64_t b = in_off[v], e = in_off[v + 1];
+      for (uint64_t i = b; i < e; ++i) {
+        const uint32_t u = __ldg(in_col + i);
+        cnt++;
+        if ((__ldg(cur + (u >> 5)) >> (u & 31)) & 1u) {
+          found = true;
+          break;
+        }
+      }
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, found);
+    if (lane == 0 && m) next[w] = m;
+  }
+  for (int o = 16; o; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  if (lane == 0 && cnt) atomicAdd(edges, cnt);
+}
+
 void* send_onew(Part& p) { return p.fs.obox_new.get(); }
 void* recv_ibits(Part& p) { return p.fs.ibox_bits.get(); }
 
@@ -68,6 +106,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
   eng.launches = 0;
   eng.comm_bytes = 0;
   cudaStream_t s = eng.stream;
+  uint64_t visited_total = 1;
   uint64_t bm_bytes = 0;  // one pass over every partition's vertex bitmap
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   if (eng.P == 1) eng.l2_window(eng.parts[0]->fs.visited.get(), words_for(eng.parts[0]->Vp) * 4);
@@ -90,19 +129,37 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
       eng.launches++;
     }
     launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), f.visited.get(), f.vals.get(), 0,
-                   f.counters.get());
+                   f.counters.get(), f.counters.get() + 2);
     std::swap(f.cur, f.next);
   }
-  uint64_t supersteps = 0, frontier = 1, edges_total = 0;
+  const DirectionPolicy dir = direction_policy(eng);
+  uint64_t supersteps = 0, frontier = 1, edges_total = 0, bu_steps = 0;
+  uint64_t mf = dir.mode == 1 ? 0 : read_vote(eng).degsum;  // out-edges of the frontier
+  uint64_t explored = mf;
+  bool was_bu = false;
   for (uint32_t L = 0;; ++L) {
     reset_vote(eng);
+    const bool bottom_up =
+        dir.bottom_up(eng, frontier, mf, eng.E - std::min(explored, eng.E), was_bu, dir.alpha);
+    was_bu = bottom_up;
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       FrontierState& f = p.fs;
-      launch_compact(eng, p.ts);
-      BfsOp op{p.col.get(), f.visited.get(), f.next.get(), f.obox_mark.get(), f.obox_new.get()};
-      launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_BFS_EXPAND, f.counters.get() + 1);
+      launch_compact(eng, p.ts);  // drains the tile marks even when unused
+      if (bottom_up) {
+        eng.prof_begin(TG_K_BFS_EXPAND);
+        k_bfs_bottom_up<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
+            p.in_off.get(), p.in_col.get(), f.cur.get(), f.visited.get(), f.next.get(), p.Vp,
+            f.counters.get() + 1);
+        eng.prof_end(TG_K_BFS_EXPAND);
+        TG_CK(cudaGetLastError());
+        eng.launches++;
+      } else {
+        BfsOp op{p.col.get(), f.visited.get(), f.next.get(), f.obox_mark.get(), f.obox_new.get()};
+        launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_BFS_EXPAND, f.counters.get() + 1);
+      }
     }
+    bu_steps += bottom_up;
     supersteps++;
     if (eng.P > 1) {
       eng.prof_begin(TG_K_EXCHANGE);
@@ -124,13 +181,25 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
       Part& p = *pp;
       FrontierState& f = p.fs;
       launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), f.visited.get(), f.vals.get(), L + 1,
-                     f.counters.get());
+                     f.counters.get(), dir.mode == 1 ? nullptr : f.counters.get() + 2);
       std::swap(f.cur, f.next);
     }
     const Vote v = read_vote(eng);
-    // expand: 4 B col per edge, 16 B row offsets per frontier vertex, frontier +
-    // visited + next bitmaps one pass each
-    eng.prof_bytes(TG_K_BFS_EXPAND, 4.0 * v.edges + 16.0 * frontier + 3.0 * bm_bytes);
+    mf = v.degsum;
+    explored += mf;
+    // top-down: 4 B col per edge, 16 B row offsets per frontier vertex, frontier +
+    // visited + next bitmaps one pass each; bottom-up: 4 B in_col per examined
+    // in-edge, 16 B in-offsets per unvisited vertex
+    if (bottom_up)
+      eng.prof_bytes(TG_K_BFS_EXPAND, 4.0 * v.edges + 16.0 * (eng.V - visited_total) + 3.0 * bm_bytes);
+    else
+      eng.prof_bytes(TG_K_BFS_EXPAND, 4.0 * v.edges + 16.0 * frontier + 3.0 * bm_bytes);
+    visited_total += v.count;
+    if (dir.trace)
+      std::fprintf(stderr, "[tg bfs] L=%u %s frontier=%llu edges=%llu next=%llu next_mf=%llu\n",
+                   L, bottom_up ? "bottom-up" : "top-down", (unsigned long long)frontier,
+                   (unsigned long long)v.edges, (unsigned long long)v.count,
+                   (unsigned long long)v.degsum);
     edges_total += v.edges;
     frontier = v.count;
     if (v.count == 0) break;  // termination vote
@@ -143,7 +212,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
     st->supersteps = supersteps;
     uint64_t nreached = 0;
     st->traversed_edges = reached_outdeg_u32(eng, &nreached);
-    TG_REQUIRE(st->traversed_edges == edges_total, TG_EINTERNAL,
+    TG_REQUIRE(bu_steps || st->traversed_edges == edges_total, TG_EINTERNAL,
                "tg_bfs: expanded edges != sum of reached out-degrees");
     // 4 B per traversed edge (col), 16 B row offsets + 4 B level write per
     // reached vertex, three bitmap passes (frontier, next, visited) per superstep.

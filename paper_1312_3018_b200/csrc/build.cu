@@ -227,54 +227,41 @@ __global__ void k_in_count(const uint64_t* row_off, const uint32_t* col, uint64_
   }
 }
 
-__global__ void k_scatter_pos(const uint32_t* vals, uint64_t n, uint64_t base, uint32_t* pos_of) {
+// in-degree -> u64 degrees for the scan + degree-class row lists (PageRank)
+__global__ void k_in_deg64(const uint32_t* indeg, uint64_t n, uint64_t* deg64) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    pos_of[vals[i]] = (uint32_t)(base + i);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= n; i += stride)
+    deg64[i] = i < n ? indeg[i] : 0ull;
 }
 
-__global__ void k_in_deg_sorted(const uint32_t* keys_sorted, uint64_t n, uint64_t base,
-                                uint64_t* deg64, unsigned long long* cls, uint32_t t_cta) {
+__global__ void k_class_list(const uint32_t* indeg, uint64_t n, uint32_t lo, uint32_t hi,
+                             uint32_t* list, unsigned long long* count) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  unsigned long long c_cta = 0, c_warp = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t d = ~keys_sorted[i];
-    deg64[base + i] = d;
-    c_cta += d >= t_cta;
-    c_warp += d >= 32;
+    const uint32_t d = indeg[i];
+    if (d >= lo && d < hi) list[atomicAdd(count, 1ull)] = (uint32_t)i;
   }
-  block_add_u64(&cls[0], c_cta);
-  block_add_u64(&cls[1], c_warp);
 }
 
+// in-CSR fill: row = local target (or Vp + outbox slot), entry = local source
 __global__ void k_in_fill(const uint64_t* row_off, const uint32_t* col, uint64_t Ep, uint64_t Vp,
-                          const uint32_t* vf, const uint32_t* vl, const uint32_t* in_pos,
-                          const uint32_t* slot_pos, const uint64_t* in_off, uint32_t* cursor,
-                          uint32_t* in_col) {
+                          const uint32_t* vf, const uint32_t* vl, const uint64_t* in_off,
+                          uint32_t* cursor, uint32_t* in_col) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < Ep; e += stride) {
     const uint64_t tile = e / kTile;
     const uint32_t l = row_of_edge(row_off, vf[tile], vl[tile], e);
     const uint32_t t = col[e];
-    const uint32_t r = (t & kRemote) ? slot_pos[t & ~kRemote] : in_pos[t];
+    const uint64_t r = (t & kRemote) ? Vp + (t & ~kRemote) : t;
     const uint64_t pos = in_off[r] + atomicAdd(&cursor[r], 1u);
-    in_col[pos] = in_pos[l];
+    in_col[pos] = l;
   }
 }
 
-__global__ void k_in_outdeg(const uint64_t* row_off, const uint32_t* in_local, uint64_t Vp,
-                            uint32_t* in_outdeg) {
+__global__ void k_outdeg_local(const uint64_t* row_off, uint64_t Vp, uint32_t* outdeg) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride) {
-    const uint32_t l = in_local[i];
-    in_outdeg[i] = (uint32_t)(row_off[l + 1] - row_off[l]);
-  }
-}
-
-__global__ void k_ibox_inpos(const uint32_t* lid, uint64_t n, const uint32_t* in_pos, uint32_t* out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-    out[i] = lid[i] == kInf ? kInf : in_pos[lid[i]];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride)
+    outdeg[i] = (uint32_t)(row_off[i + 1] - row_off[i]);
 }
 
 template <typename T>
@@ -522,56 +509,61 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
                                          pt.tile_vf.get(), pt.tile_vl.get(), indeg.get());
       TG_CK(cudaGetLastError());
     }
-    DevBuf<uint32_t> keys(std::max<uint64_t>(R, 1)), keys_out(std::max<uint64_t>(R, 1));
-    DevBuf<uint32_t> vals(std::max<uint64_t>(R, 1));
-    pt.in_local.alloc(std::max<uint64_t>(Vp, 1));
-    pt.in_pos.alloc(std::max<uint64_t>(Vp, 1));
-    pt.in_slot.alloc(std::max<uint64_t>(pt.S, 1));
-    DevBuf<uint32_t> slot_pos(std::max<uint64_t>(pt.S, 1));
-    // keys = ~indeg, vals = iota (per range)
-    k_neg_iota<<<G(Vp), kB, 0, s>>>(indeg.get(), Vp, keys.get(), vals.get());
-    if (pt.S) k_neg_iota<<<G(pt.S), kB, 0, s>>>(indeg.get() + Vp, pt.S, keys.get() + Vp, vals.get() + Vp);
-    TG_CK(cudaGetLastError());
-    if (Vp) sort_pairs_u32(keys.get(), keys_out.get(), vals.get(), pt.in_local.get(), Vp, s);
-    if (pt.S)
-      sort_pairs_u32(keys.get() + Vp, keys_out.get() + Vp, vals.get() + Vp, pt.in_slot.get(), pt.S, s);
-    k_scatter_pos<<<G(Vp), kB, 0, s>>>(pt.in_local.get(), Vp, 0, pt.in_pos.get());
-    if (pt.S) k_scatter_pos<<<G(pt.S), kB, 0, s>>>(pt.in_slot.get(), pt.S, Vp, slot_pos.get());
-    TG_CK(cudaGetLastError());
+    // rows stay in local-id order (out-degree order: the gathered side of a
+    // pull is the source, so hubs -- the hot sources -- are a compact prefix)
     DevBuf<uint64_t> deg64(R + 1);
-    TG_CK(cudaMemsetAsync(deg64.get(), 0, deg64.bytes(), s));
-    DevBuf<unsigned long long> cls(4);
-    TG_CK(cudaMemsetAsync(cls.get(), 0, cls.bytes(), s));
-    k_in_deg_sorted<<<G(Vp), kB, 0, s>>>(keys_out.get(), Vp, 0, deg64.get(), cls.get(), kPrCta);
-    if (pt.S)
-      k_in_deg_sorted<<<G(pt.S), kB, 0, s>>>(keys_out.get() + Vp, pt.S, Vp, deg64.get(),
-                                             cls.get() + 2, kPrCta);
+    k_in_deg64<<<G(R + 1), kB, 0, s>>>(indeg.get(), R, deg64.get());
     TG_CK(cudaGetLastError());
-    unsigned long long hc[4];
-    TG_CK(cudaMemcpyAsync(hc, cls.get(), sizeof(hc), cudaMemcpyDeviceToHost, s));
-    TG_CK(cudaStreamSynchronize(s));
-    pt.loc_cta = hc[0];
-    pt.loc_warp = hc[1];
-    pt.box_cta = hc[2];
-    pt.box_warp = hc[3];
     pt.in_off.alloc(R + 1);
     exclusive_scan_u64(deg64.get(), pt.in_off.get(), R + 1, s);
     deg64.release();
-    keys.release();
-    keys_out.release();
+    // degree-class row lists for the PageRank pull (CTA / warp classes)
+    {
+      DevBuf<unsigned long long> cnt2(2);
+      TG_CK(cudaMemsetAsync(cnt2.get(), 0, 16, s));
+      DevBuf<uint32_t> lc(std::max<uint64_t>(R, 1)), lw(std::max<uint64_t>(R, 1));
+      k_class_list<<<G(R), kB, 0, s>>>(indeg.get(), R, kPrCta, 0xFFFFFFFFu, lc.get(), cnt2.get());
+      k_class_list<<<G(R), kB, 0, s>>>(indeg.get(), R, 32u, kPrCta, lw.get(), cnt2.get() + 1);
+      TG_CK(cudaGetLastError());
+      unsigned long long hc[2];
+      TG_CK(cudaMemcpyAsync(hc, cnt2.get(), 16, cudaMemcpyDeviceToHost, s));
+      TG_CK(cudaStreamSynchronize(s));
+      pt.n_cta = hc[0];
+      pt.n_warp = hc[1];
+      pt.pr_cta.alloc(std::max<uint64_t>(pt.n_cta, 1));
+      pt.pr_warp.alloc(std::max<uint64_t>(pt.n_warp, 1));
+      auto sort_list = [&](DevBuf<uint32_t>& src, DevBuf<uint32_t>& dst, uint64_t n) {
+        if (!n) return;
+        size_t tmp = 0;
+        TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, src.get(), dst.get(), (int)n, 0, 32, s));
+        DevBuf<uint8_t> t(tmp ? tmp : 1);
+        TG_CK(cub::DeviceRadixSort::SortKeys(t.get(), tmp, src.get(), dst.get(), (int)n, 0, 32, s));
+      };
+      sort_list(lc, pt.pr_cta, pt.n_cta);   // ascending row ids: coalesced output writes
+      sort_list(lw, pt.pr_warp, pt.n_warp);
+    }
     pt.in_col.alloc(std::max<uint64_t>(pt.Ep, 1));
     TG_CK(cudaMemsetAsync(indeg.get(), 0, indeg.bytes(), s));  // reuse as cursor
     if (pt.Ep) {
       k_in_fill<<<G(pt.Ep), kB, 0, s>>>(pt.row_off.get(), pt.col.get(), pt.Ep, Vp, pt.tile_vf.get(),
-                                        pt.tile_vl.get(), pt.in_pos.get(), slot_pos.get(),
-                                        pt.in_off.get(), indeg.get(), pt.in_col.get());
+                                        pt.tile_vl.get(), pt.in_off.get(), indeg.get(),
+                                        pt.in_col.get());
       TG_CK(cudaGetLastError());
     }
     indeg.release();
-    slot_pos.release();
     sort_rows(pt.in_off.get(), R, pt.in_col.get(), nullptr, s);
-    pt.in_outdeg.alloc(std::max<uint64_t>(Vp, 1));
-    k_in_outdeg<<<G(Vp), kB, 0, s>>>(pt.row_off.get(), pt.in_local.get(), Vp, pt.in_outdeg.get());
+    // edge tiles over the local rows of the in-CSR (BC backward push)
+    pt.in_E_local = Vp ? d2h(pt.in_off.get() + Vp, s) : 0;
+    pt.in_ntiles = (pt.in_E_local + kTile - 1) / kTile;
+    pt.in_tile_vf.alloc(std::max<uint64_t>(pt.in_ntiles, 1));
+    pt.in_tile_vl.alloc(std::max<uint64_t>(pt.in_ntiles, 1));
+    if (pt.in_ntiles) {
+      k_tiles<<<G(pt.in_ntiles), kB, 0, s>>>(pt.in_off.get(), Vp, pt.in_E_local, pt.in_ntiles,
+                                             pt.in_tile_vf.get(), pt.in_tile_vl.get());
+      TG_CK(cudaGetLastError());
+    }
+    pt.outdeg.alloc(std::max<uint64_t>(Vp, 1));
+    k_outdeg_local<<<G(Vp), kB, 0, s>>>(pt.row_off.get(), Vp, pt.outdeg.get());
     TG_CK(cudaGetLastError());
   }
   TG_CK(cudaStreamSynchronize(s));
@@ -641,14 +633,6 @@ void build_engine(Engine& eng, const EdgeInput& in) {
       if (n)
         TG_CK(cudaMemcpyAsync(qt->ibox_lid.get() + qt->ibox_off[p], pp.obox_rid.get() + pp.obox_off[q],
                               n * 4, cudaMemcpyDeviceToDevice, s));
-    }
-    if (qt->has_in) {
-      qt->ibox_inpos.alloc(std::max<uint64_t>(qt->I, 1));
-      if (qt->I) {
-        k_ibox_inpos<<<G(qt->I), kB, 0, s>>>(qt->ibox_lid.get(), qt->I, qt->in_pos.get(),
-                                             qt->ibox_inpos.get());
-        TG_CK(cudaGetLastError());
-      }
     }
   }
   for (auto& pt : eng.parts) {

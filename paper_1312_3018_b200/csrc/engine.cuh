@@ -16,9 +16,10 @@
 //   * edge tiles: the edge array is cut into tiles of kTile edges; tile t knows
 //     the first/last row it touches, so a frontier kernel is load balanced over
 //     edges whatever the degree skew (hubs span many tiles);
-//   * PageRank in-CSR in its own "in-order" index space (rows sorted by
-//     in-degree): rows [0,Vp) are local vertices, rows [Vp,Vp+S) are outbox
-//     slots (their sums are the partition's partial-sum messages).
+//   * in-CSR (PageRank pull, bottom-up BFS, pull-sigma BC): rows [0,Vp) are
+//     local vertices in local-id order, rows [Vp,Vp+S) are outbox slots (their
+//     PageRank sums are the partition's partial-sum messages); entries are the
+//     local ids of the sources, each row sorted ascending.
 #pragma once
 
 #include <memory>
@@ -54,7 +55,7 @@ struct TileSched {
   DevBuf<uint32_t> list;  // compacted active tiles
   DevBuf<unsigned long long> count;
   uint64_t nwords = 0;
-  void ensure(const Part& p);
+  void ensure(uint64_t ntiles);
 };
 
 struct PRState {  // PageRank (in-order space)
@@ -101,16 +102,16 @@ struct Part {
   bool has_in = false;
   DevBuf<uint64_t> in_off;          // Vp + S + 1
   DevBuf<uint32_t> in_col;          // in-order position of the local source
-  DevBuf<uint32_t> in_local;        // in-order position -> local id (Vp)
-  DevBuf<uint32_t> in_pos;          // local id -> in-order position (Vp)
-  DevBuf<uint32_t> in_slot;         // outbox row r (0..S) -> slot
-  DevBuf<uint32_t> in_outdeg;       // out-degree of the vertex at in-position (Vp)
-  DevBuf<uint32_t> ibox_inpos;      // inbox entry -> in-order position (I)
-  uint64_t loc_cta = 0, loc_warp = 0;  // class ends of local rows
-  uint64_t box_cta = 0, box_warp = 0;  // class ends of outbox rows (relative)
+  DevBuf<uint32_t> outdeg;          // out-degree per local id (Vp)
+  uint64_t in_E_local = 0;          // in-edges of the local rows [0, Vp)
+  uint64_t in_ntiles = 0;           // edge tiles of the in-CSR local rows
+  DevBuf<uint32_t> in_tile_vf, in_tile_vl;
+  DevBuf<uint32_t> pr_cta, pr_warp; // in-CSR rows with in-degree >= 2048 / in [32, 2048)
+  uint64_t n_cta = 0, n_warp = 0;
   std::vector<uint64_t> seg_real;  // real (unpadded) outbox slots per peer
   // algorithm state (lazily allocated)
-  TileSched ts;
+  TileSched ts;     // tiles of the out-CSR
+  TileSched ts_in;  // tiles of the in-CSR (BC backward push)
   FrontierState fs;
   PRState pr;
   BCState bcs;
@@ -189,9 +190,10 @@ void ensure_frontier_state(Engine& eng);
 // read the per-partition counters[idx] (one sync) and return their sum
 unsigned long long read_counts(Engine& eng, int idx);
 // counters layout: [0] new-frontier count (advance), [1] edges processed by the
-// superstep's expand, [2] error flags, [3] spare.  One sync for all partitions.
+// superstep's expand, [2] out-degree sum of the new frontier, [3] its in-degree
+// sum, [4] error flags.  One sync for all partitions.
 struct Vote {
-  unsigned long long count = 0, edges = 0;
+  unsigned long long count = 0, edges = 0, degsum = 0, indegsum = 0;
 };
 Vote read_vote(Engine& eng);
 // zero counters[0..1] of every partition (start of a superstep)

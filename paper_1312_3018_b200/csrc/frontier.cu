@@ -1,4 +1,7 @@
 // frontier.cu -- tile scheduling and frontier advance kernels (see frontier.cuh).
+#include <cstdlib>
+#include <cstring>
+
 #include "frontier.cuh"
 
 namespace tg {
@@ -58,10 +61,11 @@ __device__ __forceinline__ void block_add(unsigned long long* dst, unsigned long
 __global__ void k_advance(uint32_t* next, uint32_t* cur_old, uint32_t* visited, uint32_t* vals,
                           uint32_t level_val, uint64_t Vp, const uint64_t* row_off,
                           uint32_t* tile_bm, unsigned long long* count,
-                          unsigned long long* degsum) {
+                          unsigned long long* degsum, const uint64_t* in_off,
+                          unsigned long long* indegsum) {
   const uint64_t nwords = words_for(Vp);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  unsigned long long cnt = 0, dsum = 0;
+  unsigned long long cnt = 0, dsum = 0, isum = 0;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
     uint32_t x = next[w];
     if (cur_old) cur_old[w] = 0;
@@ -70,7 +74,30 @@ __global__ void k_advance(uint32_t* next, uint32_t* cur_old, uint32_t* visited, 
     if (visited) visited[w] |= x;
     const uint64_t v0 = w * 32;
     const uint64_t v1 = (v0 + 32 < Vp) ? v0 + 32 : Vp;
-    if (degsum) dsum += row_off[v1] - row_off[v0];  // upper bound (whole word), diagnostics
+    if (degsum) {  // exact out-degree sum of the new frontier (direction choice)
+      if (x == 0xFFFFFFFFu) {
+        dsum += row_off[v1] - row_off[v0];
+      } else {
+        uint32_t y = x;
+        while (y) {
+          const int b = __ffs(y) - 1;
+          y &= y - 1;
+          dsum += row_off[v0 + b + 1] - row_off[v0 + b];
+        }
+      }
+    }
+    if (indegsum) {  // exact in-degree sum (BC backward direction choice)
+      if (x == 0xFFFFFFFFu) {
+        isum += in_off[v1] - in_off[v0];
+      } else {
+        uint32_t y = x;
+        while (y) {
+          const int b = __ffs(y) - 1;
+          y &= y - 1;
+          isum += in_off[v0 + b + 1] - in_off[v0 + b];
+        }
+      }
+    }
     if (vals) {
       if (x == 0xFFFFFFFFu && v0 + 32 <= Vp) {
         uint4* p = reinterpret_cast<uint4*>(vals + v0);
@@ -89,6 +116,7 @@ __global__ void k_advance(uint32_t* next, uint32_t* cur_old, uint32_t* visited, 
   }
   block_add(count, cnt);
   if (degsum) block_add(degsum, dsum);
+  if (indegsum) block_add(indegsum, isum);
 }
 
 __global__ void k_mark_tiles(const uint32_t* bm, uint64_t Vp, const uint64_t* row_off,
@@ -107,14 +135,27 @@ __global__ void k_seed(uint32_t* bm, uint32_t i, uint32_t* vals, uint32_t val) {
   if (vals) vals[i] = val;
 }
 
-void TileSched::ensure(const Part& p) {
-  const uint64_t nw = words_for(p.ntiles);
-  if (list.n >= std::max<uint64_t>(p.ntiles, 1) && bm.n >= std::max<uint64_t>(nw, 1)) return;
+void TileSched::ensure(uint64_t ntiles) {
+  const uint64_t nw = words_for(ntiles);
+  if (list.n >= std::max<uint64_t>(ntiles, 1) && bm.n >= std::max<uint64_t>(nw, 1)) return;
   bm.alloc(std::max<uint64_t>(nw, 1));
-  list.alloc(std::max<uint64_t>(p.ntiles, 1));
+  list.alloc(std::max<uint64_t>(ntiles, 1));
   count.alloc(1);
   nwords = nw;
   TG_CK(cudaMemset(bm.get(), 0, bm.bytes()));
+}
+
+DirectionPolicy direction_policy(const Engine&) {
+  DirectionPolicy d;
+  if (const char* m = std::getenv("TG_DIRECTION")) {
+    if (!std::strcmp(m, "top")) d.mode = 1;
+    else if (!std::strcmp(m, "bottom")) d.mode = 2;
+  }
+  if (const char* t = std::getenv("TG_TRACE")) d.trace = t[0] == '1';
+  if (const char* v = std::getenv("TG_BU_ALPHA")) d.alpha = std::atof(v);
+  if (const char* v = std::getenv("TG_BC_ALPHA")) d.bc_alpha = std::atof(v);
+  if (const char* v = std::getenv("TG_BU_BETA")) d.beta = std::atof(v);
+  return d;
 }
 
 static int g_num_sms = 0;
@@ -141,15 +182,26 @@ void launch_compact(Engine& eng, TileSched& ts) {
   eng.launches++;
 }
 
+void launch_mark_tiles(Engine& eng, const CsrTiles& c, uint64_t Vp, const uint32_t* bm,
+                       TileSched& ts) {
+  if (!c.ntiles || !Vp) return;
+  k_mark_tiles<<<grid_for(words_for(Vp), 256, 148u * 16u), 256, 0, eng.stream>>>(
+      bm, Vp, c.row_off, ts.bm.get());
+  TG_CK(cudaGetLastError());
+  eng.launches++;
+}
+
 void launch_advance(Engine& eng, Part& p, TileSched& ts, uint32_t* next, uint32_t* cur_old,
                     uint32_t* visited, uint32_t* vals, uint32_t level_val,
-                    unsigned long long* count, unsigned long long* degsum) {
+                    unsigned long long* count, unsigned long long* degsum,
+                    unsigned long long* indegsum) {
   if (!p.Vp) return;
   const uint64_t nwords = words_for(p.Vp);
   const unsigned blocks = grid_for(nwords, 256, 148u * 16u);
   eng.prof_begin(TG_K_ADVANCE);
   k_advance<<<blocks, 256, 0, eng.stream>>>(next, cur_old, visited, vals, level_val, p.Vp,
-                                            p.row_off.get(), ts.bm.get(), count, degsum);
+                                            p.row_off.get(), ts.bm.get(), count, degsum,
+                                            p.in_off.get(), p.has_in ? indegsum : nullptr);
   eng.prof_end(TG_K_ADVANCE);
   // next read + cur_old clear + visited RMW, one pass each
   eng.prof_bytes(TG_K_ADVANCE, 4.0 * nwords * (1 + (cur_old ? 1 : 0) + (visited ? 2 : 0)));

@@ -146,7 +146,8 @@ __global__ void k_tile_compact(uint32_t* tile_bm, uint64_t nwords, uint32_t* lis
 __global__ void k_advance(uint32_t* next, uint32_t* cur_old, uint32_t* visited, uint32_t* vals,
                           uint32_t level_val, uint64_t Vp, const uint64_t* row_off,
                           uint32_t* tile_bm, unsigned long long* count,
-                          unsigned long long* degsum);
+                          unsigned long long* degsum, const uint64_t* in_off,
+                          unsigned long long* indegsum);
 
 // mark the tiles touched by the rows set in `bm`
 __global__ void k_mark_tiles(const uint32_t* bm, uint64_t Vp, const uint64_t* row_off,
@@ -155,19 +156,68 @@ __global__ void k_mark_tiles(const uint32_t* bm, uint64_t Vp, const uint64_t* ro
 // set bit i of bm and (optionally) vals[i] = val
 __global__ void k_seed(uint32_t* bm, uint32_t i, uint32_t* vals, uint32_t val);
 
+// Direction optimization (Beamer et al. 2013, cited at
+// PAPER.md:767): switch top-down -> bottom-up when the frontier's out-edges m_f
+// exceed (edges not yet explored m_u) / alpha, and back when the frontier holds
+// fewer than V/beta vertices.  Single-partition engines with an in-CSR only.
+// Env overrides: TG_DIRECTION=top|bottom|auto, TG_BU_ALPHA (BFS, 14),
+// TG_BC_ALPHA (BC pull-sigma, 2), TG_BU_BETA (24), TG_TRACE=1.
+struct DirectionPolicy {
+  int mode = 0;  // 0 auto, 1 top-down only, 2 always bottom-up
+  double alpha = 14.0, bc_alpha = 2.0, beta = 24.0;
+  bool trace = false;  // one stderr line per superstep
+  bool bottom_up(const Engine& eng, uint64_t nf, uint64_t mf, uint64_t mu, bool was_bu,
+                 double a) const {
+    if (eng.P != 1 || !eng.has_in || mode == 1) return false;
+    if (mode == 2) return true;
+    if (was_bu) return (double)nf * beta > (double)eng.V;
+    return (double)mf * a > (double)mu;
+  }
+};
+DirectionPolicy direction_policy(const Engine& eng);
+
+// A CSR with its edge tiles: the out-CSR, or the in-CSR restricted to the
+// local rows [0, Vp).
+struct CsrTiles {
+  const uint64_t* row_off;
+  const uint32_t* vf;
+  const uint32_t* vl;
+  uint64_t ntiles, E;
+};
+inline CsrTiles out_tiles(const Part& p) {
+  return {p.row_off.get(), p.tile_vf.get(), p.tile_vl.get(), p.ntiles, p.Ep};
+}
+inline CsrTiles in_tiles(const Part& p) {
+  return {p.in_off.get(), p.in_tile_vf.get(), p.in_tile_vl.get(), p.in_ntiles, p.in_E_local};
+}
+
+template <class Op>
+void launch_expand_on(Engine& eng, const CsrTiles& c, TileSched& ts, const uint32_t* frontier,
+                      const Op& op, int kid, unsigned long long* edges);
+
 // launch helpers (frontier.cu)
 void launch_compact(Engine& eng, TileSched& ts);
+// degsum (nullable) += out-degree sum of the new frontier; indegsum (nullable)
+// += its in-degree sum (needs the in-CSR)
 void launch_advance(Engine& eng, Part& p, TileSched& ts, uint32_t* next, uint32_t* cur_old,
                     uint32_t* visited, uint32_t* vals, uint32_t level_val,
-                    unsigned long long* count, unsigned long long* degsum = nullptr);
+                    unsigned long long* count, unsigned long long* degsum = nullptr,
+                    unsigned long long* indegsum = nullptr);
+void launch_mark_tiles(Engine& eng, const CsrTiles& c, uint64_t Vp, const uint32_t* bm,
+                       TileSched& ts);
 unsigned expand_grid();
 
 template <class Op>
 void launch_expand(Engine& eng, Part& p, TileSched& ts, const uint32_t* frontier, const Op& op,
                    int kid, unsigned long long* edges) {
-  if (!p.ntiles) return;
-  TileArgs a{p.row_off.get(), p.tile_vf.get(), p.tile_vl.get(), ts.list.get(), ts.count.get(),
-             p.Ep, frontier, edges};
+  launch_expand_on(eng, out_tiles(p), ts, frontier, op, kid, edges);
+}
+
+template <class Op>
+void launch_expand_on(Engine& eng, const CsrTiles& c, TileSched& ts, const uint32_t* frontier,
+                      const Op& op, int kid, unsigned long long* edges) {
+  if (!c.ntiles) return;
+  TileArgs a{c.row_off, c.vf, c.vl, ts.list.get(), ts.count.get(), c.E, frontier, edges};
   // persistent grid = exactly the resident CTAs (static tile striding assumes residency)
   static int per_sm = 0;
   if (!per_sm) {

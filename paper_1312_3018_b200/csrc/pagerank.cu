@@ -1,12 +1,14 @@
 // pagerank.cu -- pull PageRank over BSP rounds (Fig. 14;
-// readings A1-A8 in DESIGN.md).  Iteration t on partition p, in the in-order
-// index space (rows sorted by in-degree, so each degree class is a contiguous
-// row range and gets its own kernel shape):
+// readings A1-A8 in DESIGN.md).  Iteration t on partition p, everything in
+// local-id order (out-degree order: the gathered side of a pull is the source,
+// so the hottest contributions -- the hubs -- are a compact prefix):
 //   pull    : sum_e contrib[in_col[e]] over the row's in-edges from LOCAL
 //             sources, accumulated in fp64 (contrib = rank/outdeg stored fp32,
 //             the paper's 4-byte rank).  Rows [Vp, Vp+S) are outbox
 //             slots: their sums are this partition's source-reduced partial
 //             sums for remote vertices ("the 'rank' sum in PageRank").
+//             Three row classes by in-degree: a CTA per row (>= 2048), a warp
+//             per row (32..2047, from build-time row lists), a thread per row.
 //   P == 1  : fused finalize: rank = (1-d)/V + d*sum, next contrib = rank/outdeg.
 //   P > 1   : outbox partial sums -> owners' inboxes (full buffer),
 //             scatter-add into acc, then finalize.
@@ -48,12 +50,11 @@ struct PullOut {
   bool fused;
   uint64_t Vp;
   double base, d;
-  double* acc;               // !fused: local rows
-  double* obox;              // outbox partial sums (slot-indexed)
-  const uint32_t* in_slot;   // outbox row -> slot
-  float* rank;               // fused
-  float* contrib_next;       // fused
-  const uint32_t* outdeg;    // fused
+  double* acc;             // !fused: local rows
+  double* obox;            // outbox partial sums (row Vp + slot)
+  float* rank;             // fused
+  float* contrib_next;     // fused
+  const uint32_t* outdeg;  // fused
   __device__ __forceinline__ void put(uint64_t r, double sum) const {
     if (r < Vp) {
       if (fused) {
@@ -65,17 +66,18 @@ struct PullOut {
         acc[r] = sum;
       }
     } else {
-      obox[in_slot[r - Vp]] = sum;
+      obox[r - Vp] = sum;
     }
   }
 };
 
-// one CTA per row (in-degree >= kPrCta)
-__global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off, const uint32_t* in_col,
-                                                          const float* contrib, uint64_t r0,
-                                                          PullOut o) {
+// one CTA per listed row (in-degree >= kPrCta)
+__global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off,
+                                                          const uint32_t* in_col,
+                                                          const float* contrib,
+                                                          const uint32_t* rows, PullOut o) {
   __shared__ double s_part[kCtaThreads / 32];
-  const uint64_t r = r0 + blockIdx.x;
+  const uint64_t r = rows[blockIdx.x];
   const uint64_t b = in_off[r], e = in_off[r + 1];
   double sum = gather_sum(in_col, contrib, b + threadIdx.x, e, kCtaThreads);
   sum = warp_sum(sum);
@@ -88,14 +90,14 @@ __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off
   }
 }
 
-// one warp per row (32 <= in-degree < kPrCta)
+// one warp per listed row (32 <= in-degree < kPrCta)
 __global__ void __launch_bounds__(256) k_pull_warp(const uint64_t* in_off, const uint32_t* in_col,
-                                                   const float* contrib, uint64_t r0, uint64_t r1,
-                                                   PullOut o) {
+                                                   const float* contrib, const uint32_t* rows,
+                                                   uint64_t n, PullOut o) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t r = r0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); r < r1;
-       r += nwarps) {
+  for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps) {
+    const uint64_t r = rows[k];
     const uint64_t b = in_off[r], e = in_off[r + 1];
     double sum = gather_sum(in_col, contrib, b + lane, e, 32);
     sum = warp_sum(sum);
@@ -103,13 +105,14 @@ __global__ void __launch_bounds__(256) k_pull_warp(const uint64_t* in_off, const
   }
 }
 
-// one thread per row (in-degree < 32, including 0)
+// one thread per row of [r0, r1) with in-degree < 32 (incl. 0); others skipped
 __global__ void __launch_bounds__(256) k_pull_thread(const uint64_t* in_off, const uint32_t* in_col,
                                                      const float* contrib, uint64_t r0, uint64_t r1,
                                                      PullOut o) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < r1; r += stride) {
     const uint64_t b = in_off[r], e = in_off[r + 1];
+    if (e - b >= 32) continue;
     o.put(r, gather_sum(in_col, contrib, b, e, 1));
   }
 }
@@ -123,10 +126,10 @@ __global__ void k_pr_init(const uint32_t* outdeg, uint64_t Vp, double r0, float*
   }
 }
 
-__global__ void k_pr_scatter(const double* msg, const uint32_t* inpos, uint64_t I, double* acc) {
+__global__ void k_pr_scatter(const double* msg, const uint32_t* lid, uint64_t I, double* acc) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < I; j += stride) {
-    const uint32_t r = inpos[j];
+    const uint32_t r = lid[j];
     if (r != kInf) atomicAdd(&acc[r], msg[j]);
   }
 }
@@ -142,29 +145,28 @@ __global__ void k_pr_finalize(const double* acc, const uint32_t* outdeg, uint64_
   }
 }
 
-__global__ void k_pr_collect(const float* rank, const uint32_t* in_local, const uint32_t* global_of,
-                             uint64_t Vp, float* out) {
+__global__ void k_pr_collect(const float* rank, const uint32_t* global_of, uint64_t Vp, float* out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride)
-    out[global_of[in_local[i]]] = rank[i];
+    out[global_of[i]] = rank[i];
 }
 
-void launch_pull_range(Engine& eng, Part& p, const float* contrib, uint64_t r0, uint64_t cta_end,
-                       uint64_t warp_end, uint64_t r1, const PullOut& o) {
+void launch_pull(Engine& eng, Part& p, const float* contrib, const PullOut& o) {
   cudaStream_t s = eng.stream;
-  if (cta_end > r0) {
-    k_pull_cta<<<(unsigned)(cta_end - r0), kCtaThreads, 0, s>>>(p.in_off.get(), p.in_col.get(),
-                                                                contrib, r0, o);
+  const uint64_t R = p.Vp + p.S;
+  if (p.n_cta) {
+    k_pull_cta<<<(unsigned)p.n_cta, kCtaThreads, 0, s>>>(p.in_off.get(), p.in_col.get(), contrib,
+                                                         p.pr_cta.get(), o);
     eng.launches++;
   }
-  if (warp_end > cta_end) {
-    k_pull_warp<<<grid_for((warp_end - cta_end) * 32, 256, 148u * 16u), 256, 0, s>>>(
-        p.in_off.get(), p.in_col.get(), contrib, cta_end, warp_end, o);
+  if (p.n_warp) {
+    k_pull_warp<<<grid_for(p.n_warp * 32, 256, 148u * 16u), 256, 0, s>>>(
+        p.in_off.get(), p.in_col.get(), contrib, p.pr_warp.get(), p.n_warp, o);
     eng.launches++;
   }
-  if (r1 > warp_end) {
-    k_pull_thread<<<grid_for(r1 - warp_end, 256, 148u * 16u), 256, 0, s>>>(
-        p.in_off.get(), p.in_col.get(), contrib, warp_end, r1, o);
+  if (R) {
+    k_pull_thread<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(p.in_off.get(), p.in_col.get(),
+                                                               contrib, 0, R, o);
     eng.launches++;
   }
   TG_CK(cudaGetLastError());
@@ -202,7 +204,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   for (auto& pp : eng.parts) {
     Part& p = *pp;
     if (!p.Vp) continue;
-    k_pr_init<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.in_outdeg.get(), p.Vp, r0, p.pr.contrib[0].get(),
+    k_pr_init<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.outdeg.get(), p.Vp, r0, p.pr.contrib[0].get(),
                                                   p.pr.rank.get());
     eng.launches++;
   }
@@ -212,38 +214,35 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       PRState& r = p.pr;
-      PullOut o{eng.P == 1, p.Vp, base, d, r.acc.get(), r.obox.get(), p.in_slot.get(), r.rank.get(),
-                r.contrib[cur ^ 1].get(), p.in_outdeg.get()};
-      // hubs are the first in-order positions: keep the hot prefix of the
-      // gathered contribution array resident in L2
-      if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));
-      launch_pull_range(eng, p, r.contrib[cur].get(), 0, p.loc_cta, p.loc_warp, p.Vp, o);
-      if (p.S)
-        launch_pull_range(eng, p, r.contrib[cur].get(), p.Vp, p.Vp + p.box_cta, p.Vp + p.box_warp,
-                          p.Vp + p.S, o);
+      PullOut o{eng.P == 1, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
+                r.contrib[cur ^ 1].get(), p.outdeg.get()};
+      if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
+      launch_pull(eng, p, r.contrib[cur].get(), o);
     }
     eng.prof_end(TG_K_PR_PULL);
     // pull: in_col 4 + contrib gather 4 per edge; in_off 8 + outdeg 4 + rank 4 +
     // next contrib 4 per row
     eng.prof_bytes(TG_K_PR_PULL, 8.0 * eng.E + 20.0 * eng.V);
     if (eng.P > 1) {
+      eng.prof_begin(TG_K_EXCHANGE);
       exchange(eng, send_obox, recv_ibox, 8, false);
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         PRState& r = p.pr;
         if (p.I) {
-          k_pr_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(r.ibox.get(), p.ibox_inpos.get(), p.I,
+          k_pr_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(r.ibox.get(), p.ibox_lid.get(), p.I,
                                                           r.acc.get());
           eng.launches++;
         }
         if (p.Vp) {
-          k_pr_finalize<<<grid_for(p.Vp, 256), 256, 0, s>>>(r.acc.get(), p.in_outdeg.get(), p.Vp,
-                                                            base, d, r.rank.get(),
+          k_pr_finalize<<<grid_for(p.Vp, 256), 256, 0, s>>>(r.acc.get(), p.outdeg.get(), p.Vp, base,
+                                                            d, r.rank.get(),
                                                             r.contrib[cur ^ 1].get());
           eng.launches++;
         }
         TG_CK(cudaGetLastError());
       }
+      eng.prof_end(TG_K_EXCHANGE);
     }
     cur ^= 1;
   }
@@ -269,8 +268,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   for (auto& pp : eng.parts) {
     Part& p = *pp;
     if (!p.Vp) continue;
-    k_pr_collect<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.pr.rank.get(), p.in_local.get(),
-                                                     p.global_of.get(), p.Vp, dout);
+    k_pr_collect<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.pr.rank.get(), p.global_of.get(), p.Vp, dout);
   }
   TG_CK(cudaGetLastError());
   if (mem == TG_MEM_HOST)

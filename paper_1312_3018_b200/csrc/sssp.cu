@@ -81,7 +81,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   if (eng.P == 1) eng.l2_window(eng.parts[0]->fs.vals.get(), eng.parts[0]->Vp * 4);
   time_begin(eng);
-  for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get(), 0, 32, s));
+  for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get(), 0, 64, s));
   for (auto& pp : eng.parts) {
     Part& p = *pp;
     FrontierState& f = p.fs;
@@ -105,7 +105,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
       SsspOp op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
-                f.counters.get() + 2};
+                f.counters.get() + 4};
       launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
     }
     supersteps++;
@@ -140,7 +140,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   }
   const double ms = time_end(eng);
   eng.l2_window(nullptr, 0);
-  TG_REQUIRE(read_counts(eng, 2) == 0, TG_EINTERNAL, "tg_sssp: distance overflows uint32");
+  TG_REQUIRE(read_counts(eng, 4) == 0, TG_EINTERNAL, "tg_sssp: distance overflows uint32");
   if (st) {
     uint64_t nreached = 0;
     st->device_ms = ms;

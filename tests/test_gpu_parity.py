@@ -141,6 +141,28 @@ def test_partition_invariance_rmat12(tg, P):
     check_all(tg, G, eng, bfs_src=srcs, sssp_src=srcs[:3], pr_T=(5,), bc_src=srcs[:4])
 
 
+@pytest.mark.parametrize("mode", ["top", "bottom", "auto"])
+def test_direction_modes_same_result(tg, mode, monkeypatch):
+    """Direction-optimizing BFS / pull-sigma BC: top-down,
+    forced bottom-up and the automatic switch all give the oracle's result."""
+    monkeypatch.setenv("TG_DIRECTION", mode)
+    scale = 13
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    eng = tg.Engine.from_edges(V, src, dst, w)
+    srcs = inputs.list_sources(src, 5)
+    for s in srcs:
+        assert np.array_equal(eng.bfs(int(s))[0], G.bfs(int(s))), (mode, s)
+    assert_bc(eng.bc(srcs[:3])[0], G.bc(srcs[:3]))
+    # a path: every level is tiny, bottom-up must still be exact
+    n = 500
+    p_src = np.arange(n - 1, dtype=np.uint32)
+    Gp, ep = both(tg, n, p_src, p_src + 1)
+    assert np.array_equal(ep.bfs(0)[0], Gp.bfs(0))
+    assert_bc(ep.bc([0, 3])[0], Gp.bc([0, 3]))
+
+
 # ------------------------------------------------------------ adversarial shapes
 @pytest.mark.parametrize("P", [1, 2])
 def test_hub_of_degree_2_20(tg, P):
