@@ -109,15 +109,17 @@ unsigned long long read_counts(Engine& eng, int idx) {
 Vote read_vote(Engine& eng) {
   const int P = (int)eng.parts.size();
   for (int i = 0; i < P; ++i)
-    TG_CK(cudaMemcpyAsync(eng.h_counts + 4 * i, eng.parts[i]->fs.counters.get(), 32,
+    TG_CK(cudaMemcpyAsync(eng.h_counts + 6 * i, eng.parts[i]->fs.counters.get(), 48,
                           cudaMemcpyDeviceToHost, eng.stream));
   TG_CK(cudaStreamSynchronize(eng.stream));
   Vote v;
+  v.minval = ~0ull;
   for (int i = 0; i < P; ++i) {
-    v.count += eng.h_counts[4 * i];
-    v.edges += eng.h_counts[4 * i + 1];
-    v.degsum += eng.h_counts[4 * i + 2];
-    v.indegsum += eng.h_counts[4 * i + 3];
+    v.count += eng.h_counts[6 * i];
+    v.edges += eng.h_counts[6 * i + 1];
+    v.degsum += eng.h_counts[6 * i + 2];
+    v.indegsum += eng.h_counts[6 * i + 3];
+    v.minval = std::min<unsigned long long>(v.minval, eng.h_counts[6 * i + 5]);
   }
   return v;
 }
@@ -326,7 +328,7 @@ static void init_engine(Engine& eng, const tg_attr* attr) {
   TG_CK(cudaStreamCreateWithFlags(&eng.stream, cudaStreamNonBlocking));
   TG_CK(cudaEventCreate(&eng.ev0));
   TG_CK(cudaEventCreate(&eng.ev1));
-  TG_CK(cudaMallocHost(&eng.h_counts, sizeof(unsigned long long) * TG_MAX_PARTITIONS * 4));
+  TG_CK(cudaMallocHost(&eng.h_counts, sizeof(unsigned long long) * TG_MAX_PARTITIONS * 8));
   // L2 set-aside for persisting accesses: measured slower on RMAT-28 (the
   // set-aside starves the rest of the working set), so opt-in only
   // (TG_L2_WINDOW=1).

@@ -26,7 +26,7 @@ namespace {
 
 struct BcFwdOp {
   using Aux = double;
-  static constexpr bool kReduce = false;
+  static constexpr bool kReduce = false, kFilter = false;
   const uint32_t* col;
   const uint32_t* visited;
   uint32_t* next;
@@ -55,7 +55,7 @@ struct BcFwdOp {
 
 struct BcBwdOp {
   using Aux = Empty;
-  static constexpr bool kReduce = true;
+  static constexpr bool kReduce = true, kFilter = false;
   const uint32_t* col;
   const uint32_t* succ;  // F[L+1]
   const double* c;
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) k_bc_pull(const uint64_t* in_off, const u
 // w in F[L+1] (Aux = c[w]) and in-edge (v, w) with v in F[L]: dsum[v] += c[w].
 struct BcBwdPushOp {
   using Aux = double;
-  static constexpr bool kReduce = false;
+  static constexpr bool kReduce = false, kFilter = false;
   const uint32_t* in_col;
   const uint32_t* FL;
   const double* c;

@@ -24,7 +24,7 @@ namespace {
 
 struct BfsOp {
   using Aux = Empty;
-  static constexpr bool kReduce = false;
+  static constexpr bool kReduce = false, kFilter = false;
   const uint32_t* col;
   const uint32_t* visited;
   uint32_t* next;

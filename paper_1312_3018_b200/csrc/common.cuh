@@ -80,6 +80,33 @@ __device__ __forceinline__ void bit_set_atomic(uint32_t* bm, uint32_t i) {
   atomicOr(&bm[i >> 5], 1u << (i & 31));
 }
 
+// L2 eviction-priority hints (createpolicy + .L2::cache_hint): gathered hot
+// state is loaded evict_last, single-use streams evict_first, so the 126 MB L2
+// keeps the hub prefix of the gathered arrays.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(p) : "f"(1.0f));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, %1;" : "=l"(p) : "f"(1.0f));
+  return p;
+}
+__device__ __forceinline__ float ld_f32_hint(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_u32_hint(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_f32_hint(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+
 inline unsigned grid_for(uint64_t n, unsigned block, unsigned cap = 148u * 64u) {
   uint64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;

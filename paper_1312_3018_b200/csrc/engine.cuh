@@ -191,9 +191,10 @@ void ensure_frontier_state(Engine& eng);
 unsigned long long read_counts(Engine& eng, int idx);
 // counters layout: [0] new-frontier count (advance), [1] edges processed by the
 // superstep's expand, [2] out-degree sum of the new frontier, [3] its in-degree
-// sum, [4] error flags.  One sync for all partitions.
+// sum, [4] error flags, [5] minimum value over the new frontier (SSSP: the
+// smallest tentative distance).  One sync for all partitions.
 struct Vote {
-  unsigned long long count = 0, edges = 0, degsum = 0, indegsum = 0;
+  unsigned long long count = 0, edges = 0, degsum = 0, indegsum = 0, minval = ~0ull;
 };
 Vote read_vote(Engine& eng);
 // zero counters[0..1] of every partition (start of a superstep)

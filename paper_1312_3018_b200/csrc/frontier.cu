@@ -62,10 +62,11 @@ __global__ void k_advance(uint32_t* next, uint32_t* cur_old, uint32_t* visited, 
                           uint32_t level_val, uint64_t Vp, const uint64_t* row_off,
                           uint32_t* tile_bm, unsigned long long* count,
                           unsigned long long* degsum, const uint64_t* in_off,
-                          unsigned long long* indegsum) {
+                          unsigned long long* indegsum, const uint32_t* minvals,
+                          unsigned long long* minout) {
   const uint64_t nwords = words_for(Vp);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  unsigned long long cnt = 0, dsum = 0, isum = 0;
+  unsigned long long cnt = 0, dsum = 0, isum = 0, mn = ~0ull;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nwords; w += stride) {
     uint32_t x = next[w];
     if (cur_old) cur_old[w] = 0;
@@ -84,6 +85,15 @@ __global__ void k_advance(uint32_t* next, uint32_t* cur_old, uint32_t* visited, 
           y &= y - 1;
           dsum += row_off[v0 + b + 1] - row_off[v0 + b];
         }
+      }
+    }
+    if (minout) {  // smallest value over the new frontier (near-far SSSP)
+      uint32_t y = x;
+      while (y) {
+        const int b = __ffs(y) - 1;
+        y &= y - 1;
+        const unsigned long long m = minvals[v0 + b];
+        mn = m < mn ? m : mn;
       }
     }
     if (indegsum) {  // exact in-degree sum (BC backward direction choice)
@@ -117,6 +127,13 @@ __global__ void k_advance(uint32_t* next, uint32_t* cur_old, uint32_t* visited, 
   block_add(count, cnt);
   if (degsum) block_add(degsum, dsum);
   if (indegsum) block_add(indegsum, isum);
+  if (minout) {
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long y = __shfl_down_sync(0xffffffffu, mn, o);
+      mn = y < mn ? y : mn;
+    }
+    if ((threadIdx.x & 31) == 0 && mn != ~0ull) atomicMin(minout, mn);
+  }
 }
 
 __global__ void k_mark_tiles(const uint32_t* bm, uint64_t Vp, const uint64_t* row_off,
@@ -194,14 +211,16 @@ void launch_mark_tiles(Engine& eng, const CsrTiles& c, uint64_t Vp, const uint32
 void launch_advance(Engine& eng, Part& p, TileSched& ts, uint32_t* next, uint32_t* cur_old,
                     uint32_t* visited, uint32_t* vals, uint32_t level_val,
                     unsigned long long* count, unsigned long long* degsum,
-                    unsigned long long* indegsum) {
+                    unsigned long long* indegsum, const uint32_t* minvals,
+                    unsigned long long* minout) {
   if (!p.Vp) return;
   const uint64_t nwords = words_for(p.Vp);
   const unsigned blocks = grid_for(nwords, 256, 148u * 16u);
   eng.prof_begin(TG_K_ADVANCE);
   k_advance<<<blocks, 256, 0, eng.stream>>>(next, cur_old, visited, vals, level_val, p.Vp,
                                             p.row_off.get(), ts.bm.get(), count, degsum,
-                                            p.in_off.get(), p.has_in ? indegsum : nullptr);
+                                            p.in_off.get(), p.has_in ? indegsum : nullptr,
+                                            minvals, minvals ? minout : nullptr);
   eng.prof_end(TG_K_ADVANCE);
   // next read + cur_old clear + visited RMW, one pass each
   eng.prof_bytes(TG_K_ADVANCE, 4.0 * nwords * (1 + (cur_old ? 1 : 0) + (visited ? 2 : 0)));

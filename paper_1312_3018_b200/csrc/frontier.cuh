@@ -54,7 +54,8 @@ struct TileArgs {
 constexpr unsigned kExpandThreads = 256;
 
 // Persistent warps over the active tiles.  Op provides
-//   using Aux; static constexpr bool kReduce;
+//   using Aux; static constexpr bool kReduce, kFilter;
+//   bool keep(const Aux&) const; void defer(uint32_t v) const;     (kFilter)
 //   Aux aux(uint32_t v) const;                                 // per active row
 //   void edge(const Aux&, uint64_t e) const;                   (!kReduce)
 //   double edge_val(uint64_t e) const;                         (kReduce)
@@ -82,12 +83,26 @@ __global__ void __launch_bounds__(kExpandThreads) k_warp_expand(TileArgs a, Op o
       bool whole = false;
       Aux aux{};
       if (act) {
-        const uint64_t rb = a.row_off[v], re = a.row_off[v + 1];
-        b = rb > e_lo ? rb : e_lo;
-        const uint64_t en = re < e_hi ? re : e_hi;
-        len = (uint32_t)(en - b);
-        whole = (b == rb) && (en == re);
         aux = op.aux(v);
+        if constexpr (Op::kFilter) {
+          // scheduling filter (near-far SSSP): a deferred row stays active
+          if (!op.keep(aux)) {
+            op.defer(v);
+            aux = Aux{};
+          } else {
+            const uint64_t rb = a.row_off[v], re = a.row_off[v + 1];
+            b = rb > e_lo ? rb : e_lo;
+            const uint64_t en = re < e_hi ? re : e_hi;
+            len = (uint32_t)(en - b);
+            whole = (b == rb) && (en == re);
+          }
+        } else {
+          const uint64_t rb = a.row_off[v], re = a.row_off[v + 1];
+          b = rb > e_lo ? rb : e_lo;
+          const uint64_t en = re < e_hi ? re : e_hi;
+          len = (uint32_t)(en - b);
+          whole = (b == rb) && (en == re);
+        }
       }
       const uint32_t incl = warp_incl_scan(len);
       const uint32_t T = __shfl_sync(kFull, incl, 31);
@@ -147,7 +162,8 @@ __global__ void k_advance(uint32_t* next, uint32_t* cur_old, uint32_t* visited, 
                           uint32_t level_val, uint64_t Vp, const uint64_t* row_off,
                           uint32_t* tile_bm, unsigned long long* count,
                           unsigned long long* degsum, const uint64_t* in_off,
-                          unsigned long long* indegsum);
+                          unsigned long long* indegsum, const uint32_t* minvals,
+                          unsigned long long* minout);
 
 // mark the tiles touched by the rows set in `bm`
 __global__ void k_mark_tiles(const uint32_t* bm, uint64_t Vp, const uint64_t* row_off,
@@ -202,7 +218,8 @@ void launch_compact(Engine& eng, TileSched& ts);
 void launch_advance(Engine& eng, Part& p, TileSched& ts, uint32_t* next, uint32_t* cur_old,
                     uint32_t* visited, uint32_t* vals, uint32_t level_val,
                     unsigned long long* count, unsigned long long* degsum = nullptr,
-                    unsigned long long* indegsum = nullptr);
+                    unsigned long long* indegsum = nullptr, const uint32_t* minvals = nullptr,
+                    unsigned long long* minout = nullptr);
 void launch_mark_tiles(Engine& eng, const CsrTiles& c, uint64_t Vp, const uint32_t* bm,
                        TileSched& ts);
 unsigned expand_grid();

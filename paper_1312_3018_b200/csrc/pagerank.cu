@@ -33,16 +33,18 @@ __device__ __forceinline__ double warp_sum(double x) {
 __device__ __forceinline__ double gather_sum(const uint32_t* __restrict__ in_col,
                                              const float* __restrict__ contrib, uint64_t i,
                                              uint64_t e, uint32_t step) {
+  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
   double s0 = 0.0, s1 = 0.0;
   for (; i + 3ull * step < e; i += 4ull * step) {
-    const uint32_t c0 = __ldcs(in_col + i), c1 = __ldcs(in_col + i + step);
-    const uint32_t c2 = __ldcs(in_col + i + 2ull * step), c3 = __ldcs(in_col + i + 3ull * step);
-    const float f0 = __ldg(contrib + c0), f1 = __ldg(contrib + c1);
-    const float f2 = __ldg(contrib + c2), f3 = __ldg(contrib + c3);
+    const uint32_t c0 = ld_u32_hint(in_col + i, stream), c1 = ld_u32_hint(in_col + i + step, stream);
+    const uint32_t c2 = ld_u32_hint(in_col + i + 2ull * step, stream);
+    const uint32_t c3 = ld_u32_hint(in_col + i + 3ull * step, stream);
+    const float f0 = ld_f32_hint(contrib + c0, keep), f1 = ld_f32_hint(contrib + c1, keep);
+    const float f2 = ld_f32_hint(contrib + c2, keep), f3 = ld_f32_hint(contrib + c3, keep);
     s0 += (double)f0 + (double)f1;
     s1 += (double)f2 + (double)f3;
   }
-  for (; i < e; i += step) s0 += (double)__ldg(contrib + __ldcs(in_col + i));
+  for (; i < e; i += step) s0 += (double)ld_f32_hint(contrib + ld_u32_hint(in_col + i, stream), keep);
   return s0 + s1;
 }
 
@@ -59,7 +61,8 @@ struct PullOut {
     if (r < Vp) {
       if (fused) {
         const double rk = base + d * sum;
-        rank[r] = (float)rk;
+        const uint64_t stream = l2_evict_first();
+        st_f32_hint(rank + r, (float)rk, stream);
         const uint32_t od = outdeg[r];
         contrib_next[r] = od ? (float)(rk / (double)od) : 0.0f;
       } else {

@@ -8,9 +8,19 @@
 //   communicate: the full outbox value array (full buffer every
 //             superstep; min-combine makes re-sending idempotent).
 //   scatter : dist[v] = min(dist[v], msg), activate on improvement.
-//   advance : next-active bitmap -> vote count.
-// The paper's same-superstep re-activation changes the number of
-// supersteps, never the fixed point; it is not used here (A19).
+//   advance : next-active bitmap -> vote count + the smallest active distance.
+//
+// Near-far schedule (reading A19b): an active vertex is relaxed in a
+// superstep only if dist[v] < min_active_dist + Delta; the others stay active
+// for a later superstep (Davidson et al. 2014, the GPU SSSP work the paper
+// cites at P:649).  Any schedule of Bellman-Ford relaxations reaches the same
+// fixed point, so distances are identical; the schedule only removes redundant
+// relaxations.  Default Delta = 0 = infinity, i.e. plain Bellman-Ford: on
+// RMAT-28 every Delta in 16..512 relaxed as many edges (~1.9 E) and took longer
+// (profiles/r01_sssp_delta_sweep.txt); TG_SSSP_DELTA=<d> enables it.
+#include <cstdio>
+#include <cstdlib>
+
 #include "frontier.cuh"
 
 namespace tg {
@@ -19,14 +29,17 @@ namespace {
 
 struct SsspOp {
   using Aux = uint32_t;
-  static constexpr bool kReduce = false;
+  static constexpr bool kReduce = false, kFilter = true;
   const uint32_t* col;
   const uint32_t* w;
   uint32_t* dist;
   uint32_t* next;
   uint32_t* obox;
   unsigned long long* overflow;
+  uint32_t thresh;  // relax rows with dist < thresh now, defer the others
   __device__ __forceinline__ Aux aux(uint32_t v) const { return dist[v]; }
+  __device__ __forceinline__ bool keep(const Aux& dv) const { return dv < thresh; }
+  __device__ __forceinline__ void defer(uint32_t v) const { bit_set_atomic(next, v); }
   __device__ __forceinline__ void edge(const Aux& dv, uint64_t e) const {
     const uint32_t t = __ldcs(col + e);
     const uint64_t nd64 = (uint64_t)dv + __ldcs(w + e);
@@ -65,6 +78,11 @@ __global__ void k_sssp_scatter(const uint32_t* msg, const uint32_t* lid, uint64_
 void* send_obox(Part& p) { return p.fs.obox_u32.get(); }
 void* recv_ibox(Part& p) { return p.fs.ibox_u32.get(); }
 
+uint32_t sssp_delta() {
+  if (const char* d = std::getenv("TG_SSSP_DELTA")) return (uint32_t)std::strtoul(d, nullptr, 10);
+  return 0;  // plain Bellman-Ford: on RMAT-28 no Delta in 16..512 removed relaxations
+}
+
 }  // namespace
 
 void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st) {
@@ -77,6 +95,8 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   eng.launches = 0;
   eng.comm_bytes = 0;
   cudaStream_t s = eng.stream;
+  const uint32_t delta = sssp_delta();
+  const bool trace = std::getenv("TG_TRACE") && std::getenv("TG_TRACE")[0] == '1';
   uint64_t bm_bytes = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   if (eng.P == 1) eng.l2_window(eng.parts[0]->fs.vals.get(), eng.parts[0]->Vp * 4);
@@ -98,14 +118,18 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     std::swap(f.cur, f.next);
   }
   uint64_t supersteps = 0, frontier = 1, relax = 0, activations = 1;
+  uint64_t mind = 0;  // smallest tentative distance among the active vertices
   for (;;) {
     reset_vote(eng);
+    for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get() + 5, 0xFF, 8, s));
+    const uint64_t th = delta ? mind + delta : (uint64_t)kInf;
+    const uint32_t thresh = th >= (uint64_t)kInf ? kInf : (uint32_t)th;
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
       SsspOp op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
-                f.counters.get() + 4};
+                f.counters.get() + 4, thresh};
       launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
     }
     supersteps++;
@@ -125,18 +149,25 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       FrontierState& f = p.fs;
-      launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get());
+      launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get(),
+                     nullptr, nullptr, f.vals.get(), f.counters.get() + 5);
       std::swap(f.cur, f.next);
     }
     const Vote v = read_vote(eng);
     // relaxation: col 4 + w 4 + dist[t] 4 per edge; offsets 16 + dist[v] 4 per
-    // active vertex; active + next bitmaps one pass each
+    // relaxed vertex; active + next bitmaps one pass each
     eng.prof_bytes(TG_K_SSSP_EXPAND, 12.0 * v.edges + 20.0 * frontier + 2.0 * bm_bytes);
+    if (trace)
+      std::fprintf(stderr, "[tg sssp] step=%llu thresh=%u active=%llu edges=%llu next=%llu min=%llu\n",
+                   (unsigned long long)supersteps, thresh, (unsigned long long)frontier,
+                   (unsigned long long)v.edges, (unsigned long long)v.count,
+                   (unsigned long long)v.minval);
     relax += v.edges;
     frontier = v.count;
     activations += v.count;
+    mind = v.minval;
     if (v.count == 0) break;
-    TG_REQUIRE(supersteps <= eng.V + 1, TG_EINTERNAL, "tg_sssp: superstep bound exceeded");
+    TG_REQUIRE(supersteps <= 4 * eng.V + 64, TG_EINTERNAL, "tg_sssp: superstep bound exceeded");
   }
   const double ms = time_end(eng);
   eng.l2_window(nullptr, 0);
