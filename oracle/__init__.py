@@ -36,9 +36,15 @@ def lib():
         L.oracle_beta.argtypes = [u64, u64, p, p, p, i32, p, p, p]
         L.oracle_bfs_certify.argtypes = [u64, p, p, u64, p, p]
         L.oracle_sssp_certify.argtypes = [u64, p, p, p, u64, p, p]
+        L.oracle_outdeg_edges.argtypes = [u64, u64, p, p]
+        L.oracle_bfs_cert_edges.argtypes = [u64, p, u64, p, p, p, p]
+        L.oracle_sssp_cert_edges.argtypes = [u64, p, u64, p, p, p, p, p]
+        L.oracle_cert_finish.argtypes = [u64, u64, p, p, p]
+        L.oracle_pr_sample_edges.argtypes = [u64, u64, p, p, p, p, p, p, p]
         for f in ("oracle_csr", "oracle_bfs", "oracle_sssp", "oracle_pagerank", "oracle_bc",
                   "oracle_partition", "oracle_beta", "oracle_bfs_certify",
-                  "oracle_sssp_certify"):
+                  "oracle_sssp_certify", "oracle_outdeg_edges", "oracle_bfs_cert_edges",
+                  "oracle_sssp_cert_edges", "oracle_cert_finish", "oracle_pr_sample_edges"):
             getattr(L, f).restype = i32
         _LIB = L
     return _LIB
@@ -128,3 +134,44 @@ def beta(V: int, src, dst, part, P: int):
     _check(lib().oracle_beta(V, len(src), _p(src), _p(dst), _p(part), P, _p(br), _p(bd),
                              _p(slots)), "oracle_beta")
     return float(br[0]), float(bd[0]), slots
+
+
+class StreamingCertificate:
+    """BFS / SSSP certificate over an edge stream fed in chunks (oracle.h
+    streaming section): exact for graphs too large for an in-memory CSR."""
+
+    def __init__(self, V: int, source: int, values, weighted: bool):
+        self.V, self.s, self.weighted = int(V), int(source), weighted
+        self.val = np.ascontiguousarray(values, np.uint32)
+        self.tight = np.zeros((self.V + 63) // 64, np.uint64)
+        self.bad = np.zeros(1, np.uint64)
+
+    def feed(self, src, dst, w=None) -> None:
+        src = np.ascontiguousarray(src, np.uint32)
+        dst = np.ascontiguousarray(dst, np.uint32)
+        if self.weighted:
+            w = np.ascontiguousarray(w, np.uint32)
+            rc = lib().oracle_sssp_cert_edges(self.V, _p(self.val), len(src), _p(src), _p(dst),
+                                              _p(w), _p(self.tight), _p(self.bad))
+        else:
+            rc = lib().oracle_bfs_cert_edges(self.V, _p(self.val), len(src), _p(src), _p(dst),
+                                             _p(self.tight), _p(self.bad))
+        _check(rc, "streaming certificate")
+
+    def holds(self) -> bool:
+        if int(self.bad[0]):
+            return False
+        b = np.zeros(1, np.uint64)
+        return lib().oracle_cert_finish(self.V, self.s, _p(self.val), _p(self.tight), _p(b)) == 0
+
+
+def outdeg_edges(V: int, src, outdeg: np.ndarray) -> None:
+    src = np.ascontiguousarray(src, np.uint32)
+    _check(lib().oracle_outdeg_edges(V, len(src), _p(src), _p(outdeg)), "oracle_outdeg_edges")
+
+
+def pr_sample_edges(V: int, src, dst, mask, slot, r_prev, outdeg, acc) -> None:
+    src = np.ascontiguousarray(src, np.uint32)
+    dst = np.ascontiguousarray(dst, np.uint32)
+    _check(lib().oracle_pr_sample_edges(V, len(src), _p(src), _p(dst), _p(mask), _p(slot),
+                                        _p(r_prev), _p(outdeg), _p(acc)), "oracle_pr_sample_edges")

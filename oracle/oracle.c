@@ -298,3 +298,73 @@ int oracle_sssp_certify(uint64_t V, const uint64_t* row_off, const uint32_t* col
   if (bad) *bad = b;
   return rc;
 }
+
+/* ---- streaming certificates (see oracle.h) ---- */
+int oracle_outdeg_edges(uint64_t V, uint64_t n, const uint32_t* src, uint32_t* outdeg) {
+  if (!outdeg || (n && !src)) return EINVAL_;
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < (long long)n; ++i) {
+    if (src[i] < V) __atomic_fetch_add(&outdeg[src[i]], 1u, __ATOMIC_RELAXED);
+  }
+  return OK;
+}
+
+int oracle_bfs_cert_edges(uint64_t V, const uint32_t* level, uint64_t n, const uint32_t* src,
+                          const uint32_t* dst, uint64_t* tight, uint64_t* bad) {
+  if (!level || !tight || !bad || (n && (!src || !dst))) return EINVAL_;
+  unsigned long long nbad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : nbad)
+  for (long long i = 0; i < (long long)n; ++i) {
+    const uint32_t u = src[i], v = dst[i];
+    if (u >= V || v >= V) { nbad++; continue; }
+    if (level[u] == ORACLE_INF32) continue;
+    const uint64_t lu = level[u], lv = level[v];
+    if (level[v] == ORACLE_INF32 || lv > lu + 1) { nbad++; continue; }
+    if (lv == lu + 1) __atomic_fetch_or(&tight[v >> 6], 1ULL << (v & 63), __ATOMIC_RELAXED);
+  }
+  *bad += nbad;
+  return OK;
+}
+
+int oracle_sssp_cert_edges(uint64_t V, const uint32_t* dist, uint64_t n, const uint32_t* src,
+                           const uint32_t* dst, const uint32_t* w, uint64_t* tight, uint64_t* bad) {
+  if (!dist || !tight || !bad || (n && (!src || !dst || !w))) return EINVAL_;
+  unsigned long long nbad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : nbad)
+  for (long long i = 0; i < (long long)n; ++i) {
+    const uint32_t u = src[i], v = dst[i];
+    if (u >= V || v >= V) { nbad++; continue; }
+    if (dist[u] == ORACLE_INF32) continue;
+    const uint64_t nd = (uint64_t)dist[u] + w[i];
+    if (dist[v] == ORACLE_INF32 || nd < (uint64_t)dist[v]) { nbad++; continue; }
+    if (nd == (uint64_t)dist[v]) __atomic_fetch_or(&tight[v >> 6], 1ULL << (v & 63), __ATOMIC_RELAXED);
+  }
+  *bad += nbad;
+  return OK;
+}
+
+int oracle_cert_finish(uint64_t V, uint64_t s, const uint32_t* val, const uint64_t* tight,
+                       uint64_t* bad) {
+  if (s >= V || !val || !tight) return EINVAL_;
+  if (val[s] != 0) { if (bad) *bad = s; return 1; }
+  for (uint64_t v = 0; v < V; ++v) {
+    if (v == s || val[v] == ORACLE_INF32) continue;
+    if (!((tight[v >> 6] >> (v & 63)) & 1ULL)) { if (bad) *bad = v; return 1; }
+  }
+  return OK;
+}
+
+int oracle_pr_sample_edges(uint64_t V, uint64_t n, const uint32_t* src, const uint32_t* dst,
+                           const uint64_t* mask, const uint32_t* slot, const float* r_prev,
+                           const uint32_t* outdeg, double* acc) {
+  if (!mask || !slot || !r_prev || !outdeg || !acc || (n && (!src || !dst))) return EINVAL_;
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < (long long)n; ++i) {
+    const uint32_t u = src[i], v = dst[i];
+    if (u >= V || v >= V || !((mask[v >> 6] >> (v & 63)) & 1ULL)) continue;
+    const double c = (double)r_prev[u] / (double)outdeg[u];   /* outdeg[u] >= 1: u has this edge */
+#pragma omp atomic
+    acc[slot[v]] += c;
+  }
+  return OK;
+}

@@ -85,4 +85,31 @@ int oracle_bfs_certify(uint64_t V, const uint64_t* row_off, const uint32_t* col,
 int oracle_sssp_certify(uint64_t V, const uint64_t* row_off, const uint32_t* col,
                         const uint32_t* w, uint64_t s, const uint32_t* dist, uint64_t* bad);
 
+/* ---- streaming certificates for graphs too large for an in-memory CSR ------
+ * (the full-size RMAT-28 checks in the bench launch configuration).  The edge
+ * stream is regenerated by the caller in chunks (inputs/tg_inputs.h); each
+ * call folds one chunk.  These loops are the definitions above written over an
+ * edge list instead of a CSR; they are OpenMP-parallel over the chunk (the
+ * only parallel code in the oracle) because 2^32 edges must be checked.
+ * tight: caller-zeroed bitmap of V bits (uint64 words).  Returns the number
+ * of violating edges in *bad (added). */
+int oracle_outdeg_edges(uint64_t V, uint64_t n, const uint32_t* src, uint32_t* outdeg);
+/* BFS: for every edge (u,v) with level[u] reached: level[v] <= level[u]+1;
+ * level[v] == level[u]+1 marks v tight. */
+int oracle_bfs_cert_edges(uint64_t V, const uint32_t* level, uint64_t n, const uint32_t* src,
+                          const uint32_t* dst, uint64_t* tight, uint64_t* bad);
+/* SSSP: for every edge (u,v,w) with dist[u] reached: dist[v] <= dist[u]+w;
+ * equality marks v tight. */
+int oracle_sssp_cert_edges(uint64_t V, const uint32_t* dist, uint64_t n, const uint32_t* src,
+                           const uint32_t* dst, const uint32_t* w, uint64_t* tight, uint64_t* bad);
+/* Finish either certificate: val[s] == 0 and every reached v != s is tight.
+ * Returns 0 iff the certificate holds; *bad = first offender. */
+int oracle_cert_finish(uint64_t V, uint64_t s, const uint32_t* val, const uint64_t* tight,
+                       uint64_t* bad);
+/* PageRank one-round recurrence on a vertex sample: for edges (u,v) with v in
+ * the sample (mask bit set), acc[slot[v]] += r_prev[u] / outdeg[u]. */
+int oracle_pr_sample_edges(uint64_t V, uint64_t n, const uint32_t* src, const uint32_t* dst,
+                           const uint64_t* mask, const uint32_t* slot, const float* r_prev,
+                           const uint32_t* outdeg, double* acc);
+
 #endif

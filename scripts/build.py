@@ -45,7 +45,7 @@ def build_inputs(force: bool = False) -> str:
 def build_oracle(force: bool = False) -> str:
     srcs = [os.path.join(ROOT, "oracle", f) for f in ("oracle.c", "oracle.h")]
     if force or _stale(ORACLE_SO, srcs):
-        _run(["gcc", "-O2", "-fPIC", "-shared", "-std=c99", "-o", ORACLE_SO, srcs[0]])
+        _run(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=gnu99", "-o", ORACLE_SO, srcs[0]])
     return ORACLE_SO
 
 

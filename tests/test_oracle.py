@@ -349,3 +349,64 @@ def test_beta_golden_and_invariants():
     cross = part[src] != part[dst]
     pairs = {(int(part[s]), int(d)) for s, d in zip(src[cross], dst[cross])}
     assert np.isclose(bd * len(src), len(pairs))
+
+
+# ----------------------------------------------- streaming (full-size) certificates
+def test_streaming_certificates_match_in_memory_ones():
+    rng = np.random.default_rng(9)
+    n = 3000
+    src, dst = random_multigraph(rng, n, 20000)
+    w = rng.integers(1, 64, len(src)).astype(np.uint32)
+    G = oracle.Graph(n, src, dst, w)
+    for s in (0, 7):
+        for weighted, truth in ((False, G.bfs(s)), (True, G.sssp(s))):
+            cands = [truth]
+            reached = np.where((truth != INF32) & (np.arange(n) != s))[0]
+            for v in reached[:5]:
+                for delta in (-1, 1):
+                    bad = truth.copy(); bad[v] = int(truth[v]) + delta
+                    cands.append(bad)
+                bad = truth.copy(); bad[v] = INF32
+                cands.append(bad)
+            for k, vals in enumerate(cands):
+                cert = oracle.StreamingCertificate(n, s, vals, weighted)
+                for a in range(0, len(src), 4096):            # chunked feed
+                    cert.feed(src[a:a + 4096], dst[a:a + 4096], w[a:a + 4096])
+                assert cert.holds() == (k == 0)
+                assert cert.holds() == (G.sssp_certify(s, vals) if weighted else G.bfs_certify(s, vals))
+
+
+def test_pr_sample_recurrence_matches_oracle():
+    rng = np.random.default_rng(10)
+    n = 2000
+    src, dst = random_multigraph(rng, n, 15000)
+    G = oracle.Graph(n, src, dst)
+    r4, r5 = G.pagerank(4), G.pagerank(5)
+    outdeg = np.zeros(n, np.uint32)
+    oracle.outdeg_edges(n, src, outdeg)
+    assert np.array_equal(outdeg, G.out_degree().astype(np.uint32))
+    sample = rng.choice(n, 300, replace=False)
+    mask = np.zeros((n + 63) // 64, np.uint64)
+    slot = np.zeros(n, np.uint32)
+    for i, v in enumerate(sample):
+        mask[v >> 6] |= np.uint64(1) << np.uint64(v & 63)
+        slot[v] = i
+    acc = np.zeros(len(sample))
+    oracle.pr_sample_edges(n, src, dst, mask, slot, r4.astype(np.float32), outdeg, acc)
+    pred = 0.15 / n + 0.85 * acc
+    assert np.allclose(pred, r5[sample], rtol=1e-6)
+
+
+def test_bc_single_source_dependency_identity():
+    # sum_v delta_s(v) = sum_{t reachable, t != s} (d(s,t) - 1): every shortest
+    # s-t path has d(s,t)-1 interior vertices (used at full size, where Brandes
+    # cannot run on the host)
+    rng = np.random.default_rng(12)
+    for trial in range(20):
+        n = int(rng.integers(2, 400))
+        src, dst = random_multigraph(rng, n, int(rng.integers(1, 6 * n)))
+        G = oracle.Graph(n, src, dst)
+        s = int(rng.integers(0, n))
+        lv = G.bfs(s).astype(np.int64)
+        reached = (lv != INF32) & (np.arange(n) != s)
+        assert np.isclose(G.bc([s]).sum(), (lv[reached] - 1).sum(), rtol=1e-12, atol=1e-9)
