@@ -20,11 +20,11 @@ int tgin_rmat_edges(int scale, int edge_factor, double a, double b, double c, ui
   if (scale < 1 || scale > 32 || edge_factor < 1) return TGIN_EINVAL;
   if (a < 0 || b < 0 || c < 0 || a + b + c > 1.0 + 1e-12) return TGIN_EINVAL;
   if (count && (!src || !dst)) return TGIN_EINVAL;
-  const tgin_thresholds t = tgin_make_thresholds(a, b, c);
+  const tgin_rmat g = tgin_make_rmat(scale, a, b, c, seed, scramble);
 #pragma omp parallel for schedule(static)
   for (long long i = 0; i < (long long)count; ++i) {
     const uint64_t k = first + (uint64_t)i;
-    tgin_rmat_edge(scale, t, seed, scramble, k, &src[i], &dst[i]);
+    tgin_rmat_edge_g(&g, k, &src[i], &dst[i]);
     if (w) w[i] = tgin_weight(wseed, k);
   }
   return TGIN_OK;

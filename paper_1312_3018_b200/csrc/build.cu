@@ -27,12 +27,11 @@ namespace {
 struct EdgeGen {
   const uint32_t *src, *dst, *w;
   bool gen;
-  int scale, scramble;
-  tgin_thresholds t;
-  uint64_t seed, wseed;
+  tgin_rmat r;
+  uint64_t wseed;
   __device__ __forceinline__ void get(uint64_t k, uint32_t& s, uint32_t& d) const {
     if (gen) {
-      tgin_rmat_edge(scale, t, seed, scramble, k, &s, &d);
+      tgin_rmat_edge_g(&r, k, &s, &d);
     } else {
       s = src[k];
       d = dst[k];
@@ -579,10 +578,7 @@ void build_engine(Engine& eng, const EdgeInput& in) {
   g.dst = in.dst;
   g.w = in.w;
   g.gen = in.generated;
-  g.scale = in.scale;
-  g.scramble = in.scramble;
-  g.t = tgin_make_thresholds(in.a, in.b, in.c);
-  g.seed = in.seed;
+  g.r = tgin_make_rmat(in.scale, in.a, in.b, in.c, in.seed, in.scramble);
   g.wseed = in.wseed;
   const uint64_t V = eng.V;
 
