@@ -58,23 +58,44 @@ const char* tg_last_error(void);
 
 typedef struct tg_engine tg_engine;
 
+/* Host-side communicator for multi-process engines (one process per GPU).
+ * The library moves boundary messages itself (CUDA IPC-mapped peer memory:
+ * NVLink/NVSwitch peer copies between GPUs); it only needs these two host
+ * collectives for metadata, the per-superstep vote and barriers.
+ * Both are collective over all `world` processes and must return 0 on success.
+ *   allgather(ctx, send, recv, bytes): recv[r*bytes .. (r+1)*bytes) = rank r's send.
+ *   allreduce_u64(ctx, data, n, op): in place, op 0 = sum, 1 = min. */
+typedef struct {
+  void* ctx;
+  int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes);
+  int (*allreduce_u64)(void* ctx, uint64_t* data, int n, int op);
+} tg_comm;
+
 /* Engine attributes (the paper's totem_attr_t, re-aimed at GPUs).
- *   num_partitions: logical partitions hosted on this process's device, >= 1.
- *       Vertices are dealt to partitions by the degree-aware serpentine rule
- *       (reading A23; §6.2): order by out-degree desc,
- *       id asc; position i -> round r = i/P, j = i%P, partition
- *       (r even ? j : P-1-j), local id r.  P > 1 on one device exercises the
- *       full outbox/inbox machinery with device-to-device exchange.
+ *   num_partitions: logical partitions hosted on this process's device, >= 1
+ *       (world == 1 only).  Vertices are dealt to partitions by the
+ *       degree-aware serpentine rule (reading A23; §6.2):
+ *       order by out-degree desc, id asc; position i -> round r = i/P,
+ *       j = i%P, partition (r even ? j : P-1-j), local id r.  P > 1 on one
+ *       device exercises the full outbox/inbox machinery in one process.
  *   device: CUDA device ordinal.
  *   weighted: 1 to keep per-edge SSSP weights (required by tg_sssp).
  *   build_in_csr: 1 to build the in-edge CSR used by tg_pagerank (pull).
+ *   rank, world: multi-process engine (world > 1): this process hosts
+ *       partition `rank` of `world` (num_partitions must be 1); every process
+ *       makes the same calls in the same order (SPMD), results are written on
+ *       rank 0 only (other ranks may pass NULL outputs).
+ *   comm: required when world > 1 (copied; must outlive the engine).
  *   reserved: must be zero. */
 typedef struct {
   int num_partitions;
   int device;
   int weighted;
   int build_in_csr;
-  int reserved[4];
+  int rank;
+  int world;
+  const tg_comm* comm;
+  int reserved[2];
 } tg_attr;
 
 /* Build an engine from an explicit directed edge list (duplicates and
@@ -92,6 +113,12 @@ int tg_engine_create_rmat(int scale, int edge_factor, double a, double b, double
                           tg_engine** out);
 
 void tg_engine_free(tg_engine* eng);
+
+/* |V_p| of partition p of P under the degree-serpentine deal (host only; no
+ * device needed): rounds r = i / P deal positions j = i % P to partition
+ * (r even ? j : P-1-j).  TG_EINVAL if P < 1, P > TG_MAX_PARTITIONS or p out of
+ * range. */
+int tg_partition_size(uint64_t V, int p, int P, uint64_t* Vp);
 
 typedef struct {
   uint64_t V, E;

@@ -11,6 +11,8 @@ from .tgraph import (  # noqa: F401
     Engine,
     Stats,
     TGraphError,
+    TorchComm,
+    tg_partition_size,
     lib,
     tg_bc,
     tg_bfs,

@@ -12,6 +12,9 @@ static thread_local std::string g_last_error;
 
 Engine::~Engine() {
   if (stream) cudaStreamSynchronize(stream);
+  for (auto& pv : peers)
+    for (void* ptr : pv.opened) cudaIpcCloseMemHandle(ptr);
+  peers.clear();
   parts.clear();
   rank_of.release();
   if (ev0) cudaEventDestroy(ev0);
@@ -37,7 +40,8 @@ uint64_t Engine::device_bytes() const {
     const Part& p = *pp;
     t += b(p.row_off) + b(p.col) + b(p.w) + b(p.global_of) + b(p.tile_vf) + b(p.tile_vl) +
          b(p.obox_rid) + b(p.ibox_lid) + b(p.in_off) + b(p.in_col) + b(p.outdeg) + b(p.pr_cta) +
-         b(p.pr_warp) + b(p.in_tile_vf) + b(p.in_tile_vl);
+         b(p.pr_warp) + b(p.in_tile_vf) + b(p.in_tile_vl) + b(p.arena_fwd) + b(p.arena_rev) +
+         b(p.staging);
   }
   return t;
 }
@@ -63,35 +67,68 @@ void ensure_frontier_state(Engine& eng) {
     f.obox_mark.alloc(sw);
     f.obox_new.alloc(sw);
     f.obox_u32.alloc(std::max<uint64_t>(p.S, 1));
-    f.ibox_bits.alloc(iw);
-    f.ibox_u32.alloc(std::max<uint64_t>(p.I, 1));
+    (void)iw;
     f.counters.alloc(8);
     p.ts.ensure(p.ntiles);
     if (p.in_ntiles) p.ts_in.ensure(p.in_ntiles);
   }
 }
 
+void comm_allreduce(Engine& eng, uint64_t* data, int n, int op) {
+  if (!eng.multi()) return;
+  TG_REQUIRE(eng.comm.allreduce_u64(eng.comm.ctx, data, n, op) == 0, TG_ENCCL,
+             "tg_comm.allreduce_u64 failed");
+}
+
+void comm_barrier(Engine& eng) {
+  if (!eng.multi()) return;
+  uint64_t x = 0;
+  comm_allreduce(eng, &x, 1, 0);
+}
+
 void exchange(Engine& eng, BufOf send, BufOf recv, size_t elem, bool reverse) {
-  // LOCAL transport: every partition lives on this device; the segments are
-  // symmetric by construction, so each (p, q) pair is one D2D copy.
+  // The communication phase.  Segments are symmetric by
+  // construction, so each (p, q) pair is one copy straight into the peer's
+  // receive arena: a device-to-device copy in one process, a peer (NVLink /
+  // NVSwitch) copy into the CUDA-IPC-mapped arena of another process.
+  // push: p's outbox segment for q -> q.arena_fwd at q's inbox offset of p.
+  // pull: p's inbox segment from q (packed owner state) -> q.arena_rev at q's
+  //       outbox offset for p.
+  (void)recv;
+  if (eng.multi()) {  // receivers must be done with the previous messages
+    TG_CK(cudaStreamSynchronize(eng.stream));
+    comm_barrier(eng);
+  }
   for (auto& pp : eng.parts) {
     Part& p = *pp;
-    for (auto& qq : eng.parts) {
-      Part& q = *qq;
-      if (p.id == q.id) continue;
-      const uint64_t o0 = p.obox_off[q.id], n = p.obox_off[q.id + 1] - o0;  // p -> q segment
-      const uint64_t i0 = q.ibox_off[p.id];
+    for (int q = 0; q < eng.P; ++q) {
+      if (q == p.id) continue;
+      const PeerView& peer = eng.peers[q];
+      uint64_t src_off, n, dst_off;
+      uint8_t* dst;
+      if (!reverse) {
+        src_off = p.obox_off[q];
+        n = p.obox_off[q + 1] - src_off;
+        dst_off = peer.ibox_off[p.id];
+        dst = peer.arena_fwd;
+      } else {
+        src_off = p.ibox_off[q];
+        n = p.ibox_off[q + 1] - src_off;
+        dst_off = peer.obox_off[p.id];
+        dst = peer.arena_rev;
+      }
       if (!n) continue;
       const uint64_t bytes = elem ? n * elem : n / 8;
-      const uint64_t so = elem ? o0 * elem : o0 / 8, ro = elem ? i0 * elem : i0 / 8;
-      char* ps = static_cast<char*>(reverse ? send(q) : send(p));
-      char* pr = static_cast<char*>(reverse ? recv(p) : recv(q));
-      if (!reverse)
-        TG_CK(cudaMemcpyAsync(pr + ro, ps + so, bytes, cudaMemcpyDeviceToDevice, eng.stream));
-      else
-        TG_CK(cudaMemcpyAsync(pr + so, ps + ro, bytes, cudaMemcpyDeviceToDevice, eng.stream));
+      const uint64_t so = elem ? src_off * elem : src_off / 8;
+      const uint64_t ro = elem ? dst_off * elem : dst_off / 8;
+      const uint8_t* src = static_cast<const uint8_t*>(send(p));
+      TG_CK(cudaMemcpyAsync(dst + ro, src + so, bytes, cudaMemcpyDefault, eng.stream));
       eng.comm_bytes += bytes;
     }
+  }
+  if (eng.multi()) {  // everyone's messages have landed before anyone scatters
+    TG_CK(cudaStreamSynchronize(eng.stream));
+    comm_barrier(eng);
   }
 }
 
@@ -101,8 +138,9 @@ unsigned long long read_counts(Engine& eng, int idx) {
     TG_CK(cudaMemcpyAsync(eng.h_counts + i, eng.parts[i]->fs.counters.get() + idx, 8,
                           cudaMemcpyDeviceToHost, eng.stream));
   TG_CK(cudaStreamSynchronize(eng.stream));
-  unsigned long long t = 0;
+  uint64_t t = 0;
   for (int i = 0; i < P; ++i) t += eng.h_counts[i];
+  comm_allreduce(eng, &t, 1, 0);
   return t;
 }
 
@@ -120,6 +158,16 @@ Vote read_vote(Engine& eng) {
     v.degsum += eng.h_counts[6 * i + 2];
     v.indegsum += eng.h_counts[6 * i + 3];
     v.minval = std::min<unsigned long long>(v.minval, eng.h_counts[6 * i + 5]);
+  }
+  if (eng.multi()) {  // the global vote: sums + the minimum, over all ranks
+    uint64_t s4[4] = {v.count, v.edges, v.degsum, v.indegsum}, mn = v.minval;
+    comm_allreduce(eng, s4, 4, 0);
+    comm_allreduce(eng, &mn, 1, 1);
+    v.count = s4[0];
+    v.edges = s4[1];
+    v.degsum = s4[2];
+    v.indegsum = s4[3];
+    v.minval = mn;
   }
   return v;
 }
@@ -238,11 +286,23 @@ __global__ void k_reached_bm(const uint32_t* bm, const uint64_t* row_off, uint64
   }
 }
 
-__global__ void k_collect_u32(const uint32_t* vals, const uint32_t* global_of, uint64_t Vp,
-                              uint32_t* out) {
+template <typename T>
+__global__ void k_scatter_global(const T* vals, const uint32_t* global_of, uint64_t Vp, T* out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride)
     out[global_of[i]] = vals[i];
+}
+
+void scatter_global(Engine& eng, const void* vals, const uint32_t* gof, uint64_t n, size_t elem,
+                    void* out) {
+  if (!n) return;
+  if (elem == 4)
+    k_scatter_global<uint32_t><<<grid_for(n, 256), 256, 0, eng.stream>>>(
+        static_cast<const uint32_t*>(vals), gof, n, static_cast<uint32_t*>(out));
+  else
+    k_scatter_global<unsigned long long><<<grid_for(n, 256), 256, 0, eng.stream>>>(
+        static_cast<const unsigned long long*>(vals), gof, n, static_cast<unsigned long long*>(out));
+  TG_CK(cudaGetLastError());
 }
 
 uint64_t reached(Engine& eng, bool bitmap, uint64_t* nreached) {
@@ -259,9 +319,10 @@ uint64_t reached(Engine& eng, bool bitmap, uint64_t* nreached) {
                                                                  p.Vp, acc.get());
   }
   TG_CK(cudaGetLastError());
-  unsigned long long h[2];
+  uint64_t h[2];
   TG_CK(cudaMemcpyAsync(h, acc.get(), 16, cudaMemcpyDeviceToHost, eng.stream));
   TG_CK(cudaStreamSynchronize(eng.stream));
+  comm_allreduce(eng, h, 2, 0);
   if (nreached) *nreached = h[1];
   return h[0];
 }
@@ -271,24 +332,39 @@ uint64_t reached(Engine& eng, bool bitmap, uint64_t* nreached) {
 uint64_t reached_outdeg_u32(Engine& eng, uint64_t* nreached) { return reached(eng, false, nreached); }
 uint64_t reached_outdeg_bitmap(Engine& eng, uint64_t* nreached) { return reached(eng, true, nreached); }
 
-void collect_u32(Engine& eng, uint32_t* out, int mem) {
-  TG_REQUIRE(out != nullptr, TG_EINVAL, "NULL output array");
-  uint32_t* dout = out;
-  DevBuf<uint32_t> tmp;
-  if (mem == TG_MEM_HOST) {
-    tmp.alloc(eng.V);
+void collect(Engine& eng, ValsOf vals, size_t elem, void* out, int mem) {
+  const bool root = !eng.multi() || eng.rank == 0;
+  TG_REQUIRE(out != nullptr || !root, TG_EINVAL, "NULL output array");
+  cudaStream_t s = eng.stream;
+  DevBuf<uint8_t> tmp;
+  void* dout = out;
+  if (root && mem == TG_MEM_HOST) {
+    tmp.alloc(eng.V * elem);
     dout = tmp.get();
   }
-  for (auto& pp : eng.parts) {
-    Part& p = *pp;
-    if (!p.Vp) continue;
-    k_collect_u32<<<grid_for(p.Vp, 256), 256, 0, eng.stream>>>(p.fs.vals.get(), p.global_of.get(),
-                                                               p.Vp, dout);
+  if (!eng.multi()) {
+    for (auto& pp : eng.parts) scatter_global(eng, vals(*pp), pp->global_of.get(), pp->Vp, elem, dout);
+  } else {
+    // stage my values, then rank 0 scatters every rank's staging (IPC-mapped)
+    Part& me = *eng.parts[0];
+    if (me.Vp)
+      TG_CK(cudaMemcpyAsync(me.staging.get(), vals(me), me.Vp * elem, cudaMemcpyDeviceToDevice, s));
+    TG_CK(cudaStreamSynchronize(s));
+    comm_barrier(eng);
+    if (root)
+      for (int q = 0; q < eng.P; ++q)
+        scatter_global(eng, eng.peers[q].staging, eng.peers[q].global_of, eng.peers[q].Vp, elem,
+                       dout);
+    TG_CK(cudaStreamSynchronize(s));
+    comm_barrier(eng);
   }
-  TG_CK(cudaGetLastError());
-  if (mem == TG_MEM_HOST)
-    TG_CK(cudaMemcpyAsync(out, dout, eng.V * 4, cudaMemcpyDeviceToHost, eng.stream));
-  TG_CK(cudaStreamSynchronize(eng.stream));
+  if (root && mem == TG_MEM_HOST)
+    TG_CK(cudaMemcpyAsync(out, dout, eng.V * elem, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+}
+
+void collect_u32(Engine& eng, uint32_t* out, int mem) {
+  collect(eng, [](Part& p) -> const void* { return p.fs.vals.get(); }, 4, out, mem);
 }
 
 static int guard(const std::function<void()>& f) {
@@ -317,12 +393,24 @@ static void init_engine(Engine& eng, const tg_attr* attr) {
   TG_REQUIRE(attr->num_partitions <= TG_MAX_PARTITIONS, TG_ECAPACITY,
              "num_partitions > TG_MAX_PARTITIONS");
   for (int r : attr->reserved) TG_REQUIRE(r == 0, TG_EINVAL, "tg_attr.reserved must be zero");
+  const int world = attr->world < 1 ? 1 : attr->world;
+  TG_REQUIRE(world <= TG_MAX_PARTITIONS, TG_ECAPACITY, "world > TG_MAX_PARTITIONS");
+  if (world > 1) {
+    TG_REQUIRE(attr->num_partitions == 1, TG_EINVAL,
+               "multi-process engines host exactly one partition per process");
+    TG_REQUIRE(attr->rank >= 0 && attr->rank < world, TG_EINVAL, "rank outside [0, world)");
+    TG_REQUIRE(attr->comm && attr->comm->allgather && attr->comm->allreduce_u64, TG_EINVAL,
+               "world > 1 requires tg_attr.comm with allgather and allreduce_u64");
+    eng.comm = *attr->comm;
+  }
+  eng.rank = world > 1 ? attr->rank : 0;
+  eng.world = world;
   int ndev = 0;
   TG_CK(cudaGetDeviceCount(&ndev));
   TG_REQUIRE(attr->device >= 0 && attr->device < ndev, TG_EINVAL, "bad CUDA device ordinal");
   eng.device = attr->device;
   TG_CK(cudaSetDevice(eng.device));
-  eng.P = attr->num_partitions;
+  eng.P = world > 1 ? world : attr->num_partitions;
   eng.weighted = attr->weighted != 0;
   eng.has_in = attr->build_in_csr != 0;
   TG_CK(cudaStreamCreateWithFlags(&eng.stream, cudaStreamNonBlocking));
@@ -422,6 +510,15 @@ int tg_engine_create_rmat(int scale, int edge_factor, double a, double b, double
   });
 }
 
+int tg_partition_size(uint64_t V, int p, int P, uint64_t* Vp) {
+  return guard([&] {
+    TG_REQUIRE(Vp != nullptr, TG_EINVAL, "NULL output");
+    TG_REQUIRE(P >= 1 && P <= TG_MAX_PARTITIONS, TG_EINVAL, "P outside [1, TG_MAX_PARTITIONS]");
+    TG_REQUIRE(p >= 0 && p < P, TG_EINVAL, "p outside [0, P)");
+    *Vp = part_size(V, p, P);
+  });
+}
+
 void tg_engine_free(tg_engine* e) {
   if (!e) return;
   Engine* eng = reinterpret_cast<Engine*>(e);
@@ -448,7 +545,11 @@ int tg_engine_partition_info(const tg_engine* e, int p, tg_part_info* info, uint
     TG_REQUIRE(e && info, TG_EINVAL, "NULL argument");
     const Engine* eng = reinterpret_cast<const Engine*>(e);
     TG_REQUIRE(p >= 0 && p < eng->P, TG_EINVAL, "partition index out of range");
-    const Part& pt = *eng->parts[p];
+    const Part* found = nullptr;
+    for (auto& pp : eng->parts)
+      if (pp->id == p) found = pp.get();
+    TG_REQUIRE(found != nullptr, TG_EINVAL, "partition is hosted by another process");
+    const Part& pt = *found;
     info->Vp = pt.Vp;
     info->Ep = pt.Ep;
     info->Ep_local = pt.Ep_local;

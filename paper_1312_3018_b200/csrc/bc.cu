@@ -179,16 +179,10 @@ __global__ void k_bc_level(const uint32_t* F, uint64_t Vp, uint64_t nz_end, cons
   }
 }
 
-__global__ void k_collect_f64(const double* vals, const uint32_t* global_of, uint64_t Vp, double* out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride)
-    out[global_of[i]] = vals[i];
-}
-
 void* send_osigma(Part& p) { return p.bcs.obox_sigma.get(); }
-void* recv_isigma(Part& p) { return p.bcs.ibox_sigma.get(); }
+void* recv_isigma(Part& p) { return p.arena_fwd.get(); }
 void* send_pack(Part& p) { return p.bcs.ibox_pack.get(); }
-void* recv_ghost(Part& p) { return p.bcs.ghost.get(); }
+void* recv_ghost(Part& p) { return p.arena_rev.get(); }
 
 uint32_t* level_bitmap(Part& p, size_t L) {
   BCState& b = p.bcs;
@@ -201,7 +195,7 @@ uint32_t* level_bitmap(Part& p, size_t L) {
 
 void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, tg_stats* st) {
   TG_REQUIRE(k >= 0 && (k == 0 || sources), TG_EINVAL, "tg_bc: bad source list");
-  TG_REQUIRE(out != nullptr, TG_EINVAL, "tg_bc: NULL output");
+  TG_REQUIRE(out != nullptr || (eng.multi() && eng.rank != 0), TG_EINVAL, "tg_bc: NULL output");
   for (int i = 0; i < k; ++i) TG_REQUIRE(sources[i] < eng.V, TG_EINVAL, "tg_bc: source >= V");
   ensure_frontier_state(eng);
   cudaStream_t s = eng.stream;
@@ -217,8 +211,6 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     }
     if (eng.P > 1 && b.obox_sigma.n < std::max<uint64_t>(p.S, 1)) {
       b.obox_sigma.alloc(std::max<uint64_t>(p.S, 1));
-      b.ghost.alloc(std::max<uint64_t>(p.S, 1));
-      b.ibox_sigma.alloc(std::max<uint64_t>(p.I, 1));
       b.ibox_pack.alloc(std::max<uint64_t>(p.I, 1));
     }
     TG_CK(cudaMemsetAsync(b.bc.get(), 0, Vn * 8, s));
@@ -307,7 +299,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
             eng.launches++;
           }
           if (p.I) {
-            k_bc_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(b.ibox_sigma.get(), p.ibox_lid.get(), p.I,
+            k_bc_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(
+                reinterpret_cast<const double*>(p.arena_fwd.get()), p.ibox_lid.get(), p.I,
                                                             f.visited.get(), b.sigma.get(),
                                                             b.level_bm[L + 1].get());
             eng.launches++;
@@ -383,7 +376,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
             if (!p.ntiles) continue;
             launch_mark_tiles(eng, out_tiles(p), p.Vp, p.bcs.level_bm[L].get(), p.ts);
             launch_compact(eng, p.ts);
-            BcBwdOp op{p.col.get(), p.bcs.level_bm[L + 1].get(), p.bcs.c.get(), p.bcs.ghost.get(),
+            BcBwdOp op{p.col.get(), p.bcs.level_bm[L + 1].get(), p.bcs.c.get(),
+                       reinterpret_cast<const double*>(p.arena_rev.get()),
                        p.bcs.dsum.get()};
             launch_expand(eng, p, p.ts, p.bcs.level_bm[L].get(), op, TG_K_BCB_EXPAND,
                           p.fs.counters.get() + 1);
@@ -428,21 +422,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     st->comm_bytes = eng.comm_bytes;
     st->launches = eng.launches;
   }
-  double* dout = out;
-  DevBuf<double> tmp;
-  if (mem == TG_MEM_HOST) {
-    tmp.alloc(eng.V);
-    dout = tmp.get();
-  }
-  for (auto& pp : eng.parts) {
-    Part& p = *pp;
-    if (!p.Vp) continue;
-    k_collect_f64<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.bcs.bc.get(), p.global_of.get(), p.Vp, dout);
-  }
-  TG_CK(cudaGetLastError());
-  if (mem == TG_MEM_HOST)
-    TG_CK(cudaMemcpyAsync(out, dout, eng.V * sizeof(double), cudaMemcpyDeviceToHost, s));
-  TG_CK(cudaStreamSynchronize(s));
+  collect(eng, [](Part& p) -> const void* { return p.bcs.bc.get(); }, sizeof(double), out, mem);
 }
 
 }  // namespace tg

@@ -93,12 +93,12 @@ __global__ void __launch_bounds__(256) k_bfs_bottom_up(const uint64_t* in_off,
 }
 
 void* send_onew(Part& p) { return p.fs.obox_new.get(); }
-void* recv_ibits(Part& p) { return p.fs.ibox_bits.get(); }
+void* recv_ibits(Part& p) { return p.arena_fwd.get(); }
 
 }  // namespace
 
 void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st) {
-  TG_REQUIRE(out != nullptr, TG_EINVAL, "tg_bfs: NULL levels");
+  TG_REQUIRE(out != nullptr || (eng.multi() && eng.rank != 0), TG_EINVAL, "tg_bfs: NULL levels");
   int ps;
   uint32_t ls;
   eng.locate(source, &ps, &ls);
@@ -168,7 +168,8 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
         Part& p = *pp;
         if (p.S) TG_CK(cudaMemsetAsync(p.fs.obox_new.get(), 0, p.S / 8, s));
         if (p.I) {
-          k_bfs_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(p.fs.ibox_bits.get(), p.ibox_lid.get(),
+          k_bfs_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(
+              reinterpret_cast<const uint32_t*>(p.arena_fwd.get()), p.ibox_lid.get(),
                                                            p.I, p.fs.visited.get(),
                                                            p.fs.next.get());
           TG_CK(cudaGetLastError());

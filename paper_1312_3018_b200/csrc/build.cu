@@ -568,6 +568,167 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
   TG_CK(cudaStreamSynchronize(s));
 }
 
+// boundary in-edges of partition q: key (source partition, local id in q)
+__global__ void k_in_keys(EdgeGen g, uint64_t E, const uint32_t* rank_of, int P, int q,
+                          unsigned long long* keys, unsigned long long* counter) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long cnt = 0;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < E; k += stride) {
+    uint32_t s, d, ls, ld;
+    int ps, pd;
+    g.get(k, s, d);
+    deal(rank_of[d], P, &pd, &ld);
+    if (pd != q) continue;
+    deal(rank_of[s], P, &ps, &ls);
+    if (ps == q) continue;
+    if (keys) keys[atomicAdd(counter, 1ull)] = ((unsigned long long)ps << 32) | ld;
+    else cnt++;
+  }
+  if (!keys) block_add_u64(counter, cnt);
+}
+
+// Inbox of partition q: for every peer p, the distinct local ids of
+// q's vertices that p's edges reach, ascending, padded to 32 -- computed from
+// the edge stream on q's side, so it equals p's outbox segment for q by
+// construction (same set, same order, same padding) without any exchange.
+void build_inbox(Engine& eng, Part& pt, const EdgeGen& g) {
+  cudaStream_t s = eng.stream;
+  const int P = eng.P;
+  pt.ibox_off.assign(P + 1, 0);
+  pt.iseg_real.assign(P, 0);
+  DevBuf<unsigned long long> cnt(1);
+  uint64_t n = 0;
+  if (P > 1) {
+    TG_CK(cudaMemsetAsync(cnt.get(), 0, 8, s));
+    k_in_keys<<<G(eng.E), kB, 0, s>>>(g, eng.E, eng.rank_of.get(), P, pt.id, nullptr, cnt.get());
+    TG_CK(cudaGetLastError());
+    n = d2h(cnt.get(), s);
+  }
+  DevBuf<unsigned long long> ukeys;
+  uint64_t nu = 0;
+  std::vector<uint64_t> ustart(P + 1, 0);
+  if (n) {
+    TG_REQUIRE(n < (1ull << 31), TG_ECAPACITY, "too many boundary in-edges in a partition");
+    DevBuf<unsigned long long> keys(n), keys2(n);
+    TG_CK(cudaMemsetAsync(cnt.get(), 0, 8, s));
+    k_in_keys<<<G(eng.E), kB, 0, s>>>(g, eng.E, eng.rank_of.get(), P, pt.id, keys.get(), cnt.get());
+    TG_CK(cudaGetLastError());
+    size_t tmp = 0;
+    TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.get(), keys2.get(), (int)n, 0, 64, s));
+    {
+      DevBuf<uint8_t> t(tmp ? tmp : 1);
+      TG_CK(cub::DeviceRadixSort::SortKeys(t.get(), tmp, keys.get(), keys2.get(), (int)n, 0, 64, s));
+    }
+    DevBuf<unsigned long long> nsel(1);
+    tmp = 0;
+    TG_CK(cub::DeviceSelect::Unique(nullptr, tmp, keys2.get(), keys.get(), nsel.get(), (int)n, s));
+    {
+      DevBuf<uint8_t> t(tmp ? tmp : 1);
+      TG_CK(cub::DeviceSelect::Unique(t.get(), tmp, keys2.get(), keys.get(), nsel.get(), (int)n, s));
+    }
+    nu = d2h(nsel.get(), s);
+    ukeys.alloc(nu);
+    TG_CK(cudaMemcpyAsync(ukeys.get(), keys.get(), nu * 8, cudaMemcpyDeviceToDevice, s));
+    DevBuf<unsigned long long> seg(P);
+    TG_CK(cudaMemsetAsync(seg.get(), 0, seg.bytes(), s));
+    k_seg_count<<<G(nu), kB, 0, s>>>(ukeys.get(), nu, seg.get());
+    TG_CK(cudaGetLastError());
+    std::vector<unsigned long long> hseg(P);
+    TG_CK(cudaMemcpyAsync(hseg.data(), seg.get(), P * 8, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaStreamSynchronize(s));
+    for (int p = 0; p < P; ++p) {
+      pt.iseg_real[p] = hseg[p];
+      ustart[p + 1] = ustart[p] + hseg[p];
+      pt.ibox_off[p + 1] = pt.ibox_off[p] + ((hseg[p] + 31) / 32) * 32;
+    }
+  }
+  pt.I = pt.ibox_off[P];
+  pt.I_real = nu;
+  pt.ibox_lid.alloc(std::max<uint64_t>(pt.I, 1));
+  TG_CK(cudaMemsetAsync(pt.ibox_lid.get(), 0xFF, pt.ibox_lid.bytes(), s));
+  if (nu) {
+    DevBuf<uint64_t> d_ustart(P + 1), d_poff(P + 1);
+    TG_CK(cudaMemcpyAsync(d_ustart.get(), ustart.data(), (P + 1) * 8, cudaMemcpyHostToDevice, s));
+    TG_CK(cudaMemcpyAsync(d_poff.get(), pt.ibox_off.data(), (P + 1) * 8, cudaMemcpyHostToDevice, s));
+    k_place_slots<<<G(nu), kB, 0, s>>>(ukeys.get(), nu, d_ustart.get(), d_poff.get(),
+                                        pt.ibox_lid.get());
+    TG_CK(cudaGetLastError());
+    TG_CK(cudaStreamSynchronize(s));
+  }
+}
+
+// What every partition needs to know about every other: arena / staging /
+// global_of pointers and the outbox / inbox offset tables.  One process: the
+// local parts.  Several: exchanged with the host allgather, device pointers
+// mapped with CUDA IPC (peer access over NVLink between GPUs).
+struct PeerMeta {
+  cudaIpcMemHandle_t h_fwd, h_rev, h_stage, h_gof;
+  uint64_t Vp;
+  uint64_t obox_off[TG_MAX_PARTITIONS + 1];
+  uint64_t ibox_off[TG_MAX_PARTITIONS + 1];
+};
+
+void map_remote_peers(Engine& eng);
+
+void setup_peers(Engine& eng) {
+  eng.peers.assign(eng.P, PeerView{});
+  auto fill_local = [&](PeerView& v, Part& p) {
+    v.arena_fwd = p.arena_fwd.get();
+    v.arena_rev = p.arena_rev.get();
+    v.staging = p.staging.get();
+    v.global_of = p.global_of.get();
+    v.Vp = p.Vp;
+    v.obox_off = p.obox_off;
+    v.ibox_off = p.ibox_off;
+  };
+  for (auto& pt : eng.parts) fill_local(eng.peers[pt->id], *pt);
+  if (eng.multi()) map_remote_peers(eng);
+  // symmetry: p's outbox segment for q has the size of q's inbox from p
+  for (auto& pt : eng.parts)
+    for (int q = 0; q < eng.P; ++q) {
+      if (q == pt->id) continue;
+      const uint64_t a = pt->obox_off[q + 1] - pt->obox_off[q];
+      const uint64_t b = eng.peers[q].ibox_off[pt->id + 1] - eng.peers[q].ibox_off[pt->id];
+      TG_REQUIRE(a == b, TG_EINTERNAL, "outbox/inbox symmetry violated");
+    }
+}
+
+void map_remote_peers(Engine& eng) {
+  Part& me = *eng.parts[0];
+  PeerMeta mine{};
+  TG_CK(cudaIpcGetMemHandle(&mine.h_fwd, me.arena_fwd.get()));
+  TG_CK(cudaIpcGetMemHandle(&mine.h_rev, me.arena_rev.get()));
+  TG_CK(cudaIpcGetMemHandle(&mine.h_stage, me.staging.get()));
+  TG_CK(cudaIpcGetMemHandle(&mine.h_gof, me.global_of.get()));
+  mine.Vp = me.Vp;
+  for (int q = 0; q <= eng.P; ++q) {
+    mine.obox_off[q] = me.obox_off[q];
+    mine.ibox_off[q] = me.ibox_off[q];
+  }
+  std::vector<PeerMeta> all(eng.world);
+  TG_REQUIRE(eng.comm.allgather(eng.comm.ctx, &mine, all.data(), sizeof(PeerMeta)) == 0, TG_ENCCL,
+             "tg_comm.allgather failed");
+  for (int q = 0; q < eng.world; ++q) {
+    if (q == eng.rank) continue;
+    PeerView& v = eng.peers[q];
+    void* p = nullptr;
+    auto open = [&](const cudaIpcMemHandle_t& h) {
+      void* ptr = nullptr;
+      TG_CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+      v.opened.push_back(ptr);
+      return ptr;
+    };
+    (void)p;
+    v.arena_fwd = static_cast<uint8_t*>(open(all[q].h_fwd));
+    v.arena_rev = static_cast<uint8_t*>(open(all[q].h_rev));
+    v.staging = static_cast<uint8_t*>(open(all[q].h_stage));
+    v.global_of = static_cast<uint32_t*>(open(all[q].h_gof));
+    v.Vp = all[q].Vp;
+    v.obox_off.assign(all[q].obox_off, all[q].obox_off + eng.P + 1);
+    v.ibox_off.assign(all[q].ibox_off, all[q].ibox_off + eng.P + 1);
+  }
+}
+
 }  // namespace
 
 void build_engine(Engine& eng, const EdgeInput& in) {
@@ -603,44 +764,26 @@ void build_engine(Engine& eng, const EdgeInput& in) {
   k_inverse<<<G(V), kB, 0, s>>>(order.get(), V, eng.rank_of.get());
   TG_CK(cudaGetLastError());
 
+  // hosted partitions: all P in one process, or partition `rank` of `world`
   eng.parts.clear();
   for (int p = 0; p < eng.P; ++p) {
+    if (eng.multi() && p != eng.rank) continue;
     auto pt = std::make_unique<Part>();
     pt->id = p;
     pt->Vp = part_size(V, p, eng.P);
     eng.parts.push_back(std::move(pt));
   }
-  for (auto& pt : eng.parts) build_part(eng, *pt, g, order.get(), outdeg.get());
-
-  // inboxes: q's inbox from p mirrors p's outbox segment for q
-  for (auto& qt : eng.parts) {
-    const int q = qt->id;
-    qt->ibox_off.assign(eng.P + 1, 0);
-    for (int p = 0; p < eng.P; ++p) {
-      const Part& pp = *eng.parts[p];
-      qt->ibox_off[p + 1] = qt->ibox_off[p] + (p == q ? 0 : pp.obox_off[q + 1] - pp.obox_off[q]);
-    }
-    qt->I = qt->ibox_off[eng.P];
-    qt->ibox_lid.alloc(std::max<uint64_t>(qt->I, 1));
-    for (int p = 0; p < eng.P; ++p) {
-      if (p == q) continue;
-      const Part& pp = *eng.parts[p];
-      const uint64_t n = pp.obox_off[q + 1] - pp.obox_off[q];
-      if (n)
-        TG_CK(cudaMemcpyAsync(qt->ibox_lid.get() + qt->ibox_off[p], pp.obox_rid.get() + pp.obox_off[q],
-                              n * 4, cudaMemcpyDeviceToDevice, s));
-    }
-  }
   for (auto& pt : eng.parts) {
+    build_part(eng, *pt, g, order.get(), outdeg.get());
     if (pt->seg_real.empty()) pt->seg_real.assign(eng.P, 0);
-  }
-  for (auto& qt : eng.parts) {
-    uint64_t real = 0;
-    for (auto& o : eng.parts)
-      if (o->id != qt->id) real += o->seg_real[qt->id];
-    qt->I_real = real;
+    build_inbox(eng, *pt, g);
+    // receive arenas + collection staging (8 bytes per slot / vertex)
+    pt->arena_fwd.alloc(std::max<uint64_t>(pt->I, 1) * 8);
+    pt->arena_rev.alloc(std::max<uint64_t>(pt->S, 1) * 8);
+    pt->staging.alloc(std::max<uint64_t>(pt->Vp, 1) * 8);
   }
   TG_CK(cudaStreamSynchronize(s));
+  setup_peers(eng);
   eng.build_ms = (uint64_t)std::chrono::duration_cast<std::chrono::milliseconds>(
                      std::chrono::steady_clock::now() - t0)
                      .count();

@@ -58,28 +58,25 @@ struct TileSched {
   void ensure(uint64_t ntiles);
 };
 
-struct PRState {  // PageRank (in-order space)
+struct PRState {  // PageRank (local-id order)
   DevBuf<float> contrib[2];
   DevBuf<float> rank;
   DevBuf<double> acc;
-  DevBuf<double> obox;  // partial sums per outbox slot
-  DevBuf<double> ibox;  // received partial sums
+  DevBuf<double> obox;  // partial sums per outbox slot (send)
 };
 
-struct FrontierState {  // BFS / SSSP / BC-forward
+struct FrontierState {  // BFS / SSSP / BC-forward (messages arrive in Part::arena_fwd)
   DevBuf<uint32_t> cur, next, visited;            // bitmaps over local ids
   DevBuf<uint32_t> vals;                          // BFS level or SSSP dist (u32, Vp)
   DevBuf<uint32_t> obox_mark, obox_new;           // bitmaps over outbox slots
   DevBuf<uint32_t> obox_u32;                      // SSSP min-combined distances
-  DevBuf<uint32_t> ibox_bits;                     // BFS/BC inbox bitmap
-  DevBuf<uint32_t> ibox_u32;                      // SSSP inbox distances
-  DevBuf<unsigned long long> counters;            // [0] frontier count, [1] flags
+  DevBuf<unsigned long long> counters;            // see Vote
 };
 
 struct BCState {
   DevBuf<double> sigma, dsum, c, bc;
-  DevBuf<double> obox_sigma, ibox_sigma;  // forward partial sigma sums
-  DevBuf<double> ibox_pack, ghost;        // backward pull: owner-packed c, sender's ghosts
+  DevBuf<double> obox_sigma;              // forward partial sigma sums (send)
+  DevBuf<double> ibox_pack;               // backward pull: owner-packed c (send)
   std::vector<DevBuf<uint32_t>> level_bm; // frontier bitmap per level
 };
 
@@ -109,6 +106,13 @@ struct Part {
   DevBuf<uint32_t> pr_cta, pr_warp; // in-CSR rows with in-degree >= 2048 / in [32, 2048)
   uint64_t n_cta = 0, n_warp = 0;
   std::vector<uint64_t> seg_real;  // real (unpadded) outbox slots per peer
+  std::vector<uint64_t> iseg_real; // real (unpadded) inbox entries per peer
+  // Receive arenas (cudaMalloc'd, CUDA-IPC exportable): peers copy their
+  // outbox segments into arena_fwd at this partition's inbox offsets (push),
+  // owners copy packed inbox segments into arena_rev at this partition's
+  // outbox offsets (pull).  8 bytes per slot covers every message type.
+  DevBuf<uint8_t> arena_fwd, arena_rev;
+  DevBuf<uint8_t> staging;  // result collection (multi-process): Vp x 8 bytes
   // algorithm state (lazily allocated)
   TileSched ts;     // tiles of the out-CSR
   TileSched ts_in;  // tiles of the in-CSR (BC backward push)
@@ -117,9 +121,25 @@ struct Part {
   BCState bcs;
 };
 
+// What a partition exposes to the others (local pointers in one process,
+// CUDA-IPC-mapped peer pointers across processes).
+struct PeerView {
+  uint8_t* arena_fwd = nullptr;
+  uint8_t* arena_rev = nullptr;
+  uint8_t* staging = nullptr;
+  uint32_t* global_of = nullptr;
+  uint64_t Vp = 0;
+  std::vector<uint64_t> obox_off, ibox_off;  // P+1 each
+  std::vector<void*> opened;                 // IPC mappings to close
+};
+
 struct Engine {
   int device = 0;
-  int P = 1;
+  int P = 1;          // total partitions (world when multi-process)
+  int rank = 0, world = 1;
+  tg_comm comm{};
+  bool multi() const { return world > 1; }
+  std::vector<PeerView> peers;  // indexed by partition id (all P)
   uint64_t V = 0, E = 0;
   bool weighted = false, has_in = false;
   cudaStream_t stream = nullptr;
@@ -186,6 +206,15 @@ void exchange(Engine& eng, BufOf send, BufOf recv, size_t elem, bool reverse);
 uint64_t reached_outdeg_u32(Engine& eng, uint64_t* nreached = nullptr);
 uint64_t reached_outdeg_bitmap(Engine& eng, uint64_t* nreached = nullptr);
 void collect_u32(Engine& eng, uint32_t* out, int mem);  // fs.vals -> out[global]
+// Per-vertex results in global order.  vals(p) = the hosted partition's array
+// (Vp elements of `elem` bytes, local-id order).  Multi-process: gathered on
+// rank 0 through the peers' IPC-mapped staging buffers; other ranks' `out`
+// may be NULL.
+using ValsOf = const void* (*)(Part&);
+void collect(Engine& eng, ValsOf vals, size_t elem, void* out, int mem);
+// host collectives (no-ops when world == 1)
+void comm_allreduce(Engine& eng, uint64_t* data, int n, int op);  // op 0 sum, 1 min
+void comm_barrier(Engine& eng);
 void ensure_frontier_state(Engine& eng);
 // read the per-partition counters[idx] (one sync) and return their sum
 unsigned long long read_counts(Engine& eng, int idx);

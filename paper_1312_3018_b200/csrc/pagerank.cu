@@ -148,12 +148,6 @@ __global__ void k_pr_finalize(const double* acc, const uint32_t* outdeg, uint64_
   }
 }
 
-__global__ void k_pr_collect(const float* rank, const uint32_t* global_of, uint64_t Vp, float* out) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride)
-    out[global_of[i]] = rank[i];
-}
-
 void launch_pull(Engine& eng, Part& p, const float* contrib, const PullOut& o) {
   cudaStream_t s = eng.stream;
   const uint64_t R = p.Vp + p.S;
@@ -176,14 +170,15 @@ void launch_pull(Engine& eng, Part& p, const float* contrib, const PullOut& o) {
 }
 
 void* send_obox(Part& p) { return p.pr.obox.get(); }
-void* recv_ibox(Part& p) { return p.pr.ibox.get(); }
+void* recv_ibox(Part& p) { return p.arena_fwd.get(); }
 
 }  // namespace
 
 void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stats* st) {
   TG_REQUIRE(iters >= 1, TG_EINVAL, "tg_pagerank: iterations must be >= 1");
   TG_REQUIRE(eng.has_in, TG_EINVAL, "tg_pagerank: engine built without the in-CSR");
-  TG_REQUIRE(out != nullptr, TG_EINVAL, "tg_pagerank: NULL output");
+  TG_REQUIRE(out != nullptr || (eng.multi() && eng.rank != 0), TG_EINVAL,
+             "tg_pagerank: NULL output");
   cudaStream_t s = eng.stream;
   for (auto& pp : eng.parts) {
     Part& p = *pp;
@@ -196,7 +191,6 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       if (eng.P > 1) {
         r.acc.alloc(Vn);
         r.obox.alloc(std::max<uint64_t>(p.S, 1));
-        r.ibox.alloc(std::max<uint64_t>(p.I, 1));
       }
     }
   }
@@ -233,8 +227,8 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
         Part& p = *pp;
         PRState& r = p.pr;
         if (p.I) {
-          k_pr_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(r.ibox.get(), p.ibox_lid.get(), p.I,
-                                                          r.acc.get());
+          k_pr_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(
+              reinterpret_cast<const double*>(p.arena_fwd.get()), p.ibox_lid.get(), p.I, r.acc.get());
           eng.launches++;
         }
         if (p.Vp) {
@@ -261,22 +255,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
     st->comm_bytes = eng.comm_bytes;
     st->launches = eng.launches;
   }
-  // collect rank -> out[global]
-  float* dout = out;
-  DevBuf<float> tmp;
-  if (mem == TG_MEM_HOST) {
-    tmp.alloc(eng.V);
-    dout = tmp.get();
-  }
-  for (auto& pp : eng.parts) {
-    Part& p = *pp;
-    if (!p.Vp) continue;
-    k_pr_collect<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.pr.rank.get(), p.global_of.get(), p.Vp, dout);
-  }
-  TG_CK(cudaGetLastError());
-  if (mem == TG_MEM_HOST)
-    TG_CK(cudaMemcpyAsync(out, dout, eng.V * sizeof(float), cudaMemcpyDeviceToHost, s));
-  TG_CK(cudaStreamSynchronize(s));
+  collect(eng, [](Part& p) -> const void* { return p.pr.rank.get(); }, sizeof(float), out, mem);
 }
 
 }  // namespace tg

@@ -76,7 +76,7 @@ __global__ void k_sssp_scatter(const uint32_t* msg, const uint32_t* lid, uint64_
 }
 
 void* send_obox(Part& p) { return p.fs.obox_u32.get(); }
-void* recv_ibox(Part& p) { return p.fs.ibox_u32.get(); }
+void* recv_ibox(Part& p) { return p.arena_fwd.get(); }
 
 uint32_t sssp_delta() {
   if (const char* d = std::getenv("TG_SSSP_DELTA")) return (uint32_t)std::strtoul(d, nullptr, 10);
@@ -86,7 +86,7 @@ uint32_t sssp_delta() {
 }  // namespace
 
 void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st) {
-  TG_REQUIRE(out != nullptr, TG_EINVAL, "tg_sssp: NULL dist");
+  TG_REQUIRE(out != nullptr || (eng.multi() && eng.rank != 0), TG_EINVAL, "tg_sssp: NULL dist");
   TG_REQUIRE(eng.weighted, TG_EINVAL, "tg_sssp: engine was built without edge weights");
   int ps;
   uint32_t ls;
@@ -139,7 +139,8 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         if (!p.I) continue;
-        k_sssp_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(p.fs.ibox_u32.get(), p.ibox_lid.get(), p.I,
+        k_sssp_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(
+            reinterpret_cast<const uint32_t*>(p.arena_fwd.get()), p.ibox_lid.get(), p.I,
                                                           p.fs.vals.get(), p.fs.next.get());
         TG_CK(cudaGetLastError());
         eng.launches++;

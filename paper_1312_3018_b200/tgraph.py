@@ -27,9 +27,68 @@ class TGraphError(RuntimeError):
         self.code = code
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_int, C.c_int)
+
+
+class tg_comm(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("allgather", ALLGATHER_FN), ("allreduce_u64", ALLREDUCE_FN)]
+
+
 class tg_attr(C.Structure):
     _fields_ = [("num_partitions", C.c_int), ("device", C.c_int), ("weighted", C.c_int),
-                ("build_in_csr", C.c_int), ("reserved", C.c_int * 4)]
+                ("build_in_csr", C.c_int), ("rank", C.c_int), ("world", C.c_int),
+                ("comm", C.POINTER(tg_comm)), ("reserved", C.c_int * 2)]
+
+
+_U64_MAX = (1 << 64) - 1
+_I64_MAX = (1 << 63) - 1
+
+
+class TorchComm:
+    """tg_comm backed by torch.distributed (gloo or nccl): the library's host
+    collectives for metadata, the per-superstep vote and barriers.  Boundary
+    messages never go through here (they are peer-memory copies)."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.device = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+
+        def allgather(ctx, send, recv, nbytes):
+            try:
+                src = np.frombuffer((C.c_ubyte * nbytes).from_address(send), np.uint8).copy()
+                t = torch.from_numpy(src).to(self.device)
+                outs = [torch.empty_like(t) for _ in range(self.world)]
+                dist.all_gather(outs, t, group=group)
+                res = torch.cat(outs).cpu().numpy()
+                C.memmove(recv, res.ctypes.data, self.world * nbytes)
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to C as a status
+                return 1
+
+        def allreduce(ctx, data, n, op):
+            try:
+                vals = [int(data[i]) for i in range(n)]
+                if op == 1:  # min: keep the all-ones sentinel representable in int64
+                    vals = [_I64_MAX if v == _U64_MAX else v for v in vals]
+                else:        # sum modulo 2^64 via two's complement int64
+                    vals = [v - (1 << 64) if v > _I64_MAX else v for v in vals]
+                t = torch.tensor(vals, dtype=torch.int64, device=self.device)
+                dist.all_reduce(t, op=dist.ReduceOp.MIN if op == 1 else dist.ReduceOp.SUM,
+                                group=group)
+                for i, v in enumerate(t.cpu().tolist()):
+                    data[i] = _U64_MAX if (op == 1 and v == _I64_MAX) else v % (1 << 64)
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        self._ag = ALLGATHER_FN(allgather)
+        self._ar = ALLREDUCE_FN(allreduce)
+        self.struct = tg_comm(None, self._ag, self._ar)
 
 
 class tg_info(C.Structure):
@@ -96,6 +155,8 @@ def lib():
         L.tg_sssp.argtypes = [p, u64, p, i32, C.POINTER(tg_stats)]
         L.tg_pagerank.argtypes = [p, i32, dbl, p, i32, C.POINTER(tg_stats)]
         L.tg_bc.argtypes = [p, p, i32, p, i32, C.POINTER(tg_stats)]
+        L.tg_partition_size.argtypes = [u64, i32, i32, C.POINTER(C.c_uint64)]
+        L.tg_partition_size.restype = i32
         L.tg_engine_set_profiling.argtypes = [p, i32]
         L.tg_engine_kernel_stat.argtypes = [p, i32, C.POINTER(tg_kernel_stat)]
         L.tg_kernel_name.argtypes = [i32]
@@ -123,13 +184,17 @@ def _arr(a, dtype):
     return arr.ctypes.data_as(C.c_void_p), TG_MEM_HOST, arr
 
 
-def _attr(partitions, device, weighted, in_csr) -> tg_attr:
+def _attr(partitions, device, weighted, in_csr, rank=0, world=1, comm=None) -> tg_attr:
     at = tg_attr()
     at.num_partitions, at.device, at.weighted, at.build_in_csr = partitions, device, int(weighted), int(in_csr)
+    at.rank, at.world = rank, world
+    if comm is not None:
+        at.comm = C.pointer(comm.struct)
     return at
 
 
-def tg_engine_create_edges(V, src, dst, w=None, partitions=1, device=0, weighted=None, in_csr=True):
+def tg_engine_create_edges(V, src, dst, w=None, partitions=1, device=0, weighted=None, in_csr=True,
+                           rank=0, world=1, comm=None):
     ps, ms, k1 = _arr(src, np.uint32)
     pd, md, k2 = _arr(dst, np.uint32)
     pw, mw, k3 = _arr(w, np.uint32)
@@ -138,19 +203,27 @@ def tg_engine_create_edges(V, src, dst, w=None, partitions=1, device=0, weighted
         raise ValueError("src and dst must live in the same memory")
     if weighted is None:
         weighted = w is not None
-    at = _attr(partitions, device, weighted, in_csr)
+    at = _attr(partitions, device, weighted, in_csr, rank, world, comm)
     h = C.c_void_p()
     _check(lib().tg_engine_create_edges(V, E, ps, pd, pw, ms, C.byref(at), C.byref(h)))
     return h
 
 
 def tg_engine_create_rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, scramble=True,
-                          wseed=2, partitions=1, device=0, weighted=True, in_csr=True):
-    at = _attr(partitions, device, weighted, in_csr)
+                          wseed=2, partitions=1, device=0, weighted=True, in_csr=True, rank=0,
+                          world=1, comm=None):
+    at = _attr(partitions, device, weighted, in_csr, rank, world, comm)
     h = C.c_void_p()
     _check(lib().tg_engine_create_rmat(scale, edge_factor, a, b, c, seed, int(scramble), wseed,
                                        C.byref(at), C.byref(h)))
     return h
+
+
+def tg_partition_size(V: int, p: int, P: int) -> int:
+    """|V_p| under the degree-serpentine deal (host only, no GPU needed)."""
+    out = C.c_uint64()
+    _check(lib().tg_partition_size(V, p, P, C.byref(out)))
+    return out.value
 
 
 def tg_engine_free(h) -> None:
@@ -229,19 +302,21 @@ def tg_engine_kernel_stats(h) -> dict:
 class Engine:
     """Owning handle: a partitioned, device-resident graph."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, comm=None, rank=0):
         self.h = handle
+        self.comm = comm  # keeps the host-collective callbacks alive
+        self.rank = rank
         inf = tg_engine_info(handle)
         self.V, self.E, self.P = inf["V"], inf["E"], inf["num_partitions"]
         self.info = inf
 
     @classmethod
     def from_edges(cls, V, src, dst, w=None, **kw) -> "Engine":
-        return cls(tg_engine_create_edges(V, src, dst, w, **kw))
+        return cls(tg_engine_create_edges(V, src, dst, w, **kw), kw.get("comm"), kw.get("rank", 0))
 
     @classmethod
     def rmat(cls, scale, **kw) -> "Engine":
-        return cls(tg_engine_create_rmat(scale, **kw))
+        return cls(tg_engine_create_rmat(scale, **kw), kw.get("comm"), kw.get("rank", 0))
 
     def close(self):
         if self.h:

@@ -1,0 +1,33 @@
+"""Multi-process (one partition per process) paths.
+
+CPU (gloo, world 2 and 3): the host collectives the library calls through
+tg_comm (allgather of metadata, vote sums / minima, the all-ones sentinel) and
+the per-rank partition plan against the oracle.
+GPU: 2 and 3 processes on one B200 (cuda:0), one partition each, boundary
+messages copied into CUDA-IPC-mapped peer arenas -- the same code path that
+crosses NVLink between GPUs -- checked against the oracle on rank 0."""
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+import mp_workers
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_collectives_and_plan_gloo(world):
+    mp.spawn(mp_workers.comm_worker, args=(world, _port()), nprocs=world, join=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_partitions_on_one_gpu(world):
+    mp.spawn(mp_workers.engine_worker, args=(world, _port(), 12, 0), nprocs=world, join=True)
