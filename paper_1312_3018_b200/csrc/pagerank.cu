@@ -13,6 +13,8 @@
 //   P > 1   : outbox partial sums -> owners' inboxes (full buffer),
 //             scatter-add into acc, then finalize.
 // No vote: a fixed number of rounds.
+#include <cstdlib>
+
 #include "frontier.cuh"
 
 namespace tg {
@@ -30,21 +32,32 @@ __device__ __forceinline__ double warp_sum(double x) {
 // sum of contrib[in_col[i]] for i = i0, i0+step, ... < e; four independent
 // column loads then four independent gathers per iteration (memory-level
 // parallelism for the dependent load chain), fp64 accumulation.
+// Sources are in out-degree order, so ids below `hot` are the hubs that most
+// in-edges gather from: they are loaded evict_last; the cold tail and the
+// streamed in_col are evict_first, so they do not push the hub lines out of L2.
+__device__ __forceinline__ float gather_one(const float* __restrict__ contrib, uint32_t c,
+                                            uint32_t hot, uint64_t keep, uint64_t stream) {
+  return ld_f32_hint(contrib + c, c < hot ? keep : stream);
+}
+
 __device__ __forceinline__ double gather_sum(const uint32_t* __restrict__ in_col,
                                              const float* __restrict__ contrib, uint64_t i,
-                                             uint64_t e, uint32_t step) {
+                                             uint64_t e, uint32_t step, uint32_t hot) {
   const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
   double s0 = 0.0, s1 = 0.0;
   for (; i + 3ull * step < e; i += 4ull * step) {
     const uint32_t c0 = ld_u32_hint(in_col + i, stream), c1 = ld_u32_hint(in_col + i + step, stream);
     const uint32_t c2 = ld_u32_hint(in_col + i + 2ull * step, stream);
     const uint32_t c3 = ld_u32_hint(in_col + i + 3ull * step, stream);
-    const float f0 = ld_f32_hint(contrib + c0, keep), f1 = ld_f32_hint(contrib + c1, keep);
-    const float f2 = ld_f32_hint(contrib + c2, keep), f3 = ld_f32_hint(contrib + c3, keep);
+    const float f0 = gather_one(contrib, c0, hot, keep, stream);
+    const float f1 = gather_one(contrib, c1, hot, keep, stream);
+    const float f2 = gather_one(contrib, c2, hot, keep, stream);
+    const float f3 = gather_one(contrib, c3, hot, keep, stream);
     s0 += (double)f0 + (double)f1;
     s1 += (double)f2 + (double)f3;
   }
-  for (; i < e; i += step) s0 += (double)ld_f32_hint(contrib + ld_u32_hint(in_col + i, stream), keep);
+  for (; i < e; i += step)
+    s0 += (double)gather_one(contrib, ld_u32_hint(in_col + i, stream), hot, keep, stream);
   return s0 + s1;
 }
 
@@ -57,6 +70,7 @@ struct PullOut {
   float* rank;             // fused
   float* contrib_next;     // fused
   const uint32_t* outdeg;  // fused
+  uint32_t hot;            // sources [0, hot) are gathered evict_last
   __device__ __forceinline__ void put(uint64_t r, double sum) const {
     if (r < Vp) {
       if (fused) {
@@ -64,7 +78,9 @@ struct PullOut {
         const uint64_t stream = l2_evict_first();
         st_f32_hint(rank + r, (float)rk, stream);
         const uint32_t od = outdeg[r];
-        contrib_next[r] = od ? (float)(rk / (double)od) : 0.0f;
+        // next round's contributions: hubs stay evict_last like their gathers
+        st_f32_hint(contrib_next + r, od ? (float)(rk / (double)od) : 0.0f,
+                    r < hot ? l2_evict_last() : stream);
       } else {
         acc[r] = sum;
       }
@@ -82,7 +98,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off
   __shared__ double s_part[kCtaThreads / 32];
   const uint64_t r = rows[blockIdx.x];
   const uint64_t b = in_off[r], e = in_off[r + 1];
-  double sum = gather_sum(in_col, contrib, b + threadIdx.x, e, kCtaThreads);
+  double sum = gather_sum(in_col, contrib, b + threadIdx.x, e, kCtaThreads, o.hot);
   sum = warp_sum(sum);
   if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = sum;
   __syncthreads();
@@ -102,7 +118,7 @@ __global__ void __launch_bounds__(256) k_pull_warp(const uint64_t* in_off, const
   for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps) {
     const uint64_t r = rows[k];
     const uint64_t b = in_off[r], e = in_off[r + 1];
-    double sum = gather_sum(in_col, contrib, b + lane, e, 32);
+    double sum = gather_sum(in_col, contrib, b + lane, e, 32, o.hot);
     sum = warp_sum(sum);
     if (lane == 0) o.put(r, sum);
   }
@@ -116,7 +132,7 @@ __global__ void __launch_bounds__(256) k_pull_thread(const uint64_t* in_off, con
   for (uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < r1; r += stride) {
     const uint64_t b = in_off[r], e = in_off[r + 1];
     if (e - b >= 32) continue;
-    o.put(r, gather_sum(in_col, contrib, b, e, 1));
+    o.put(r, gather_sum(in_col, contrib, b, e, 1, o.hot));
   }
 }
 
@@ -197,6 +213,11 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   eng.launches = 0;
   eng.comm_bytes = 0;
   const double base = (1.0 - d) / (double)eng.V, r0 = 1.0 / (double)eng.V;
+  // hub prefix kept in L2 (evict_last): default 16M sources = 64 MB of fp32
+  // contributions, half of the 126 MB L2 (TG_PR_HOT overrides; RMAT-28 sweep
+  // in profiles/r01_pr_hot_sweep.txt: 0 -> 28.2, 16M -> 20.35, all -> 21.0 ms)
+  uint32_t hot = 16u << 20;
+  if (const char* h = std::getenv("TG_PR_HOT")) hot = (uint32_t)std::strtoul(h, nullptr, 10);
   time_begin(eng);
   for (auto& pp : eng.parts) {
     Part& p = *pp;
@@ -212,7 +233,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       Part& p = *pp;
       PRState& r = p.pr;
       PullOut o{eng.P == 1, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
-                r.contrib[cur ^ 1].get(), p.outdeg.get()};
+                r.contrib[cur ^ 1].get(), p.outdeg.get(), hot};
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
       launch_pull(eng, p, r.contrib[cur].get(), o);
     }
