@@ -37,6 +37,7 @@ __device__ __forceinline__ double warp_sum(double x) {
 // streamed in_col are evict_first, so they do not push the hub lines out of L2.
 __device__ __forceinline__ float gather_one(const float* __restrict__ contrib, uint32_t c,
                                             uint32_t hot, uint64_t keep, uint64_t stream) {
+  // (L1::evict_last / L1::no_allocate variants measured slower: 20.8 vs 20.35 ms)
   return ld_f32_hint(contrib + c, c < hot ? keep : stream);
 }
 
@@ -44,11 +45,12 @@ __device__ __forceinline__ double gather_sum(const uint32_t* __restrict__ in_col
                                              const float* __restrict__ contrib, uint64_t i,
                                              uint64_t e, uint32_t step, uint32_t hot) {
   const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
+  auto col = [&](uint64_t j) { return ld_u32_hint(in_col + j, stream); };
   double s0 = 0.0, s1 = 0.0;
   for (; i + 3ull * step < e; i += 4ull * step) {
-    const uint32_t c0 = ld_u32_hint(in_col + i, stream), c1 = ld_u32_hint(in_col + i + step, stream);
-    const uint32_t c2 = ld_u32_hint(in_col + i + 2ull * step, stream);
-    const uint32_t c3 = ld_u32_hint(in_col + i + 3ull * step, stream);
+    const uint32_t c0 = col(i), c1 = col(i + step);
+    const uint32_t c2 = col(i + 2ull * step);
+    const uint32_t c3 = col(i + 3ull * step);
     const float f0 = gather_one(contrib, c0, hot, keep, stream);
     const float f1 = gather_one(contrib, c1, hot, keep, stream);
     const float f2 = gather_one(contrib, c2, hot, keep, stream);
@@ -57,7 +59,7 @@ __device__ __forceinline__ double gather_sum(const uint32_t* __restrict__ in_col
     s1 += (double)f2 + (double)f3;
   }
   for (; i < e; i += step)
-    s0 += (double)gather_one(contrib, ld_u32_hint(in_col + i, stream), hot, keep, stream);
+    s0 += (double)gather_one(contrib, col(i), hot, keep, stream);
   return s0 + s1;
 }
 

@@ -52,11 +52,12 @@ struct SsspOp {
       const uint32_t s = t & ~kRemote;
       if (nd < obox[s]) atomicMin(&obox[s], nd);
     } else if (nd < dist[t]) {
-      const uint32_t old = atomicMin(&dist[t], nd);
-      if (nd < old) {
-        const uint32_t m = 1u << (t & 31);
-        if (!(next[t >> 5] & m)) atomicOr(&next[t >> 5], m);
-      }
+      // nd < dist[t] as read means t's distance drops in this superstep (to nd
+      // or below: values only decrease and stale reads are only ever higher),
+      // so t is active next superstep.  Both updates are fire-and-forget
+      // reductions (RED.MIN / RED.OR): no round trip on the critical path.
+      atomicMin(&dist[t], nd);
+      atomicOr(&next[t >> 5], 1u << (t & 31));
     }
   }
 };
