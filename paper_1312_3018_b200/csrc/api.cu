@@ -336,11 +336,10 @@ void collect(Engine& eng, ValsOf vals, size_t elem, void* out, int mem) {
   const bool root = !eng.multi() || eng.rank == 0;
   TG_REQUIRE(out != nullptr || !root, TG_EINVAL, "NULL output array");
   cudaStream_t s = eng.stream;
-  DevBuf<uint8_t> tmp;
   void* dout = out;
-  if (root && mem == TG_MEM_HOST) {
-    tmp.alloc(eng.V * elem);
-    dout = tmp.get();
+  if (root && mem == TG_MEM_HOST) {  // device staging for the host copy, kept across calls
+    if (eng.scratch.bytes() < eng.V * elem) eng.scratch.alloc(eng.V * elem);
+    dout = eng.scratch.get();
   }
   if (!eng.multi()) {
     for (auto& pp : eng.parts) scatter_global(eng, vals(*pp), pp->global_of.get(), pp->Vp, elem, dout);

@@ -145,6 +145,7 @@ struct Engine {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf<uint32_t> rank_of;  // global id -> degree-order position
+  DevBuf<uint8_t> scratch;   // device staging of host-bound results (V x 8 max)
   std::vector<std::unique_ptr<Part>> parts;
   uint64_t build_ms = 0;
   uint64_t launches = 0;     // kernels launched by the current run
