@@ -84,6 +84,7 @@ struct Part {
   int id = 0;
   uint64_t Vp = 0, Ep = 0, Ep_local = 0;
   uint64_t nz_end = 0;  // local ids >= nz_end have out-degree 0
+  uint32_t hub_deg = 0, hub_end = 0;  // cached: first local id with out-degree < hub_deg
   DevBuf<uint64_t> row_off;
   DevBuf<uint32_t> col, w, global_of;
   // tiles

@@ -55,7 +55,7 @@ constexpr unsigned kExpandThreads = 256;
 
 // Persistent warps over the active tiles.  Op provides
 //   using Aux; static constexpr bool kReduce, kFilter;
-//   bool keep(const Aux&) const; void defer(uint32_t v) const;     (kFilter)
+//   bool keep(uint32_t v, const Aux&) const; void defer(uint32_t v) const;  (kFilter)
 //   Aux aux(uint32_t v) const;                                 // per active row
 //   void edge(const Aux&, uint64_t e) const;                   (!kReduce)
 //   double edge_val(uint64_t e) const;                         (kReduce)
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_warp_expand(TileArgs a, Op o
         aux = op.aux(v);
         if constexpr (Op::kFilter) {
           // scheduling filter (near-far SSSP): a deferred row stays active
-          if (!op.keep(aux)) {
+          if (!op.keep(v, aux)) {
             op.defer(v);
             aux = Aux{};
           } else {

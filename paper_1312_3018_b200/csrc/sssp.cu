@@ -36,9 +36,12 @@ struct SsspOp {
   uint32_t* next;
   uint32_t* obox;
   unsigned long long* overflow;
-  uint32_t thresh;  // relax rows with dist < thresh now, defer the others
+  uint32_t thresh;   // relax rows with dist < thresh now, defer the others ...
+  uint32_t hub_end;  // ... but only rows v < hub_end (the high-degree prefix)
   __device__ __forceinline__ Aux aux(uint32_t v) const { return dist[v]; }
-  __device__ __forceinline__ bool keep(const Aux& dv) const { return dv < thresh; }
+  __device__ __forceinline__ bool keep(uint32_t v, const Aux& dv) const {
+    return v >= hub_end || dv < thresh;
+  }
   __device__ __forceinline__ void defer(uint32_t v) const { bit_set_atomic(next, v); }
   __device__ __forceinline__ void edge(const Aux& dv, uint64_t e) const {
     const uint32_t t = __ldcs(col + e);
@@ -79,9 +82,35 @@ __global__ void k_sssp_scatter(const uint32_t* msg, const uint32_t* lid, uint64_
 void* send_obox(Part& p) { return p.fs.obox_u32.get(); }
 void* recv_ibox(Part& p) { return p.arena_fwd.get(); }
 
-uint32_t sssp_delta() {
-  if (const char* d = std::getenv("TG_SSSP_DELTA")) return (uint32_t)std::strtoul(d, nullptr, 10);
-  return 0;  // plain Bellman-Ford: on RMAT-28 no Delta in 16..512 removed relaxations
+uint32_t env_u32(const char* name, uint32_t dflt) {
+  if (const char* d = std::getenv(name)) return (uint32_t)std::strtoul(d, nullptr, 10);
+  return dflt;
+}
+
+// Binary search over the degree-sorted rows: first local id whose out-degree
+// is below `deg` (ids are sorted by out-degree descending, build.cu).
+__global__ void k_hub_end(const uint64_t* __restrict__ row_off, uint64_t n, uint32_t deg,
+                          uint32_t* __restrict__ out) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (row_off[mid + 1] - row_off[mid] >= deg) lo = mid + 1;
+    else hi = mid;
+  }
+  *out = (uint32_t)lo;
+}
+
+uint32_t hub_end(Engine& eng, Part& p, uint32_t deg) {
+  if (deg == 0) return 0;  // no row is held back by degree
+  if (p.hub_deg != deg) {
+    DevBuf<uint32_t> d(1);
+    k_hub_end<<<1, 1, 0, eng.stream>>>(p.row_off.get(), p.nz_end, deg, d.get());
+    TG_CK(cudaGetLastError());
+    TG_CK(cudaMemcpyAsync(&p.hub_end, d.get(), 4, cudaMemcpyDeviceToHost, eng.stream));
+    TG_CK(cudaStreamSynchronize(eng.stream));
+    p.hub_deg = deg;
+  }
+  return p.hub_end;
 }
 
 }  // namespace
@@ -96,7 +125,16 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   eng.launches = 0;
   eng.comm_bytes = 0;
   cudaStream_t s = eng.stream;
-  const uint32_t delta = sssp_delta();
+  // Near-far (A19b): with delta > 0 a row waits while its distance
+  // is >= min + delta, but only rows of out-degree >= hub_deg wait (hub_deg 0:
+  // every row).  Rows below it are cheap and relax Bellman-Ford style.
+  // Defaults from the RMAT-28 sweep (profiles/r01_sssp_hub_sweep.txt):
+  // delta 1 / hub_deg 128 relaxes 1.5x fewer edges than plain Bellman-Ford.
+  const uint32_t delta = env_u32("TG_SSSP_DELTA", 1);
+  const uint32_t hub_deg = env_u32("TG_SSSP_HUB_DEG", 128);
+  std::vector<uint32_t> hubs(eng.parts.size(), 0);
+  if (delta)
+    for (size_t i = 0; i < eng.parts.size(); ++i) hubs[i] = hub_end(eng, *eng.parts[i], hub_deg);
   const bool trace = std::getenv("TG_TRACE") && std::getenv("TG_TRACE")[0] == '1';
   uint64_t bm_bytes = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
@@ -125,12 +163,12 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get() + 5, 0xFF, 8, s));
     const uint64_t th = delta ? mind + delta : (uint64_t)kInf;
     const uint32_t thresh = th >= (uint64_t)kInf ? kInf : (uint32_t)th;
-    for (auto& pp : eng.parts) {
-      Part& p = *pp;
+    for (size_t i = 0; i < eng.parts.size(); ++i) {
+      Part& p = *eng.parts[i];
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
       SsspOp op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
-                f.counters.get() + 4, thresh};
+                f.counters.get() + 4, thresh, hub_deg ? hubs[i] : kInf};
       launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
     }
     supersteps++;
