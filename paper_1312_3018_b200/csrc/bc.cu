@@ -321,9 +321,9 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       lvl_out.push_back(v.degsum);
       lvl_in.push_back(v.indegsum);
       if (dir.trace)
-        std::fprintf(stderr, "[tg bc] L=%u %s frontier=%llu edges=%llu next=%llu\n", L,
+        std::fprintf(stderr, "[tg bc] L=%u %s frontier=%llu edges=%llu next=%llu ms=%.3f\n", L,
                      pull ? "pull" : "push", (unsigned long long)lvl_count[L],
-                     (unsigned long long)v.edges, (unsigned long long)v.count);
+                     (unsigned long long)v.edges, (unsigned long long)v.count, dir.lap(s));
       // push: col 4 per edge; offsets 16 + sigma[v] 8 per frontier vertex;
       // sigma[t] 8 per newly reached vertex; 3 bitmap passes.  pull: in_col 4
       // per examined in-edge; in-offsets 16 per unvisited vertex; sigma 8 per
@@ -384,9 +384,9 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           }
         }
         if (dir.trace)
-          std::fprintf(stderr, "[tg bc-bwd] L=%u %s out(F[L])=%llu in(F[L+1])=%llu\n", L,
+          std::fprintf(stderr, "[tg bc-bwd] L=%u %s out(F[L])=%llu in(F[L+1])=%llu ms=%.3f\n", L,
                        push ? "push" : "pull", (unsigned long long)lvl_out[L],
-                       (unsigned long long)lvl_in[L + 1]);
+                       (unsigned long long)lvl_in[L + 1], dir.lap(s));
         // backward expand: c 8 per successor (read once); offsets 16 + dsum 8
         // per level-L vertex; level + successor bitmaps (+ 4 B per edge below)
         eng.prof_bytes(TG_K_BCB_EXPAND,

@@ -197,10 +197,10 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
       eng.prof_bytes(TG_K_BFS_EXPAND, 4.0 * v.edges + 16.0 * frontier + 3.0 * bm_bytes);
     visited_total += v.count;
     if (dir.trace)
-      std::fprintf(stderr, "[tg bfs] L=%u %s frontier=%llu edges=%llu next=%llu next_mf=%llu\n",
+      std::fprintf(stderr, "[tg bfs] L=%u %s frontier=%llu edges=%llu next=%llu next_mf=%llu ms=%.3f\n",
                    L, bottom_up ? "bottom-up" : "top-down", (unsigned long long)frontier,
                    (unsigned long long)v.edges, (unsigned long long)v.count,
-                   (unsigned long long)v.degsum);
+                   (unsigned long long)v.degsum, dir.lap(eng.stream));
     edges_total += v.edges;
     frontier = v.count;
     if (v.count == 0) break;  // termination vote

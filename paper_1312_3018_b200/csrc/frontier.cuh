@@ -19,6 +19,8 @@
 //                    vote count and the tile bitmap of the next superstep.
 #pragma once
 
+#include <chrono>
+
 #include "engine.cuh"
 
 namespace tg {
@@ -182,6 +184,15 @@ struct DirectionPolicy {
   int mode = 0;  // 0 auto, 1 top-down only, 2 always bottom-up
   double alpha = 14.0, bc_alpha = 2.0, beta = 24.0;
   bool trace = false;  // one stderr line per superstep
+  // trace only: ms since the previous lap (synchronizes the stream)
+  mutable std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  double lap(cudaStream_t s) const {
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(now - last).count();
+    last = now;
+    return ms;
+  }
   bool bottom_up(const Engine& eng, uint64_t nf, uint64_t mf, uint64_t mu, bool was_bu,
                  double a) const {
     if (eng.P != 1 || !eng.has_in || mode == 1) return false;

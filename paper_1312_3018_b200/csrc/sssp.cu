@@ -136,6 +136,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   if (delta)
     for (size_t i = 0; i < eng.parts.size(); ++i) hubs[i] = hub_end(eng, *eng.parts[i], hub_deg);
   const bool trace = std::getenv("TG_TRACE") && std::getenv("TG_TRACE")[0] == '1';
+  const DirectionPolicy tclock;  // trace lap clock only
   uint64_t bm_bytes = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   if (eng.P == 1) eng.l2_window(eng.parts[0]->fs.vals.get(), eng.parts[0]->Vp * 4);
@@ -198,10 +199,10 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     // relaxed vertex; active + next bitmaps one pass each
     eng.prof_bytes(TG_K_SSSP_EXPAND, 12.0 * v.edges + 20.0 * frontier + 2.0 * bm_bytes);
     if (trace)
-      std::fprintf(stderr, "[tg sssp] step=%llu thresh=%u active=%llu edges=%llu next=%llu min=%llu\n",
+      std::fprintf(stderr, "[tg sssp] step=%llu thresh=%u active=%llu edges=%llu next=%llu min=%llu ms=%.3f\n",
                    (unsigned long long)supersteps, thresh, (unsigned long long)frontier,
                    (unsigned long long)v.edges, (unsigned long long)v.count,
-                   (unsigned long long)v.minval);
+                   (unsigned long long)v.minval, tclock.lap(s));
     relax += v.edges;
     frontier = v.count;
     activations += v.count;
