@@ -114,6 +114,47 @@ int tg_engine_create_rmat(int scale, int edge_factor, double a, double b, double
 
 void tg_engine_free(tg_engine* eng);
 
+/* ---- host graphs and input generation ------------------------------------
+ * The load step of the paper's calling sequence (graph_initialize) as a
+ * library-owned host edge list that tg_engine_create partitions and uploads.
+ * Edge order is kept as given (the engine sorts each CSR row itself). */
+typedef struct tg_graph tg_graph;
+
+/* Copy an explicit directed edge list (host arrays of length E; w nullable =
+ * unweighted).  TG_EINVAL if an id is >= V or V is outside [1, 2^31). */
+int tg_graph_from_edges(uint64_t V, uint64_t E, const uint32_t* src, const uint32_t* dst,
+                        const uint32_t* w, tg_graph** out);
+
+/* Text edge list (the paper's loader is artifact plumbing):
+ * one edge per line, "src dst" or, with weighted = 1, "src dst weight";
+ * blank lines and lines starting with '#' are skipped; a comment "# nodes: N"
+ * fixes V (otherwise V = 1 + max id).  directed = 0 stores every edge in both
+ * directions.  Errors: TG_EIO if the file cannot be read; TG_EINVAL for a
+ * malformed line, a negative or missing weight, or an id >= the declared V --
+ * the message names the line number. */
+int tg_graph_load_edge_list(const char* path, int directed, int weighted, tg_graph** out);
+
+int tg_graph_info(const tg_graph* g, uint64_t* V, uint64_t* E, int* weighted);
+/* Copy the edges out (host arrays of length E; w ignored when NULL or when the
+ * graph is unweighted). */
+int tg_graph_edges(const tg_graph* g, uint32_t* src, uint32_t* dst, uint32_t* w);
+void tg_graph_free(tg_graph* g);
+
+/* Partition + upload a host graph (same attributes and rules as
+ * tg_engine_create_edges; attr->weighted requires a weighted graph). */
+int tg_engine_create(const tg_graph* g, const tg_attr* attr, tg_engine** out);
+
+/* Edges [first, first+count) of the RMAT stream tg_engine_create_rmat builds
+ * from (inputs/tg_inputs.h: counter-based, so any slice is independent),
+ * generated on the calling thread's current CUDA device into src/dst (and the
+ * SSSP weights 1 + mix64(wseed*phi + k) mod 63 into w when w != NULL), arrays
+ * of length count in `mem`.  (a, b, c) = (0.25, 0.25, 0.25) is the UNIFORM
+ * graph (every endpoint bit independent and fair).  TG_EINVAL as
+ * tg_engine_create_rmat, or if first + count > edge_factor * 2^scale. */
+int tg_rmat_edges(int scale, int edge_factor, double a, double b, double c, uint64_t seed,
+                  int scramble, uint64_t wseed, uint64_t first, uint64_t count, uint32_t* src,
+                  uint32_t* dst, uint32_t* w, int mem);
+
 /* |V_p| of partition p of P under the degree-serpentine deal (host only; no
  * device needed): rounds r = i / P deal positions j = i % P to partition
  * (r even ? j : P-1-j).  TG_EINVAL if P < 1, P > TG_MAX_PARTITIONS or p out of

@@ -9,6 +9,7 @@ from .tgraph import (  # noqa: F401
     TG_MEM_DEVICE,
     TG_MEM_HOST,
     Engine,
+    Graph,
     Stats,
     TGraphError,
     TorchComm,
@@ -16,11 +17,13 @@ from .tgraph import (  # noqa: F401
     lib,
     tg_bc,
     tg_bfs,
+    tg_engine_create,
     tg_engine_create_edges,
     tg_engine_create_rmat,
     tg_engine_free,
     tg_engine_info,
     tg_engine_partition_info,
     tg_pagerank,
+    tg_rmat_edges,
     tg_sssp,
 )

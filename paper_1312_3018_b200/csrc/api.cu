@@ -366,7 +366,7 @@ void collect_u32(Engine& eng, uint32_t* out, int mem) {
   collect(eng, [](Part& p) -> const void* { return p.fs.vals.get(); }, 4, out, mem);
 }
 
-static int guard(const std::function<void()>& f) {
+int guard(const std::function<void()>& f) {
   try {
     f();
     g_last_error.clear();

@@ -164,7 +164,7 @@ __global__ void k_bc_pack(const uint32_t* lid, uint64_t I, const uint32_t* succ,
 
 // delta, bc and c for the vertices of level L (one warp per bitmap word)
 __global__ void k_bc_level(const uint32_t* F, uint64_t Vp, uint64_t nz_end, const double* sigma,
-                           const double* dsum, double* bc, double* c) {
+                           const double* dsum, double* bc, double* c, unsigned long long* inexact) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t nwords = words_for(Vp);
@@ -173,6 +173,8 @@ __global__ void k_bc_level(const uint32_t* F, uint64_t Vp, uint64_t nz_end, cons
     if (!((x >> lane) & 1u)) continue;
     const uint64_t v = w * 32 + lane;
     const double sv = sigma[v];
+    // reading A11: path counts are exact fp64 integers only below 2^53
+    if (sv >= 9007199254740992.0) atomicOr(inexact, 1ull);
     const double delta = v < nz_end ? sv * dsum[v] : 0.0;
     bc[v] += delta;
     c[v] = (1.0 + delta) / sv;
@@ -214,6 +216,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       b.ibox_pack.alloc(std::max<uint64_t>(p.I, 1));
     }
     TG_CK(cudaMemsetAsync(b.bc.get(), 0, Vn * 8, s));
+    TG_CK(cudaMemsetAsync(p.fs.counters.get() + 4, 0, 8, s));  // sigma >= 2^53 flag
   }
   eng.launches = 0;
   eng.comm_bytes = 0;
@@ -398,7 +401,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         if (!p.Vp) continue;
         k_bc_level<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
             p.bcs.level_bm[L].get(), p.Vp, p.nz_end, p.bcs.sigma.get(), p.bcs.dsum.get(),
-            p.bcs.bc.get(), p.bcs.c.get());
+            p.bcs.bc.get(), p.bcs.c.get(), p.fs.counters.get() + 4);
         TG_CK(cudaGetLastError());
         eng.launches++;
       }
@@ -414,6 +417,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     // sigma/dsum/bc/c 32
     bytes += 32 * tr + 64 * nreached;
   }
+  TG_REQUIRE(read_counts(eng, 4) == 0, TG_EINTERNAL,
+             "tg_bc: a shortest-path count reached 2^53 (no longer exact in fp64, reading A11)");
   if (st) {
     st->device_ms = total_ms;
     st->supersteps = supersteps;

@@ -161,9 +161,19 @@ def lib():
         L.tg_engine_kernel_stat.argtypes = [p, i32, C.POINTER(tg_kernel_stat)]
         L.tg_kernel_name.argtypes = [i32]
         L.tg_kernel_name.restype = C.c_char_p
+        L.tg_graph_from_edges.argtypes = [u64, u64, p, p, p, C.POINTER(p)]
+        L.tg_graph_load_edge_list.argtypes = [C.c_char_p, i32, i32, C.POINTER(p)]
+        L.tg_graph_info.argtypes = [p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(i32)]
+        L.tg_graph_edges.argtypes = [p, p, p, p]
+        L.tg_graph_free.argtypes = [p]
+        L.tg_graph_free.restype = None
+        L.tg_engine_create.argtypes = [p, C.POINTER(tg_attr), C.POINTER(p)]
+        L.tg_rmat_edges.argtypes = [i32, i32, dbl, dbl, dbl, u64, i32, u64, u64, u64, p, p, p, i32]
         for f in ("tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
                   "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc",
-                  "tg_engine_set_profiling", "tg_engine_kernel_stat"):
+                  "tg_engine_set_profiling", "tg_engine_kernel_stat", "tg_graph_from_edges",
+                  "tg_graph_load_edge_list", "tg_graph_info", "tg_graph_edges", "tg_engine_create",
+                  "tg_rmat_edges"):
             getattr(L, f).restype = i32
         _LIB = L
     return _LIB
@@ -216,6 +226,88 @@ def tg_engine_create_rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1,
     h = C.c_void_p()
     _check(lib().tg_engine_create_rmat(scale, edge_factor, a, b, c, seed, int(scramble), wseed,
                                        C.byref(at), C.byref(h)))
+    return h
+
+
+def tg_rmat_edges(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, scramble=True, wseed=2,
+                  first=0, count=None, weights=False, out=None):
+    """Slice [first, first+count) of the RMAT stream, generated on the current
+    CUDA device -> (src, dst, w|None) numpy u32 (or into `out` = (src, dst, w)
+    device tensors)."""
+    E = edge_factor << scale
+    count = E - first if count is None else count
+    if out is None:
+        src, dst = np.empty(count, np.uint32), np.empty(count, np.uint32)
+        w = np.empty(count, np.uint32) if weights else None
+    else:
+        src, dst, w = out
+    ps, ms, k1 = _arr(src, np.uint32)
+    pd, md, k2 = _arr(dst, np.uint32)
+    pw, mw, k3 = _arr(w, np.uint32)
+    if ms != md or (w is not None and mw != ms):
+        raise ValueError("src, dst and w must live in the same memory")
+    _check(lib().tg_rmat_edges(scale, edge_factor, a, b, c, seed, int(scramble), wseed, first, count,
+                               ps, pd, pw, ms))
+    return src, dst, w
+
+
+class Graph:
+    """Library-owned host edge list (tg_graph): the load step."""
+
+    def __init__(self, handle):
+        self.h = handle
+        V, E, wt = C.c_uint64(), C.c_uint64(), C.c_int()
+        _check(lib().tg_graph_info(handle, C.byref(V), C.byref(E), C.byref(wt)))
+        self.V, self.E, self.weighted = V.value, E.value, bool(wt.value)
+
+    @classmethod
+    def from_edges(cls, V, src, dst, w=None) -> "Graph":
+        s = np.ascontiguousarray(src, np.uint32)
+        d = np.ascontiguousarray(dst, np.uint32)
+        ww = None if w is None else np.ascontiguousarray(w, np.uint32)
+        if len(s) != len(d) or (ww is not None and len(ww) != len(s)):
+            raise ValueError("src, dst and w must have the same length")
+        h = C.c_void_p()
+        _check(lib().tg_graph_from_edges(V, len(s), s.ctypes.data_as(C.c_void_p),
+                                         d.ctypes.data_as(C.c_void_p),
+                                         None if ww is None else ww.ctypes.data_as(C.c_void_p),
+                                         C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load_edge_list(cls, path, directed=True, weighted=False) -> "Graph":
+        h = C.c_void_p()
+        _check(lib().tg_graph_load_edge_list(os.fsencode(path), int(directed), int(weighted),
+                                             C.byref(h)))
+        return cls(h)
+
+    def edges(self):
+        src, dst = np.empty(self.E, np.uint32), np.empty(self.E, np.uint32)
+        w = np.empty(self.E, np.uint32) if self.weighted else None
+        _check(lib().tg_graph_edges(self.h, src.ctypes.data_as(C.c_void_p),
+                                    dst.ctypes.data_as(C.c_void_p),
+                                    None if w is None else w.ctypes.data_as(C.c_void_p)))
+        return src, dst, w
+
+    def close(self):
+        if self.h:
+            lib().tg_graph_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def tg_engine_create(graph: Graph, partitions=1, device=0, weighted=None, in_csr=True, rank=0, world=1,
+                     comm=None):
+    if weighted is None:
+        weighted = graph.weighted
+    at = _attr(partitions, device, weighted, in_csr, rank, world, comm)
+    h = C.c_void_p()
+    _check(lib().tg_engine_create(graph.h, C.byref(at), C.byref(h)))
     return h
 
 
@@ -313,6 +405,10 @@ class Engine:
     @classmethod
     def from_edges(cls, V, src, dst, w=None, **kw) -> "Engine":
         return cls(tg_engine_create_edges(V, src, dst, w, **kw), kw.get("comm"), kw.get("rank", 0))
+
+    @classmethod
+    def from_graph(cls, graph: "Graph", **kw) -> "Engine":
+        return cls(tg_engine_create(graph, **kw), kw.get("comm"), kw.get("rank", 0))
 
     @classmethod
     def rmat(cls, scale, **kw) -> "Engine":

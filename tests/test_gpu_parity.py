@@ -247,6 +247,83 @@ def test_device_outputs(tg):
     assert_pr(r.cpu().numpy(), G.pagerank(5))
 
 
+def layered(width, layers):
+    """Source 0 -> layer 1 -> ... -> layer `layers`, complete bipartite between
+    consecutive layers: sigma at layer k = width^(k-1) (width^k paths minus the
+    single source fan-out)."""
+    src, dst = [], []
+    prev = [0]
+    nxt_id = 1
+    for _ in range(layers):
+        cur = list(range(nxt_id, nxt_id + width))
+        nxt_id += width
+        for a in prev:
+            for b in cur:
+                src.append(a)
+                dst.append(b)
+        prev = cur
+    return nxt_id, np.array(src, np.uint32), np.array(dst, np.uint32)
+
+
+def test_bc_sigma_exactness_guard(tg):
+    # reading A11: sigma is an fp64 path count, exact below 2^53.  Width 2,
+    # 53 layers: sigma tops out at 2^52 -> exact, equals the oracle; width 2,
+    # 55 layers: 2^54 -> TG_EINTERNAL instead of a silently rounded answer.
+    V, s, d = layered(2, 53)
+    G, eng = both(tg, V, s, d)
+    assert_bc(eng.bc([0])[0], G.bc([0]))
+    V, s, d = layered(2, 55)
+    eng = tg.Engine.from_edges(V, s, d)
+    with pytest.raises(tg.TGraphError) as e:
+        eng.bc([0])
+    assert e.value.code == 5 and "2^53" in str(e.value)
+
+
+# ------------------------------------------------- host graphs / input generation
+def test_rmat_slice_matches_the_generator(tg):
+    # tg_rmat_edges (device) and inputs.rmat_edges (host C) evaluate the same
+    # counter-based stream: any slice agrees element by element.
+    for scale, first, count in ((12, 0, 5000), (20, 123456789 % (16 << 20), 70000)):
+        s, d, w = tg.tg_rmat_edges(scale, first=first, count=count, weights=True)
+        hs, hd, hw = inputs.rmat_edges(scale, first=first, count=count, weights=True)
+        assert np.array_equal(s, hs) and np.array_equal(d, hd) and np.array_equal(w, hw)
+    import torch
+    out = tuple(torch.empty(3000, dtype=torch.int32, device="cuda:0") for _ in range(3))
+    tg.tg_rmat_edges(10, a=0.25, b=0.25, c=0.25, first=77, count=3000, out=out, weights=True)
+    hs, hd, hw = inputs.rmat_edges(10, a=0.25, b=0.25, c=0.25, first=77, count=3000, weights=True)
+    for t, h in zip(out, (hs, hd, hw)):
+        assert np.array_equal(t.cpu().numpy().view(np.uint32), h)
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_engine_from_edge_list_file(tg, tmp_path, P):
+    rng = np.random.default_rng(11)
+    V, E = 300, 2400
+    src, dst = rng.integers(0, V, E), rng.integers(0, V, E)
+    w = rng.integers(1, 64, E)
+    path = tmp_path / "g.txt"
+    with open(path, "w") as f:
+        f.write(f"# nodes: {V}\n")
+        for a, b, c in zip(src, dst, w):
+            f.write(f"{a} {b} {c}\n")
+    g = tg.Graph.load_edge_list(str(path), weighted=True)
+    eng = tg.Engine.from_graph(g, partitions=P)
+    G = oracle.Graph(V, src, dst, w)
+    check_all(tg, G, eng, bfs_src=(0, 5, 299), sssp_src=(0, 17), pr_T=(1, 5), bc_src=(0, 3, 8))
+
+
+def test_uniform_graph(tg):
+    # (a, b, c) = (0.25, 0.25, 0.25): every endpoint bit fair -- the UNIFORM
+    # graph of the paper's Fig. 4 / SPEC generate_uniform
+    scale = 12
+    src, dst, w = inputs.rmat_edges(scale, a=0.25, b=0.25, c=0.25, weights=True)
+    G = oracle.Graph(1 << scale, src, dst, w)
+    for P in (1, 4):
+        eng = tg.Engine.rmat(scale, a=0.25, b=0.25, c=0.25, partitions=P)
+        ss = inputs.rmat_sources(scale, 3, a=0.25, b=0.25, c=0.25)
+        check_all(tg, G, eng, bfs_src=ss, sssp_src=ss[:2], pr_T=(5,), bc_src=ss[:2])
+
+
 # ------------------------------------------------------------ C2: RMAT-22, 1 GPU
 @pytest.fixture(scope="module")
 def c2(tg):
