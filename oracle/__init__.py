@@ -41,10 +41,14 @@ def lib():
         L.oracle_sssp_cert_edges.argtypes = [u64, p, u64, p, p, p, p, p]
         L.oracle_cert_finish.argtypes = [u64, u64, p, p, p]
         L.oracle_pr_sample_edges.argtypes = [u64, u64, p, p, p, p, p, p, p]
+        L.oracle_cc.argtypes = [u64, p, p, p]
+        L.oracle_cc_edges.argtypes = [u64, p, u64, p, p]
+        L.oracle_cc_finish.argtypes = [u64, p, p]
         for f in ("oracle_csr", "oracle_bfs", "oracle_sssp", "oracle_pagerank", "oracle_bc",
                   "oracle_partition", "oracle_beta", "oracle_bfs_certify",
                   "oracle_sssp_certify", "oracle_outdeg_edges", "oracle_bfs_cert_edges",
-                  "oracle_sssp_cert_edges", "oracle_cert_finish", "oracle_pr_sample_edges"):
+                  "oracle_sssp_cert_edges", "oracle_cert_finish", "oracle_pr_sample_edges",
+                  "oracle_cc", "oracle_cc_edges", "oracle_cc_finish"):
             getattr(L, f).restype = i32
         _LIB = L
     return _LIB
@@ -102,6 +106,12 @@ class Graph:
         out = np.empty(self.V, np.float64)
         _check(lib().oracle_bc(self.V, _p(self.row_off), _p(self.col), _p(s), len(s), _p(out)),
                "oracle_bc")
+        return out
+
+    def cc(self) -> np.ndarray:
+        """Weakly connected components: label = smallest id of the component."""
+        out = np.empty(self.V, np.uint32)
+        _check(lib().oracle_cc(self.V, _p(self.row_off), _p(self.col), _p(out)), "oracle_cc")
         return out
 
     def partition(self, P: int):
@@ -163,6 +173,25 @@ class StreamingCertificate:
             return False
         b = np.zeros(1, np.uint64)
         return lib().oracle_cert_finish(self.V, self.s, _p(self.val), _p(self.tight), _p(b)) == 0
+
+
+class StreamingCC:
+    """Union-find connected components over an edge stream fed in chunks."""
+
+    def __init__(self, V: int):
+        self.V = int(V)
+        self.parent = np.arange(self.V, dtype=np.uint32)
+
+    def feed(self, src, dst) -> None:
+        src = np.ascontiguousarray(src, np.uint32)
+        dst = np.ascontiguousarray(dst, np.uint32)
+        _check(lib().oracle_cc_edges(self.V, _p(self.parent), len(src), _p(src), _p(dst)),
+               "oracle_cc_edges")
+
+    def labels(self) -> np.ndarray:
+        out = np.empty(self.V, np.uint32)
+        _check(lib().oracle_cc_finish(self.V, _p(self.parent), _p(out)), "oracle_cc_finish")
+        return out
 
 
 def outdeg_edges(V: int, src, outdeg: np.ndarray) -> None:

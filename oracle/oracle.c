@@ -197,6 +197,52 @@ int oracle_bc(uint64_t V, const uint64_t* row_off, const uint32_t* col, const ui
   return OK;
 }
 
+/* ---- connected components: union-find (oracle.h) ---- */
+static uint32_t uf_find(uint32_t* parent, uint32_t x) {
+  while (parent[x] != x) {
+    parent[x] = parent[parent[x]];  /* path halving */
+    x = parent[x];
+  }
+  return x;
+}
+
+static void uf_union(uint32_t* parent, uint32_t a, uint32_t b) {
+  a = uf_find(parent, a);
+  b = uf_find(parent, b);
+  if (a == b) return;
+  /* the smaller id becomes the root, so every root is the minimum of its set */
+  if (a < b) parent[b] = a;
+  else parent[a] = b;
+}
+
+int oracle_cc_edges(uint64_t V, uint32_t* parent, uint64_t n, const uint32_t* src,
+                    const uint32_t* dst) {
+  if (!parent || (n && (!src || !dst))) return EINVAL_;
+  for (uint64_t k = 0; k < n; ++k) {
+    if (src[k] >= V || dst[k] >= V) return EINVAL_;
+    uf_union(parent, src[k], dst[k]);
+  }
+  return OK;
+}
+
+int oracle_cc_finish(uint64_t V, uint32_t* parent, uint32_t* label) {
+  if (!parent || !label) return EINVAL_;
+  for (uint64_t v = 0; v < V; ++v) label[v] = uf_find(parent, (uint32_t)v);
+  return OK;
+}
+
+int oracle_cc(uint64_t V, const uint64_t* row_off, const uint32_t* col, uint32_t* label) {
+  if (!row_off || !label) return EINVAL_;
+  uint32_t* parent = (uint32_t*)malloc((V ? V : 1) * sizeof(uint32_t));
+  if (!parent) return ENOMEM_;
+  for (uint64_t v = 0; v < V; ++v) parent[v] = (uint32_t)v;
+  for (uint64_t u = 0; u < V; ++u)
+    for (uint64_t e = row_off[u]; e < row_off[u + 1]; ++e) uf_union(parent, (uint32_t)u, col[e]);
+  const int rc = oracle_cc_finish(V, parent, label);
+  free(parent);
+  return rc;
+}
+
 /* qsort comparator context: (degree desc, id asc) */
 static const uint64_t* g_cmp_row_off;
 static int cmp_deg_desc(const void* a, const void* b) {

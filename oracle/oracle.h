@@ -59,6 +59,19 @@ int oracle_pagerank(uint64_t V, const uint64_t* row_off, const uint32_t* col, in
 int oracle_bc(uint64_t V, const uint64_t* row_off, const uint32_t* col, const uint64_t* sources,
               int k, double* bc);
 
+/* Connected components of the graph read as UNDIRECTED ("minimum 'label'
+ * in a connected components algorithm"; Table 5 note: CC "operates on
+ * undirected graphs"): label[v] = the smallest vertex id in
+ * v's weakly connected component.  Union-find (union by smaller root id, path
+ * halving) over every edge, then each vertex takes its root, which is the
+ * minimum of its set by construction.  Not the paper's label propagation. */
+int oracle_cc(uint64_t V, const uint64_t* row_off, const uint32_t* col, uint32_t* label);
+/* Streaming form: parent[] (length V, initialised parent[v] = v by the caller)
+ * absorbs edge chunks; oracle_cc_finish writes the labels. */
+int oracle_cc_edges(uint64_t V, uint32_t* parent, uint64_t n, const uint32_t* src,
+                    const uint32_t* dst);
+int oracle_cc_finish(uint64_t V, uint32_t* parent, uint32_t* label);
+
 /* Degree-aware partition (reading A23; §6.2 degree centrality):
  * vertices ordered by out-degree descending, ties by id ascending, dealt in
  * serpentine order over P partitions: order position i, round r = i / P,

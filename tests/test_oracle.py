@@ -410,3 +410,64 @@ def test_bc_single_source_dependency_identity():
         lv = G.bfs(s).astype(np.int64)
         reached = (lv != INF32) & (np.arange(n) != s)
         assert np.isclose(G.bc([s]).sum(), (lv[reached] - 1).sum(), rtol=1e-12, atol=1e-9)
+
+
+# ------------------------------------------------------------ connected components
+def undirected_closure_labels(n, src, dst):
+    """Brute force: boolean reachability closure of the symmetrised adjacency
+    (repeated squaring), label = smallest reachable id (v reaches itself)."""
+    A = np.eye(n, dtype=bool)
+    for a, b in zip(src, dst):
+        A[a, b] = A[b, a] = True
+    for _ in range(max(1, int(np.ceil(np.log2(max(n, 2)))))):
+        A = (A.astype(np.int64) @ A.astype(np.int64)) > 0
+    return np.array([np.flatnonzero(A[v]).min() for v in range(n)], np.uint32)
+
+
+def test_cc_golden():
+    for key in ("cc_two_edges", "cc_path5"):
+        g = GOLD[key]
+        G = oracle.Graph(g["V"], g["src"], g["dst"])
+        assert G.cc().tolist() == g["labels"], key
+
+
+def test_cc_vs_brute_force_closure_and_direction_invariance():
+    rng = np.random.default_rng(31)
+    for _ in range(300):
+        n = int(rng.integers(1, 9))
+        src, dst = random_multigraph(rng, n, int(rng.integers(0, 2 * n)))
+        want = undirected_closure_labels(n, src, dst)
+        assert np.array_equal(oracle.Graph(n, src, dst).cc(), want)
+        # weak components ignore edge direction
+        assert np.array_equal(oracle.Graph(n, dst, src).cc(), want)
+
+
+def test_cc_vs_scipy_weak_components():
+    from scipy.sparse import coo_matrix
+    from scipy.sparse.csgraph import connected_components
+
+    rng = np.random.default_rng(32)
+    for n, m in ((50, 30), (500, 400), (3000, 2500), (2000, 8000)):
+        src, dst = random_multigraph(rng, n, m)
+        A = coo_matrix((np.ones(len(src)), (src, dst)), shape=(n, n))
+        k, comp = connected_components(A, directed=True, connection="weak")
+        mins = np.full(k, n, np.int64)
+        np.minimum.at(mins, comp, np.arange(n))
+        lab = oracle.Graph(n, src, dst).cc()
+        assert np.array_equal(lab, mins[comp].astype(np.uint32))
+        assert len(np.unique(lab)) == k
+
+
+def test_cc_streaming_equals_in_memory_and_invariants():
+    rng = np.random.default_rng(33)
+    n = 4000
+    src, dst = random_multigraph(rng, n, 3500)
+    want = oracle.Graph(n, src, dst).cc()
+    S = oracle.StreamingCC(n)
+    for i in range(0, len(src), 777):
+        S.feed(src[i:i + 777], dst[i:i + 777])
+    lab = S.labels()
+    assert np.array_equal(lab, want)
+    # label[v] <= v, labels are fixed points, and every edge joins equal labels
+    assert (lab <= np.arange(n)).all() and np.array_equal(lab[lab], lab)
+    assert np.array_equal(lab[src], lab[dst])
