@@ -218,6 +218,14 @@ int tg_pagerank(tg_engine* eng, int iterations, double damping, float* rank, int
  * directed.  sources: host array of k global ids.  bc overwritten. */
 int tg_bc(tg_engine* eng, const uint64_t* sources, int k, double* bc, int mem, tg_stats* stats);
 
+/* Connected components by minimum-label propagation ("minimum 'label' in
+ * a connected components algorithm"; CC operates on undirected graphs;
+ * reading A29): the engine's directed edges are read as undirected, and
+ * labels[v] = the smallest global vertex id of v's (weakly) connected
+ * component.  Needs the in-CSR (attr.build_in_csr), else TG_EINVAL.
+ * traversed_edges = |E| (each input edge once). */
+int tg_cc(tg_engine* eng, uint32_t* labels, int mem, tg_stats* stats);
+
 /* ---- kernel ledger (measurement) --------------------------------------------
  * With profiling on, the library brackets each hot kernel launch with CUDA
  * events on the engine stream (the stream the kernel runs on) and accumulates,
@@ -233,7 +241,8 @@ typedef enum {
   TG_K_ADVANCE = 5,      /* frontier advance / vote count                 */
   TG_K_COMPACT = 6,      /* active-tile compaction                        */
   TG_K_EXCHANGE = 7,     /* inter-partition message exchange + scatter    */
-  TG_K_COUNT = 8
+  TG_K_CC_EXPAND = 8,    /* CC label push, out- and in-CSR (edge tiles)   */
+  TG_K_COUNT = 9
 } tg_kernel_id;
 
 typedef struct {

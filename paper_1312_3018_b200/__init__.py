@@ -16,6 +16,7 @@ from .tgraph import (  # noqa: F401
     tg_partition_size,
     lib,
     tg_bc,
+    tg_cc,
     tg_bfs,
     tg_engine_create,
     tg_engine_create_edges,

@@ -569,18 +569,18 @@ int tg_engine_partition_info(const tg_engine* e, int p, tg_part_info* info, uint
     body;                                                                \
   })
 
+// NULL outputs are rejected inside run_* except on non-root ranks of a
+// multi-process engine (results are written on rank 0 only).
 int tg_bfs(tg_engine* e, uint64_t source, uint32_t* levels, int mem, tg_stats* st) {
-  TG_RUN({
-    TG_REQUIRE(levels != nullptr, TG_EINVAL, "NULL levels");
-    run_bfs(eng, source, levels, mem, st);
-  });
+  TG_RUN({ run_bfs(eng, source, levels, mem, st); });
 }
 
 int tg_sssp(tg_engine* e, uint64_t source, uint32_t* dist, int mem, tg_stats* st) {
-  TG_RUN({
-    TG_REQUIRE(dist != nullptr, TG_EINVAL, "NULL dist");
-    run_sssp(eng, source, dist, mem, st);
-  });
+  TG_RUN({ run_sssp(eng, source, dist, mem, st); });
+}
+
+int tg_cc(tg_engine* e, uint32_t* labels, int mem, tg_stats* st) {
+  TG_RUN({ run_cc(eng, labels, mem, st); });
 }
 
 int tg_pagerank(tg_engine* e, int iterations, double damping, float* rank, int mem, tg_stats* st) {
@@ -613,7 +613,7 @@ int tg_engine_kernel_stat(const tg_engine* e, int kid, tg_kernel_stat* out) {
 const char* tg_kernel_name(int kid) {
   static const char* names[TG_K_COUNT] = {"bfs_expand",  "sssp_expand", "bc_fwd_expand",
                                           "bc_bwd_expand", "pr_pull",   "advance",
-                                          "tile_compact", "exchange_scatter"};
+                                          "tile_compact", "exchange_scatter", "cc_expand"};
   return (kid >= 0 && kid < TG_K_COUNT) ? names[kid] : "?";
 }
 

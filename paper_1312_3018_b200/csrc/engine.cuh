@@ -69,7 +69,8 @@ struct FrontierState {  // BFS / SSSP / BC-forward (messages arrive in Part::are
   DevBuf<uint32_t> cur, next, visited;            // bitmaps over local ids
   DevBuf<uint32_t> vals;                          // BFS level or SSSP dist (u32, Vp)
   DevBuf<uint32_t> obox_mark, obox_new;           // bitmaps over outbox slots
-  DevBuf<uint32_t> obox_u32;                      // SSSP min-combined distances
+  DevBuf<uint32_t> obox_u32;                      // SSSP / CC min-combined values
+  DevBuf<uint32_t> ibox_u32;                      // CC: owner-packed labels (reverse send)
   DevBuf<unsigned long long> counters;            // see Vote
 };
 
@@ -194,6 +195,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
 void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st);
 void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stats* st);
 void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, tg_stats* st);
+void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st);
 
 // Helpers shared by the algorithm TUs (api.cu)
 // Message exchange between partitions (the communication phase).

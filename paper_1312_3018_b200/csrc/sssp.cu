@@ -10,14 +10,15 @@
 //   scatter : dist[v] = min(dist[v], msg), activate on improvement.
 //   advance : next-active bitmap -> vote count + the smallest active distance.
 //
-// Near-far schedule (reading A19b): an active vertex is relaxed in a
-// superstep only if dist[v] < min_active_dist + Delta; the others stay active
-// for a later superstep (Davidson et al. 2014, the GPU SSSP work the paper
-// cites at P:649).  Any schedule of Bellman-Ford relaxations reaches the same
-// fixed point, so distances are identical; the schedule only removes redundant
-// relaxations.  Default Delta = 0 = infinity, i.e. plain Bellman-Ford: on
-// RMAT-28 every Delta in 16..512 relaxed as many edges (~1.9 E) and took longer
-// (profiles/r01_sssp_delta_sweep.txt); TG_SSSP_DELTA=<d> enables it.
+// Degree-aware near-far schedule (reading A19b): an active vertex of
+// out-degree >= hub_deg (128) is relaxed in a superstep only if dist[v] <
+// min_active_dist + Delta (1); otherwise it stays active for a later
+// superstep (after Davidson et al. 2014, the GPU SSSP work the paper cites at
+// P:649).  Rows below hub_deg always relax.  Any schedule of Bellman-Ford
+// relaxations reaches the same fixed point, so distances are identical; the
+// schedule only removes redundant relaxations of hubs (RMAT-28: 62 GB instead
+// of 92 GB, profiles/r01_sssp_hub_sweep.txt).  TG_SSSP_DELTA=0 gives plain
+// Bellman-Ford; TG_SSSP_HUB_DEG=0 makes every row wait (plain near-far).
 #include <cstdio>
 #include <cstdlib>
 

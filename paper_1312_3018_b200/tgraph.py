@@ -112,7 +112,7 @@ class tg_kernel_stat(C.Structure):
     _fields_ = [("launches", C.c_uint64), ("ms", C.c_double), ("algorithmic_bytes", C.c_double)]
 
 
-TG_K_COUNT = 8
+TG_K_COUNT = 9
 
 
 @dataclass
@@ -155,6 +155,7 @@ def lib():
         L.tg_sssp.argtypes = [p, u64, p, i32, C.POINTER(tg_stats)]
         L.tg_pagerank.argtypes = [p, i32, dbl, p, i32, C.POINTER(tg_stats)]
         L.tg_bc.argtypes = [p, p, i32, p, i32, C.POINTER(tg_stats)]
+        L.tg_cc.argtypes = [p, p, i32, C.POINTER(tg_stats)]
         L.tg_partition_size.argtypes = [u64, i32, i32, C.POINTER(C.c_uint64)]
         L.tg_partition_size.restype = i32
         L.tg_engine_set_profiling.argtypes = [p, i32]
@@ -171,7 +172,7 @@ def lib():
         L.tg_rmat_edges.argtypes = [i32, i32, dbl, dbl, dbl, u64, i32, u64, u64, u64, p, p, p, i32]
         for f in ("tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
                   "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc",
-                  "tg_engine_set_profiling", "tg_engine_kernel_stat", "tg_graph_from_edges",
+                  "tg_cc", "tg_engine_set_profiling", "tg_engine_kernel_stat", "tg_graph_from_edges",
                   "tg_graph_load_edge_list", "tg_graph_info", "tg_graph_edges", "tg_engine_create",
                   "tg_rmat_edges"):
             getattr(L, f).restype = i32
@@ -376,6 +377,13 @@ def tg_bc(h, V, sources, out=None):
     return out, Stats.of(st)
 
 
+def tg_cc(h, V, out=None):
+    out, ptr, mem = _out(out, V, np.uint32)
+    st = tg_stats()
+    _check(lib().tg_cc(h, ptr, mem, C.byref(st)))
+    return out, Stats.of(st)
+
+
 def tg_engine_set_profiling(h, on: bool) -> None:
     _check(lib().tg_engine_set_profiling(h, int(on)))
 
@@ -439,6 +447,9 @@ class Engine:
 
     def bc(self, sources, out=None):
         return tg_bc(self.h, self.V, sources, out)
+
+    def cc(self, out=None):
+        return tg_cc(self.h, self.V, out)
 
     def set_profiling(self, on=True):
         tg_engine_set_profiling(self.h, on)

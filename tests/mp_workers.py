@@ -85,7 +85,8 @@ def engine_worker(rank, world, port, scale, device):
         out = {"bfs": [eng.bfs(s)[0].copy() for s in srcs],
                "sssp": [eng.sssp(s)[0].copy() for s in srcs[:2]],
                "pr": eng.pagerank(5)[0].copy(),
-               "bc": eng.bc(srcs[:2])[0].copy()}
+               "bc": eng.bc(srcs[:2])[0].copy(),
+               "cc": eng.cc()[0].copy()}
         results.append(out)
     if rank == 0:
         import oracle
@@ -100,6 +101,7 @@ def engine_worker(rank, world, port, scale, device):
             assert (np.abs(out["pr"] - ref) / ref).max() <= 1e-5
             bref = G.bc(srcs[:2])
             assert np.allclose(out["bc"], bref, rtol=1e-4, atol=1e-12 * max(1.0, bref.max()))
+            assert np.array_equal(out["cc"], G.cc()), "cc"
     eng_e.close()
     eng_g.close()
     dist.barrier()

@@ -10,6 +10,10 @@ regenerated on the host by the shared input generator:
   vertex sample (hubs + random), plus the global mass identity;
 * BC (one source): sum_v delta_s(v) = sum_{t reached} (d(s,t) - 1), delta >= 0,
   zero at the source and at unreached vertices.
+* CC: every edge joins equal labels, label[v] <= v, label[label[v]] ==
+  label[v] (local conditions: they prove labels are constant on components and
+  name a member vertex, not that two components were never merged -- exact
+  union-find parity is at RMAT-22 in test_gpu_cc.py).
 
 TG_FULL_SCALE=<s> runs the same checks at a smaller scale.
 """
@@ -39,6 +43,7 @@ def full():
     r4, _ = eng.pagerank(4)
     r5, _ = eng.pagerank(5)
     bc, _ = eng.bc([s])
+    cc, st_cc = eng.cc()
     eng.close()
 
     t0 = time.time()
@@ -47,6 +52,7 @@ def full():
     outdeg = np.zeros(V, np.uint32)
     indeg = np.zeros(V, np.uint32)
     chunk = 1 << 27
+    cc_edges_ok = True
     for first in range(0, E, chunk):                   # pass 1: certificates + degrees
         src, dst, w = inputs.rmat_edges(scale, weights=True, first=first,
                                         count=min(chunk, E - first))
@@ -54,6 +60,7 @@ def full():
         sssp_c.feed(src, dst, w)
         oracle.outdeg_edges(V, src, outdeg)
         oracle.outdeg_edges(V, dst, indeg)
+        cc_edges_ok = cc_edges_ok and bool(np.array_equal(cc[src], cc[dst]))
     rng = np.random.default_rng(2024)
     sample = np.unique(np.concatenate([np.argsort(indeg)[-256:], rng.integers(0, V, 8192)]))
     mask = np.zeros((V + 63) // 64, np.uint64)
@@ -66,7 +73,8 @@ def full():
         oracle.pr_sample_edges(V, src, dst, mask, slot, r4, outdeg, acc)
     print(f"full-scale host checks: {time.time() - t0:.1f} s")
     return dict(scale=scale, V=V, E=E, s=s, lv=lv, dist=dist, r4=r4, r5=r5, bc=bc, bfs_c=bfs_c,
-                sssp_c=sssp_c, outdeg=outdeg, sample=sample, acc=acc, st_bfs=st_bfs)
+                sssp_c=sssp_c, outdeg=outdeg, indeg=indeg, sample=sample, acc=acc, st_bfs=st_bfs,
+                cc=cc, st_cc=st_cc, cc_edges_ok=cc_edges_ok)
 
 
 def test_full_bfs_certificate(full):
@@ -100,3 +108,13 @@ def test_full_bc_dependency_identity(full):
     assert abs(bc.sum() - expect) <= 1e-6 * max(expect, 1.0)
     assert (bc >= 0).all() and bc[s] == 0
     assert (bc[full["lv"] == INF] == 0).all()
+
+
+def test_full_cc_local_certificate(full):
+    cc, V = full["cc"], full["V"]
+    assert full["cc_edges_ok"]
+    assert (cc <= np.arange(V, dtype=np.uint32)).all()
+    assert np.array_equal(cc[cc], cc)
+    isolated = (full["outdeg"] == 0) & (full["indeg"] == 0)
+    assert np.array_equal(cc[isolated], np.flatnonzero(isolated).astype(np.uint32))
+    assert full["st_cc"].traversed_edges == full["E"]
