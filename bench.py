@@ -355,7 +355,9 @@ def main():
                         f"PageRank x{PR_ITERS} + BC, one source per step",
             "scale": scale, "vertices": V, "edges": E, "partitions_per_gpu": 1,
             "parallelism": "single" if world == 1 else
-            f"1D vertex partition over {world} GPUs (degree-serpentine), IPC peer-copy exchange",
+            f"1D vertex partition over {world} GPUs (degree-serpentine); exchange: BFS/SSSP/PageRank "
+            "kernels write boundary messages into CUDA-IPC-mapped peer arenas (fused), BC/CC "
+            "peer copies",
             "l2": "inputs larger than L2 (graph %.1f GB >> 126 MB L2)" % (info["device_bytes"] / 1e9),
             "build_s": round(build_s, 2)},
         "per_algorithm_gteps": {k: (v[0] / (v[1] * 1e-3) / 1e9 if v[1] else None)

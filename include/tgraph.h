@@ -252,6 +252,21 @@ typedef struct {
 } tg_kernel_stat;
 
 int tg_engine_set_profiling(tg_engine* eng, int on);   /* also resets the ledger */
+
+/* Communication-phase transport of the boundary messages (PAPER.md:207 and
+ * P:256 §4.3.2 "the communication phase"; SURVEY 8(e) fusion candidates).
+ *   TG_EXCHANGE_FUSED (default): BFS, SSSP and PageRank compute kernels write
+ *     each boundary message straight into the owner partition's receive arena
+ *     (same-process pointer, or a CUDA-IPC-mapped peer pointer: NVLink stores
+ *     and reductions between GPUs); the phase is an arrival barrier only.
+ *   TG_EXCHANGE_COPY: messages are staged in the outbox and copied segment by
+ *     segment into the owners' arenas (the paper's outbox -> inbox transfer).
+ * BC and CC always use COPY.  Results are identical in both modes.  Engines
+ * spanning processes: every rank must select the same mode before its next
+ * algorithm call (SPMD).  TG_EINVAL for NULL or an unknown mode.
+ * The environment variable TG_FUSED_EXCHANGE=0 sets the default to COPY. */
+enum { TG_EXCHANGE_COPY = 0, TG_EXCHANGE_FUSED = 1 };
+int tg_engine_set_exchange(tg_engine* eng, int mode);
 int tg_engine_kernel_stat(const tg_engine* eng, int kernel_id, tg_kernel_stat* out);
 const char* tg_kernel_name(int kernel_id);
 

@@ -5,6 +5,8 @@ only -- every step of every algorithm runs in the CUDA kernels of csrc/.  There
 is no CPU fallback: if the library is missing the import fails loudly.
 """
 from .tgraph import (  # noqa: F401
+    TG_EXCHANGE_COPY,
+    TG_EXCHANGE_FUSED,
     TG_INF32,
     TG_MEM_DEVICE,
     TG_MEM_HOST,
@@ -24,6 +26,7 @@ from .tgraph import (  # noqa: F401
     tg_engine_free,
     tg_engine_info,
     tg_engine_partition_info,
+    tg_engine_set_exchange,
     tg_pagerank,
     tg_rmat_edges,
     tg_sssp,

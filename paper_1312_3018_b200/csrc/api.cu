@@ -132,6 +132,24 @@ void exchange(Engine& eng, BufOf send, BufOf recv, size_t elem, bool reverse) {
   }
 }
 
+void fused_arrival(Engine& eng) {
+  // the compute kernels' stores / reductions into peer arenas are complete and
+  // visible once their stream has drained; the barrier orders every rank's
+  // writes before every rank's scatter (one process: stream order suffices)
+  if (!eng.multi()) return;
+  TG_CK(cudaStreamSynchronize(eng.stream));
+  comm_barrier(eng);
+}
+
+void fused_reset(Engine& eng, int byte, size_t elem) {
+  for (auto& pp : eng.parts)
+    if (pp->I) TG_CK(cudaMemsetAsync(pp->arena_fwd.get(), byte, elem ? pp->I * elem : pp->I / 8, eng.stream));
+  if (eng.multi()) {
+    TG_CK(cudaStreamSynchronize(eng.stream));
+    comm_barrier(eng);
+  }
+}
+
 unsigned long long read_counts(Engine& eng, int idx) {
   const int P = (int)eng.parts.size();
   for (int i = 0; i < P; ++i)
@@ -599,6 +617,15 @@ int tg_engine_set_profiling(tg_engine* e, int on) {
     eng.prof_flush();
     eng.prof = on != 0;
     for (auto& k : eng.kstat) k = tg_kernel_stat{};
+  });
+}
+
+int tg_engine_set_exchange(tg_engine* e, int mode) {
+  return guard([&] {
+    TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");
+    TG_REQUIRE(mode == TG_EXCHANGE_COPY || mode == TG_EXCHANGE_FUSED, TG_EINVAL,
+               "tg_engine_set_exchange: unknown mode");
+    reinterpret_cast<Engine*>(e)->fused = mode == TG_EXCHANGE_FUSED;
   });
 }
 

@@ -9,7 +9,10 @@
 //             vertex, ever).
 //   communicate: outbox bitmaps -> peers' inbox bitmaps (1 bit per slot: the
 //             "compression" P:292 allows; same result as the paper's full
-//             level buffer under min-combine).
+//             level buffer under min-combine).  Fused (default, Engine::fused):
+//             the first-time mark is an atomicOr straight into the owner's
+//             inbox bitmap (RemoteOut; peer memory across processes), so the
+//             phase is only the arrival barrier.
 //   scatter : inbox bit set and owner vertex unvisited -> next bit
 //             (totem_engine_scatter_inbox_min).
 //   advance : next bitmap -> level[v] = L+1, visited |= next, vote count
@@ -30,6 +33,8 @@ struct BfsOp {
   uint32_t* next;
   uint32_t* omark;
   uint32_t* onew;
+  RemoteOut rout;  // fused: first-time remote marks go straight to the owner's inbox bits
+  bool fused;
   __device__ __forceinline__ Aux aux(uint32_t) const { return {}; }
   __device__ __forceinline__ void edge(const Aux&, uint64_t e) const {
     const uint32_t t = __ldcs(col + e);
@@ -37,7 +42,7 @@ struct BfsOp {
       const uint32_t s = t & ~kRemote, m = 1u << (s & 31);
       if (!(omark[s >> 5] & m)) {
         const uint32_t old = atomicOr(&omark[s >> 5], m);
-        if (!(old & m)) atomicOr(&onew[s >> 5], m);
+        if (!(old & m)) atomicOr(fused ? rout.word(s) : &onew[s >> 5], m);
       }
     } else {
       const uint32_t m = 1u << (t & 31);
@@ -124,6 +129,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
       TG_CK(cudaMemsetAsync(f.obox_mark.get(), 0, p.S / 8, s));
       TG_CK(cudaMemsetAsync(f.obox_new.get(), 0, p.S / 8, s));
     }
+    if (eng.fused && p.I) TG_CK(cudaMemsetAsync(p.arena_fwd.get(), 0, p.I / 8, s));
     if (p.id == ps) {
       k_seed<<<1, 1, 0, s>>>(f.next.get(), ls, nullptr, 0);
       eng.launches++;
@@ -132,6 +138,10 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
                    f.counters.get(), f.counters.get() + 2);
     std::swap(f.cur, f.next);
   }
+  // fused: every inbox bitmap is clear before any peer writes into it (the vote
+  // below synchronizes the ranks when direction optimization reads it; the
+  // barrier covers the forced top-down mode)
+  if (eng.fused && eng.multi()) fused_arrival(eng);
   const DirectionPolicy dir = direction_policy(eng);
   uint64_t supersteps = 0, frontier = 1, edges_total = 0, bu_steps = 0;
   uint64_t mf = dir.mode == 1 ? 0 : read_vote(eng).degsum;  // out-edges of the frontier
@@ -155,7 +165,8 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
         TG_CK(cudaGetLastError());
         eng.launches++;
       } else {
-        BfsOp op{p.col.get(), f.visited.get(), f.next.get(), f.obox_mark.get(), f.obox_new.get()};
+        BfsOp op{p.col.get(), f.visited.get(), f.next.get(), f.obox_mark.get(), f.obox_new.get(),
+                 p.rout(), eng.fused};
         launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_BFS_EXPAND, f.counters.get() + 1);
       }
     }
@@ -163,10 +174,15 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
     supersteps++;
     if (eng.P > 1) {
       eng.prof_begin(TG_K_EXCHANGE);
-      exchange(eng, send_onew, recv_ibits, 0, false);
+      if (eng.fused) {
+        fused_arrival(eng);
+        for (auto& pp : eng.parts) eng.comm_bytes += pp->S / 8;  // bitmap capacity written into
+      } else {
+        exchange(eng, send_onew, recv_ibits, 0, false);
+      }
       for (auto& pp : eng.parts) {
         Part& p = *pp;
-        if (p.S) TG_CK(cudaMemsetAsync(p.fs.obox_new.get(), 0, p.S / 8, s));
+        if (p.S && !eng.fused) TG_CK(cudaMemsetAsync(p.fs.obox_new.get(), 0, p.S / 8, s));
         if (p.I) {
           k_bfs_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(
               reinterpret_cast<const uint32_t*>(p.arena_fwd.get()), p.ibox_lid.get(),
@@ -174,6 +190,9 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
                                                            p.fs.next.get());
           TG_CK(cudaGetLastError());
           eng.launches++;
+          // fused: the inbox bits are consumed; clear them for the next superstep
+          // (peers write again only after the vote below has synchronized)
+          if (eng.fused) TG_CK(cudaMemsetAsync(p.arena_fwd.get(), 0, p.I / 8, s));
         }
       }
       eng.prof_end(TG_K_EXCHANGE);

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 
 #include "engine.cuh"
 #include "tg_inputs.h"
@@ -691,6 +692,27 @@ void setup_peers(Engine& eng) {
       const uint64_t b = eng.peers[q].ibox_off[pt->id + 1] - eng.peers[q].ibox_off[pt->id];
       TG_REQUIRE(a == b, TG_EINTERNAL, "outbox/inbox symmetry violated");
     }
+  // fused-exchange tables: slot s of p's segment for q -> q's arena index of it
+  for (auto& pt : eng.parts) {
+    Part& p = *pt;
+    std::vector<uint8_t> owner(std::max<uint64_t>(p.S / 32, 1), 0);
+    std::vector<uint8_t*> arena(eng.P, nullptr);
+    std::vector<int64_t> delta(eng.P, 0);
+    for (int q = 0; q < eng.P; ++q) {
+      for (uint64_t w = p.obox_off[q] / 32; w < p.obox_off[q + 1] / 32; ++w) owner[w] = (uint8_t)q;
+      if (q == p.id) continue;
+      arena[q] = eng.peers[q].arena_fwd;
+      delta[q] = (int64_t)eng.peers[q].ibox_off[p.id] - (int64_t)p.obox_off[q];
+      TG_REQUIRE(delta[q] % 32 == 0, TG_EINTERNAL, "unaligned inbox segment");
+    }
+    p.rmt_owner.alloc(owner.size());
+    p.rmt_arena.alloc(eng.P);
+    p.rmt_delta.alloc(eng.P);
+    TG_CK(cudaMemcpy(p.rmt_owner.get(), owner.data(), owner.size(), cudaMemcpyHostToDevice));
+    TG_CK(cudaMemcpy(p.rmt_arena.get(), arena.data(), eng.P * sizeof(uint8_t*), cudaMemcpyHostToDevice));
+    TG_CK(cudaMemcpy(p.rmt_delta.get(), delta.data(), eng.P * sizeof(int64_t), cudaMemcpyHostToDevice));
+  }
+  if (const char* f = std::getenv("TG_FUSED_EXCHANGE")) eng.fused = f[0] != '0';
 }
 
 void map_remote_peers(Engine& eng) {
@@ -778,7 +800,7 @@ void build_engine(Engine& eng, const EdgeInput& in) {
     if (pt->seg_real.empty()) pt->seg_real.assign(eng.P, 0);
     build_inbox(eng, *pt, g);
     // receive arenas + collection staging (8 bytes per slot / vertex)
-    pt->arena_fwd.alloc(std::max<uint64_t>(pt->I, 1) * 8);
+    pt->arena_fwd.alloc(std::max<uint64_t>(pt->I, 1) * 16);  // 2 x 8 B: double-buffered PR sums
     pt->arena_rev.alloc(std::max<uint64_t>(pt->S, 1) * 8);
     pt->staging.alloc(std::max<uint64_t>(pt->Vp, 1) * 8);
   }

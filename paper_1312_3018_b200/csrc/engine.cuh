@@ -58,6 +58,28 @@ struct TileSched {
   void ensure(uint64_t ntiles);
 };
 
+// Fused exchange (the fusion candidates of SURVEY 8(e)): the
+// compute kernel writes a boundary message straight into the owner's receive
+// arena -- a local pointer for partitions of one process, a CUDA-IPC-mapped
+// peer pointer (NVLink / NVSwitch stores and reductions) across processes --
+// instead of staging it in an outbox that the communication phase then copies.
+// p's outbox slot s (segment of owner q) lands at q's inbox index of p, which
+// is s + delta[q]; both offsets are multiples of 32, so bitmap words map whole.
+struct RemoteOut {
+  const uint8_t* owner = nullptr;   // [S/32] owner partition of each 32-slot word
+  uint8_t* const* arena = nullptr;  // [P] owners' arena_fwd
+  const int64_t* delta = nullptr;   // [P] inbox index at q minus outbox index at p
+  template <class T>
+  __device__ __forceinline__ T* slot(uint32_t s) const {
+    const int q = owner[s >> 5];
+    return reinterpret_cast<T*>(arena[q]) + ((int64_t)s + delta[q]);
+  }
+  __device__ __forceinline__ uint32_t* word(uint32_t s) const {
+    const int q = owner[s >> 5];
+    return reinterpret_cast<uint32_t*>(arena[q]) + (((int64_t)s + delta[q]) >> 5);
+  }
+};
+
 struct PRState {  // PageRank (local-id order)
   DevBuf<float> contrib[2];
   DevBuf<float> rank;
@@ -115,6 +137,11 @@ struct Part {
   // outbox offsets (pull).  8 bytes per slot covers every message type.
   DevBuf<uint8_t> arena_fwd, arena_rev;
   DevBuf<uint8_t> staging;  // result collection (multi-process): Vp x 8 bytes
+  // fused-exchange tables (RemoteOut), built once the peers are known
+  DevBuf<uint8_t> rmt_owner;
+  DevBuf<uint8_t*> rmt_arena;
+  DevBuf<int64_t> rmt_delta;
+  RemoteOut rout() const { return {rmt_owner.get(), rmt_arena.get(), rmt_delta.get()}; }
   // algorithm state (lazily allocated)
   TileSched ts;     // tiles of the out-CSR
   TileSched ts_in;  // tiles of the in-CSR (BC backward push)
@@ -141,6 +168,10 @@ struct Engine {
   int rank = 0, world = 1;
   tg_comm comm{};
   bool multi() const { return world > 1; }
+  // boundary messages written by the compute kernels into the owners' arenas
+  // (RemoteOut) for BFS, SSSP and PageRank; TG_FUSED_EXCHANGE=0 selects the
+  // outbox + copy communication phase instead
+  bool fused = true;
   std::vector<PeerView> peers;  // indexed by partition id (all P)
   uint64_t V = 0, E = 0;
   bool weighted = false, has_in = false;
@@ -205,6 +236,14 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st);
 // per slot, or 0 for a bitmap (one bit per slot, segments are 32-aligned).
 using BufOf = void* (*)(Part&);
 void exchange(Engine& eng, BufOf send, BufOf recv, size_t elem, bool reverse);
+// Communication phase of a fused exchange: the messages were written by the
+// compute kernels; make them visible to their owners before anyone scatters
+// (stream sync + barrier across processes; nothing to do in one process).
+void fused_arrival(Engine& eng);
+// Reset every hosted partition's forward arena to a byte value (before the
+// first superstep of an algorithm that accumulates into it); across processes
+// a barrier follows, so no peer writes into an arena being reset.
+void fused_reset(Engine& eng, int byte, size_t elem);
 // sum of out-degrees over reached vertices (vals != INF, or visited bits);
 // *nreached (nullable) receives the number of reached vertices
 uint64_t reached_outdeg_u32(Engine& eng, uint64_t* nreached = nullptr);

@@ -11,7 +11,11 @@
 //             per row (32..2047, from build-time row lists), a thread per row.
 //   P == 1  : fused finalize: rank = (1-d)/V + d*sum, next contrib = rank/outdeg.
 //   P > 1   : outbox partial sums -> owners' inboxes (full buffer),
-//             scatter-add into acc, then finalize.
+//             scatter-add into acc, then finalize.  Fused (default): the pull
+//             kernel stores each outbox row's sum straight into the owner's
+//             inbox slot (RemoteOut; NVLink peer stores across processes),
+//             double-buffered by round parity, so the communication phase is
+//             one arrival barrier per round and no copy.
 // No vote: a fixed number of rounds.
 #include <cstdlib>
 
@@ -73,6 +77,9 @@ struct PullOut {
   float* contrib_next;     // fused
   const uint32_t* outdeg;  // fused
   uint32_t hot;            // sources [0, hot) are gathered evict_last
+  RemoteOut rout;          // remote: outbox sums go straight into the owner's inbox ...
+  bool remote;
+  int parity;              // ... double-buffered by round parity (arena slot = 2 x f64)
   __device__ __forceinline__ void put(uint64_t r, double sum) const {
     if (r < Vp) {
       if (fused) {
@@ -86,6 +93,8 @@ struct PullOut {
       } else {
         acc[r] = sum;
       }
+    } else if (remote) {
+      reinterpret_cast<double*>(rout.slot<double2>((uint32_t)(r - Vp)))[parity] = sum;
     } else {
       obox[r - Vp] = sum;
     }
@@ -147,11 +156,13 @@ __global__ void k_pr_init(const uint32_t* outdeg, uint64_t Vp, double r0, float*
   }
 }
 
-__global__ void k_pr_scatter(const double* msg, const uint32_t* lid, uint64_t I, double* acc) {
+// msg[j * stride] is inbox entry j (stride 2 for the fused double buffer)
+__global__ void k_pr_scatter(const double* msg, uint32_t mstride, const uint32_t* lid, uint64_t I,
+                             double* acc) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < I; j += stride) {
     const uint32_t r = lid[j];
-    if (r != kInf) atomicAdd(&acc[r], msg[j]);
+    if (r != kInf) atomicAdd(&acc[r], msg[j * mstride]);
   }
 }
 
@@ -235,7 +246,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       Part& p = *pp;
       PRState& r = p.pr;
       PullOut o{eng.P == 1, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
-                r.contrib[cur ^ 1].get(), p.outdeg.get(), hot};
+                r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, p.rout(), eng.fused, it & 1};
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
       launch_pull(eng, p, r.contrib[cur].get(), o);
     }
@@ -245,13 +256,24 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
     eng.prof_bytes(TG_K_PR_PULL, 8.0 * eng.E + 20.0 * eng.V);
     if (eng.P > 1) {
       eng.prof_begin(TG_K_EXCHANGE);
-      exchange(eng, send_obox, recv_ibox, 8, false);
+      // fused: the pull wrote this round's sums into the owners' arenas (buffer
+      // it & 1); one barrier per round orders them before the scatters, and the
+      // next round writes the other buffer, whose readers finished before that
+      // barrier (their scatter precedes their pull in stream order)
+      if (eng.fused) {
+        fused_arrival(eng);
+        for (auto& pp : eng.parts) eng.comm_bytes += pp->S * 8;
+      } else {
+        exchange(eng, send_obox, recv_ibox, 8, false);
+      }
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         PRState& r = p.pr;
         if (p.I) {
-          k_pr_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(
-              reinterpret_cast<const double*>(p.arena_fwd.get()), p.ibox_lid.get(), p.I, r.acc.get());
+          const double* msg = reinterpret_cast<const double*>(p.arena_fwd.get());
+          k_pr_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(eng.fused ? msg + (it & 1) : msg,
+                                                          eng.fused ? 2u : 1u, p.ibox_lid.get(),
+                                                          p.I, r.acc.get());
           eng.launches++;
         }
         if (p.Vp) {

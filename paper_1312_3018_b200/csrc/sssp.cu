@@ -6,7 +6,11 @@
 //             min-combiner of P:182).  nd is formed in 64 bits; a value that
 //             does not fit u32 raises the overflow flag (TG_EINTERNAL).
 //   communicate: the full outbox value array (full buffer every
-//             superstep; min-combine makes re-sending idempotent).
+//             superstep; min-combine makes re-sending idempotent).  Fused
+//             (default): the local outbox minimum filters, and each improvement
+//             is also a RED.MIN straight into the owner's inbox slot
+//             (RemoteOut), which then holds the running minimum; the phase is
+//             only the arrival barrier.
 //   scatter : dist[v] = min(dist[v], msg), activate on improvement.
 //   advance : next-active bitmap -> vote count + the smallest active distance.
 //
@@ -37,6 +41,8 @@ struct SsspOp {
   uint32_t* next;
   uint32_t* obox;
   unsigned long long* overflow;
+  RemoteOut rout;    // fused: improvements of the local outbox minimum are forwarded
+  bool fused;        // as RED.MIN straight into the owner's inbox slot
   uint32_t thresh;   // relax rows with dist < thresh now, defer the others ...
   uint32_t hub_end;  // ... but only rows v < hub_end (the high-degree prefix)
   __device__ __forceinline__ Aux aux(uint32_t v) const { return dist[v]; }
@@ -54,7 +60,10 @@ struct SsspOp {
     const uint32_t nd = (uint32_t)nd64;
     if (t & kRemote) {
       const uint32_t s = t & ~kRemote;
-      if (nd < obox[s]) atomicMin(&obox[s], nd);
+      if (nd < obox[s]) {
+        atomicMin(&obox[s], nd);
+        if (fused) atomicMin(rout.slot<uint32_t>(s), nd);
+      }
     } else if (nd < dist[t]) {
       // nd < dist[t] as read means t's distance drops in this superstep (to nd
       // or below: values only decrease and stale reads are only ever higher),
@@ -151,6 +160,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     TG_CK(cudaMemsetAsync(f.cur.get(), 0, nw * 4, s));
     TG_CK(cudaMemsetAsync(f.next.get(), 0, nw * 4, s));
     if (p.S) TG_CK(cudaMemsetAsync(f.obox_u32.get(), 0xFF, p.S * 4, s));
+    if (eng.fused && p.I) TG_CK(cudaMemsetAsync(p.arena_fwd.get(), 0xFF, p.I * 4, s));
     if (p.id == ps) {
       k_seed<<<1, 1, 0, s>>>(f.next.get(), ls, f.vals.get(), 0);
       eng.launches++;
@@ -158,6 +168,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get());
     std::swap(f.cur, f.next);
   }
+  if (eng.fused && eng.multi()) fused_arrival(eng);  // inboxes at INF before any peer writes
   uint64_t supersteps = 0, frontier = 1, relax = 0, activations = 1;
   uint64_t mind = 0;  // smallest tentative distance among the active vertices
   for (;;) {
@@ -170,13 +181,18 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
       SsspOp op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
-                f.counters.get() + 4, thresh, hub_deg ? hubs[i] : kInf};
+                f.counters.get() + 4, p.rout(), eng.fused, thresh, hub_deg ? hubs[i] : kInf};
       launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
     }
     supersteps++;
     if (eng.P > 1) {
       eng.prof_begin(TG_K_EXCHANGE);
-      exchange(eng, send_obox, recv_ibox, 4, false);
+      if (eng.fused) {
+        fused_arrival(eng);
+        for (auto& pp : eng.parts) eng.comm_bytes += pp->S * 4;
+      } else {
+        exchange(eng, send_obox, recv_ibox, 4, false);
+      }
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         if (!p.I) continue;

@@ -159,6 +159,7 @@ def lib():
         L.tg_partition_size.argtypes = [u64, i32, i32, C.POINTER(C.c_uint64)]
         L.tg_partition_size.restype = i32
         L.tg_engine_set_profiling.argtypes = [p, i32]
+        L.tg_engine_set_exchange.argtypes = [p, i32]
         L.tg_engine_kernel_stat.argtypes = [p, i32, C.POINTER(tg_kernel_stat)]
         L.tg_kernel_name.argtypes = [i32]
         L.tg_kernel_name.restype = C.c_char_p
@@ -172,7 +173,7 @@ def lib():
         L.tg_rmat_edges.argtypes = [i32, i32, dbl, dbl, dbl, u64, i32, u64, u64, u64, p, p, p, i32]
         for f in ("tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
                   "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc",
-                  "tg_cc", "tg_engine_set_profiling", "tg_engine_kernel_stat", "tg_graph_from_edges",
+                  "tg_cc", "tg_engine_set_profiling", "tg_engine_set_exchange", "tg_engine_kernel_stat", "tg_graph_from_edges",
                   "tg_graph_load_edge_list", "tg_graph_info", "tg_graph_edges", "tg_engine_create",
                   "tg_rmat_edges"):
             getattr(L, f).restype = i32
@@ -388,6 +389,13 @@ def tg_engine_set_profiling(h, on: bool) -> None:
     _check(lib().tg_engine_set_profiling(h, int(on)))
 
 
+TG_EXCHANGE_COPY, TG_EXCHANGE_FUSED = 0, 1
+
+
+def tg_engine_set_exchange(h, mode: int) -> None:
+    _check(lib().tg_engine_set_exchange(h, int(mode)))
+
+
 def tg_engine_kernel_stats(h) -> dict:
     """{kernel name: {launches, ms, algorithmic_bytes}} from the engine's ledger."""
     out = {}
@@ -456,3 +464,7 @@ class Engine:
 
     def kernel_stats(self):
         return tg_engine_kernel_stats(self.h)
+
+    def set_exchange(self, mode):
+        """TG_EXCHANGE_FUSED (default) or TG_EXCHANGE_COPY (tg_engine_set_exchange)."""
+        tg_engine_set_exchange(self.h, mode)

@@ -65,9 +65,11 @@ def comm_worker(rank, world, port):
     dist.destroy_process_group()
 
 
-def engine_worker(rank, world, port, scale, device):
+def engine_worker(rank, world, port, scale, device, exchange=1):
     """One partition per process on `device`; boundary messages through
-    CUDA-IPC-mapped peer arenas; rank 0 checks against the oracle."""
+    CUDA-IPC-mapped peer arenas (exchange 1: written by the compute kernels
+    into the peers' arenas; 0: outbox + peer copies); rank 0 checks against
+    the oracle."""
     import inputs
     import paper_1312_3018_b200 as tg
 
@@ -80,6 +82,7 @@ def engine_worker(rank, world, port, scale, device):
     srcs = [int(x) for x in inputs.list_sources(src, 4)]
     results = []
     for eng in (eng_e, eng_g):
+        eng.set_exchange(exchange)
         pi = eng.partition_info(rank)
         assert pi["Vp"] == tg.tg_partition_size(V, rank, world)
         out = {"bfs": [eng.bfs(s)[0].copy() for s in srcs],

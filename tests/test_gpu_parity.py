@@ -141,6 +141,35 @@ def test_partition_invariance_rmat12(tg, P):
     check_all(tg, G, eng, bfs_src=srcs, sssp_src=srcs[:3], pr_T=(5,), bc_src=srcs[:4])
 
 
+@pytest.mark.parametrize("P", [2, 3, 8])
+@pytest.mark.parametrize("mode", ["copy", "fused"])
+def test_exchange_modes_rmat13(tg, P, mode):
+    """Both communication-phase transports (tg_engine_set_exchange): outbox +
+    segment copies, and boundary messages written by the compute kernels
+    straight into the owners' arenas.  Same oracle results either way."""
+    scale = 13
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    eng = tg.Engine.from_edges(V, src, dst, w, partitions=P)
+    eng.set_exchange(tg.TG_EXCHANGE_FUSED if mode == "fused" else tg.TG_EXCHANGE_COPY)
+    srcs = inputs.list_sources(src, 5)
+    # twice in a row: arenas left by one run (and by another algorithm) must not leak
+    check_all(tg, G, eng, bfs_src=srcs, sssp_src=srcs[:3], pr_T=(5, 6), bc_src=srcs[:2])
+    check_all(tg, G, eng, bfs_src=srcs[:2], sssp_src=srcs[:2], pr_T=(1,))
+    _, st = eng.bfs(int(srcs[0]))
+    assert st.comm_bytes > 0
+
+
+def test_set_exchange_rejects_unknown_mode(tg):
+    from paper_1312_3018_b200 import tgraph
+
+    eng = tg.Engine.rmat(8, partitions=2)
+    with pytest.raises(tgraph.TGraphError) as e:
+        eng.set_exchange(7)
+    assert e.value.code == tgraph.TG_EINVAL
+
+
 @pytest.mark.parametrize("mode", ["top", "bottom", "auto"])
 def test_direction_modes_same_result(tg, mode, monkeypatch):
     """Direction-optimizing BFS / pull-sigma BC: top-down,

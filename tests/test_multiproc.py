@@ -4,8 +4,9 @@ CPU (gloo, world 2 and 3): the host collectives the library calls through
 tg_comm (allgather of metadata, vote sums / minima, the all-ones sentinel) and
 the per-rank partition plan against the oracle.
 GPU: 2 and 3 processes on one B200 (cuda:0), one partition each, boundary
-messages copied into CUDA-IPC-mapped peer arenas -- the same code path that
-crosses NVLink between GPUs -- checked against the oracle on rank 0."""
+messages copied into CUDA-IPC-mapped peer arenas, or (fused exchange) written
+there by the compute kernels -- the same code paths that cross NVLink between
+GPUs -- checked against the oracle on rank 0."""
 import socket
 
 import pytest
@@ -29,5 +30,7 @@ def test_host_collectives_and_plan_gloo(world):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3])
-def test_ipc_partitions_on_one_gpu(world):
-    mp.spawn(mp_workers.engine_worker, args=(world, _port(), 12, 0), nprocs=world, join=True)
+@pytest.mark.parametrize("exchange", [0, 1])
+def test_ipc_partitions_on_one_gpu(world, exchange):
+    mp.spawn(mp_workers.engine_worker, args=(world, _port(), 12, 0, exchange), nprocs=world,
+             join=True)
