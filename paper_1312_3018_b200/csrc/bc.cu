@@ -35,19 +35,37 @@ struct BcFwdOp {
   uint32_t* onew;
   double* osigma;
   __device__ __forceinline__ Aux aux(uint32_t v) const { return sigma[v]; }
-  __device__ __forceinline__ void edge(const Aux& sv, uint64_t e) const {
-    const uint32_t t = __ldcs(col + e);
+  // split walker (frontier.cuh): column, then the target's state words, then
+  // the sigma reductions
+  static constexpr bool kSplit = true;
+  static constexpr int kUnroll = 2;
+  struct Pre {
+    uint32_t t;
+  };
+  struct St {
+    uint32_t a, b;  // local: visited / next word; remote: sent-before / sent-now word
+  };
+  __device__ __forceinline__ Pre pre(uint64_t e) const { return {__ldcs(col + e)}; }
+  __device__ __forceinline__ St st(const Pre& p) const {
+    if (p.t & kRemote) {
+      const uint32_t s = p.t & ~kRemote;
+      return {omark[s >> 5], onew[s >> 5]};
+    }
+    return {__ldg(visited + (p.t >> 5)), next[p.t >> 5]};
+  }
+  __device__ __forceinline__ void fin(const Aux& sv, const Pre& p, const St& q) const {
+    const uint32_t t = p.t;
     if (t & kRemote) {
       const uint32_t s = t & ~kRemote, m = 1u << (s & 31);
-      if (!(omark[s >> 5] & m)) {
+      if (!(q.a & m)) {
         atomicAdd(&osigma[s], sv);
-        if (!(onew[s >> 5] & m)) atomicOr(&onew[s >> 5], m);
+        if (!(q.b & m)) atomicOr(&onew[s >> 5], m);
       }
     } else {
       const uint32_t m = 1u << (t & 31);
-      if (!(__ldg(visited + (t >> 5)) & m)) {
+      if (!(q.a & m)) {
         atomicAdd(&sigma[t], sv);
-        if (!(next[t >> 5] & m)) atomicOr(&next[t >> 5], m);
+        if (!(q.b & m)) atomicOr(&next[t >> 5], m);
       }
     }
   }
@@ -117,9 +135,18 @@ struct BcBwdPushOp {
   const double* c;
   double* dsum;
   __device__ __forceinline__ Aux aux(uint32_t w) const { return c[w]; }
-  __device__ __forceinline__ void edge(const Aux& cw, uint64_t e) const {
-    const uint32_t v = __ldcs(in_col + e);
-    if (bit_test(FL, v)) atomicAdd(&dsum[v], cw);
+  static constexpr bool kSplit = true;
+  static constexpr int kUnroll = 2;  // in_col, then the F[L] word, then the add
+  struct Pre {
+    uint32_t v;
+  };
+  struct St {
+    uint32_t word;
+  };
+  __device__ __forceinline__ Pre pre(uint64_t e) const { return {__ldcs(in_col + e)}; }
+  __device__ __forceinline__ St st(const Pre& p) const { return {FL[p.v >> 5]}; }
+  __device__ __forceinline__ void fin(const Aux& cw, const Pre& p, const St& q) const {
+    if ((q.word >> (p.v & 31)) & 1u) atomicAdd(&dsum[p.v], cw);
   }
 };
 

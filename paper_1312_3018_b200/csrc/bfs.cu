@@ -36,17 +36,32 @@ struct BfsOp {
   RemoteOut rout;  // fused: first-time remote marks go straight to the owner's inbox bits
   bool fused;
   __device__ __forceinline__ Aux aux(uint32_t) const { return {}; }
-  __device__ __forceinline__ void edge(const Aux&, uint64_t e) const {
-    const uint32_t t = __ldcs(col + e);
+  // split walker (frontier.cuh): column, then the target's state words, then
+  // the test-and-set reductions
+  static constexpr bool kSplit = true;
+  static constexpr int kUnroll = 2;
+  struct Pre {
+    uint32_t t;
+  };
+  struct St {
+    uint32_t a, b;  // local: visited / next word; remote: "ever sent" word
+  };
+  __device__ __forceinline__ Pre pre(uint64_t e) const { return {__ldcs(col + e)}; }
+  __device__ __forceinline__ St st(const Pre& p) const {
+    if (p.t & kRemote) return {omark[(p.t & ~kRemote) >> 5], 0u};
+    return {__ldg(visited + (p.t >> 5)), next[p.t >> 5]};
+  }
+  __device__ __forceinline__ void fin(const Aux&, const Pre& p, const St& q) const {
+    const uint32_t t = p.t;
     if (t & kRemote) {
       const uint32_t s = t & ~kRemote, m = 1u << (s & 31);
-      if (!(omark[s >> 5] & m)) {
+      if (!(q.a & m)) {
         const uint32_t old = atomicOr(&omark[s >> 5], m);
         if (!(old & m)) atomicOr(fused ? rout.word(s) : &onew[s >> 5], m);
       }
     } else {
       const uint32_t m = 1u << (t & 31);
-      if (!(__ldg(visited + (t >> 5)) & m) && !(next[t >> 5] & m)) atomicOr(&next[t >> 5], m);
+      if (!(q.a & m) && !(q.b & m)) atomicOr(&next[t >> 5], m);
     }
   }
 };

@@ -20,6 +20,8 @@
 #pragma once
 
 #include <chrono>
+#include <cstdlib>
+#include <type_traits>
 
 #include "engine.cuh"
 
@@ -55,6 +57,22 @@ struct TileArgs {
 
 constexpr unsigned kExpandThreads = 256;
 
+// Split (pipelined) edge ops: an Op with kSplit = true provides
+//   Pre pre(uint64_t e)            -- the streamed loads of edge e (col, weight)
+//   St  st(const Pre&)             -- the dependent gathers (target state words)
+//   void fin(const Aux&, const Pre&, const St&)  -- compare + reductions
+// and the walker runs U consecutive 32-edge steps per batch: U column loads in
+// flight, then U gathers, then the reductions (memory-level parallelism for the
+// latency-bound walk: ncu shows long-scoreboard stalls dominating).
+template <class Op, class = void>
+struct is_split {
+  static constexpr bool value = false;
+};
+template <class Op>
+struct is_split<Op, std::void_t<decltype(Op::kSplit)>> {
+  static constexpr bool value = Op::kSplit;
+};
+
 // Persistent warps over the active tiles.  Op provides
 //   using Aux; static constexpr bool kReduce, kFilter;
 //   bool keep(uint32_t v, const Aux&) const; void defer(uint32_t v) const;  (kFilter)
@@ -62,7 +80,7 @@ constexpr unsigned kExpandThreads = 256;
 //   void edge(const Aux&, uint64_t e) const;                   (!kReduce)
 //   double edge_val(uint64_t e) const;                         (kReduce)
 //   void vertex_done(uint32_t v, double sum, bool whole_row) const;  (kReduce)
-template <class Op>
+template <class Op, int U>
 __global__ void __launch_bounds__(kExpandThreads) k_warp_expand(TileArgs a, Op op) {
   using Aux = typename Op::Aux;
   const uint32_t lane = threadIdx.x & 31;
@@ -114,6 +132,41 @@ __global__ void __launch_bounds__(kExpandThreads) k_warp_expand(TileArgs a, Op o
       const uint32_t owner_of = __fns(lmask, 0, (int)lane + 1);  // lane of segment #lane
       double acc = 0.0;
       uint32_t s0 = 0;
+      if constexpr (!Op::kReduce && is_split<Op>::value) {
+        for (uint32_t c0 = 0; c0 < T; c0 += 32u * U) {
+          Aux ax[U];
+          uint64_t ee[U];
+          bool ok[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t cc = c0 + 32u * u;
+            const uint32_t flag = (len > 0 && excl > cc && excl < cc + 32) ? (1u << (excl - cc)) : 0u;
+            const uint32_t starts = __reduce_or_sync(kFull, flag);
+            const uint32_t s = s0 + __popc(starts & lowm);
+            const uint32_t idx = cc + lane;
+            ok[u] = idx < T;
+            const uint32_t ow = __shfl_sync(kFull, owner_of, s & 31);
+            ee[u] = __shfl_sync(kFull, basev, ow & 31) + idx;
+            ax[u] = shfl_aux(aux, ow & 31);
+            const uint32_t sl = __shfl_sync(kFull, s, 31);
+            const uint32_t nb = __reduce_or_sync(kFull, (len > 0 && excl == cc + 32) ? 1u : 0u);
+            s0 = sl + nb;
+          }
+          typename Op::Pre pr[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) pr[u] = op.pre(ee[u]);
+          typename Op::St st[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) st[u] = op.st(pr[u]);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) op.fin(ax[u], pr[u], st[u]);
+        }
+        edges += T;
+        continue;
+      }
       for (uint32_t c0 = 0; c0 < T; c0 += 32) {
         const uint32_t flag = (len > 0 && excl > c0 && excl < c0 + 32) ? (1u << (excl - c0)) : 0u;
         const uint32_t starts = __reduce_or_sync(kFull, flag);
@@ -123,8 +176,10 @@ __global__ void __launch_bounds__(kExpandThreads) k_warp_expand(TileArgs a, Op o
         const uint32_t ow = __shfl_sync(kFull, owner_of, s & 31);
         const uint64_t bs = __shfl_sync(kFull, basev, ow & 31);
         if constexpr (!Op::kReduce) {
-          const Aux ax = shfl_aux(aux, ow & 31);
-          if (valid) op.edge(ax, bs + idx);
+          if constexpr (!is_split<Op>::value) {  // split ops never reach this loop
+            const Aux ax = shfl_aux(aux, ow & 31);
+            if (valid) op.edge(ax, bs + idx);
+          }
         } else {
           double val = valid ? op.edge_val(bs + idx) : 0.0;
 #pragma unroll
@@ -241,20 +296,39 @@ void launch_expand(Engine& eng, Part& p, TileSched& ts, const uint32_t* frontier
   launch_expand_on(eng, out_tiles(p), ts, frontier, op, kid, edges);
 }
 
+template <class Op, int U>
+void launch_walker(Engine& eng, const TileArgs& a, const Op& op) {
+  // persistent grid = exactly the resident CTAs (static tile striding assumes residency)
+  static int per_sm = 0;
+  if (!per_sm) {
+    TG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_warp_expand<Op, U>,
+                                                        kExpandThreads, 0));
+    if (per_sm < 1) per_sm = 1;
+  }
+  k_warp_expand<Op, U><<<expand_grid() / 8u * (unsigned)per_sm, kExpandThreads, 0, eng.stream>>>(a, op);
+}
+
 template <class Op>
 void launch_expand_on(Engine& eng, const CsrTiles& c, TileSched& ts, const uint32_t* frontier,
                       const Op& op, int kid, unsigned long long* edges) {
   if (!c.ntiles) return;
   TileArgs a{c.row_off, c.vf, c.vl, ts.list.get(), ts.count.get(), c.E, frontier, edges};
-  // persistent grid = exactly the resident CTAs (static tile striding assumes residency)
-  static int per_sm = 0;
-  if (!per_sm) {
-    TG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_warp_expand<Op>,
-                                                        kExpandThreads, 0));
-    if (per_sm < 1) per_sm = 1;
-  }
   eng.prof_begin(kid);
-  k_warp_expand<Op><<<expand_grid() / 8u * (unsigned)per_sm, kExpandThreads, 0, eng.stream>>>(a, op);
+  if constexpr (is_split<Op>::value) {
+    // 32-edge steps per batch of the split walker: Op::kUnroll (RMAT-28 sweep,
+    // profiles/r01_walker_unroll.txt), TG_UNROLL=1|2|4|8 overrides
+    static int unroll = 0;
+    if (!unroll) {
+      const char* u = std::getenv("TG_UNROLL");
+      unroll = u ? std::atoi(u) : Op::kUnroll;
+    }
+    if (unroll == 1) launch_walker<Op, 1>(eng, a, op);
+    else if (unroll == 4) launch_walker<Op, 4>(eng, a, op);
+    else if (unroll == 8) launch_walker<Op, 8>(eng, a, op);
+    else launch_walker<Op, 2>(eng, a, op);
+  } else {
+    launch_walker<Op, 1>(eng, a, op);
+  }
   eng.prof_end(kid);
   TG_CK(cudaGetLastError());
   eng.launches++;

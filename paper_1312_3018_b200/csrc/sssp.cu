@@ -50,21 +50,33 @@ struct SsspOp {
     return v >= hub_end || dv < thresh;
   }
   __device__ __forceinline__ void defer(uint32_t v) const { bit_set_atomic(next, v); }
-  __device__ __forceinline__ void edge(const Aux& dv, uint64_t e) const {
-    const uint32_t t = __ldcs(col + e);
-    const uint64_t nd64 = (uint64_t)dv + __ldcs(w + e);
+  // split walker (frontier.cuh): column + weight, then the target's current
+  // distance (or outbox minimum), then the relaxation
+  static constexpr bool kSplit = true;
+  static constexpr int kUnroll = 4;
+  struct Pre {
+    uint32_t t, w;
+  };
+  struct St {
+    uint32_t cur;
+  };
+  __device__ __forceinline__ Pre pre(uint64_t e) const { return {__ldcs(col + e), __ldcs(w + e)}; }
+  __device__ __forceinline__ St st(const Pre& p) const {
+    return {(p.t & kRemote) ? obox[p.t & ~kRemote] : dist[p.t]};
+  }
+  __device__ __forceinline__ void fin(const Aux& dv, const Pre& p, const St& q) const {
+    const uint64_t nd64 = (uint64_t)dv + p.w;
     if (nd64 >= (uint64_t)kInf) {
       *overflow = 1ull;
       return;
     }
-    const uint32_t nd = (uint32_t)nd64;
+    const uint32_t nd = (uint32_t)nd64, t = p.t;
+    if (!(nd < q.cur)) return;
     if (t & kRemote) {
       const uint32_t s = t & ~kRemote;
-      if (nd < obox[s]) {
-        atomicMin(&obox[s], nd);
-        if (fused) atomicMin(rout.slot<uint32_t>(s), nd);
-      }
-    } else if (nd < dist[t]) {
+      atomicMin(&obox[s], nd);
+      if (fused) atomicMin(rout.slot<uint32_t>(s), nd);
+    } else {
       // nd < dist[t] as read means t's distance drops in this superstep (to nd
       // or below: values only decrease and stale reads are only ever higher),
       // so t is active next superstep.  Both updates are fire-and-forget

@@ -380,3 +380,28 @@ def test_c2_pagerank_bc(c2):
     assert_pr(eng.pagerank(5)[0], G.pagerank(5))
     bs = inputs.rmat_sources(scale, 2)
     assert_bc(eng.bc(bs)[0], G.bc(bs))
+
+
+# ------------------------------------------------------------ C3: RMAT-26, 1/2/4 partitions
+@pytest.mark.slow
+def test_c3_rmat26_pagerank_bc_partitions(tg):
+    """BASELINE configs[2]: RMAT-26, PageRank (T = 5) and BC from sampled
+    sources over 1, 2 and 4 degree-aware partitions (one B200 hosts all of
+    them here; the multi-process path is the same partition code), full oracle.
+    Fused exchange by default; PageRank at P = 4 also through the copy path."""
+    scale = 26
+    src, dst, _ = inputs.rmat_edges(scale)
+    G = oracle.Graph(1 << scale, src, dst)
+    del src, dst
+    pr_ref = G.pagerank(5)
+    srcs = [int(x) for x in inputs.rmat_sources(scale, 2)]
+    bc_ref = G.bc(srcs)
+    for P in (1, 2, 4):
+        eng = tg.Engine.rmat(scale, partitions=P, weighted=False)
+        assert_pr(eng.pagerank(5)[0], pr_ref)
+        if P == 4:
+            eng.set_exchange(tg.TG_EXCHANGE_COPY)
+            assert_pr(eng.pagerank(5)[0], pr_ref)
+            eng.set_exchange(tg.TG_EXCHANGE_FUSED)
+        assert_bc(eng.bc(srcs)[0], bc_ref)
+        eng.close()
