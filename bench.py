@@ -109,6 +109,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def gather_probe_ceiling():
+    """Best random-gather rate (loads/s) in the committed L2 probe table."""
+    path = os.path.join(ROOT, "profiles", "r01_l2_gather_probe.txt")
+    best = 0.0
+    try:
+        for ln in open(path):
+            f = ln.split()
+            if len(f) == 3 and not ln.startswith("#"):
+                best = max(best, float(f[1]), float(f[2]))
+    except OSError:
+        return None
+    return best * 1e9 or None
+
+
 def measured_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -334,6 +348,17 @@ def main():
                 "algorithmic_bytes_per_launch": ks["algorithmic_bytes"] / max(ks["launches"], 1),
                 "avg_launch_ms": ks["ms"] / max(ks["launches"], 1), "peak_source": peak_src,
                 "share_of_kernel_time": ks["ms"] / tot_ms if tot_ms else None}
+    if dom == "pr_pull":
+        # PageRank's pull is bounded by random 4-byte gather requests, not DRAM
+        # bytes: the probe (scripts/probes/l2_probe.cu) measures the B200's rate
+        # for random 4 B loads that all hit in L2 -- the ceiling for this kernel
+        ceil = gather_probe_ceiling()
+        gps = E / (roofline["avg_launch_ms"] * 1e-3)
+        roofline["gather_bound"] = {
+            "gathers_per_s": gps, "probe_ceiling_per_s": ceil,
+            "frac": gps / ceil if ceil else None,
+            "source": "profiles/r01_l2_gather_probe.txt (random 4 B loads, L2-resident region, "
+                      "evict_last; 40 G/s when they miss to HBM)"}
     kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                    "GBps": (v["algorithmic_bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] else None}
                for k, v in kstats.items() if v["launches"]}

@@ -69,6 +69,7 @@ void ensure_frontier_state(Engine& eng) {
     f.obox_u32.alloc(std::max<uint64_t>(p.S, 1));
     (void)iw;
     f.counters.alloc(8);
+    TG_CK(cudaMemset(f.counters.get(), 0, 8 * sizeof(unsigned long long)));
     p.ts.ensure(p.ntiles);
     if (p.in_ntiles) p.ts_in.ensure(p.in_ntiles);
   }

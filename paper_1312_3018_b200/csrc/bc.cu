@@ -257,6 +257,9 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     eng.locate(sources[si], &ps, &ls);
     if (eng.P == 1) eng.l2_window(eng.parts[0]->bcs.sigma.get(), eng.parts[0]->Vp * 8);
     time_begin(eng);
+    // the init advance below accumulates F[0]'s count and degree sums into the
+    // vote counters: start them from zero (they hold the previous run's values)
+    reset_vote(eng);
     // ---------------- forward cycle ----------------
     for (auto& pp : eng.parts) {
       Part& p = *pp;
