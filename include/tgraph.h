@@ -255,13 +255,13 @@ int tg_engine_set_profiling(tg_engine* eng, int on);   /* also resets the ledger
 
 /* Communication-phase transport of the boundary messages (PAPER.md:207 and
  * P:256 §4.3.2 "the communication phase"; SURVEY 8(e) fusion candidates).
- *   TG_EXCHANGE_FUSED (default): BFS, SSSP and PageRank compute kernels write
- *     each boundary message straight into the owner partition's receive arena
+ *   TG_EXCHANGE_FUSED (default): BFS, SSSP, PageRank, BC and CC kernels write
+ *     each boundary message straight into the receiving partition's arena
  *     (same-process pointer, or a CUDA-IPC-mapped peer pointer: NVLink stores
  *     and reductions between GPUs); the phase is an arrival barrier only.
  *   TG_EXCHANGE_COPY: messages are staged in the outbox and copied segment by
  *     segment into the owners' arenas (the paper's outbox -> inbox transfer).
- * BC and CC always use COPY.  Results are identical in both modes.  Engines
+ * Results are identical in both modes.  Engines
  * spanning processes: every rank must select the same mode before its next
  * algorithm call (SPMD).  TG_EINVAL for NULL or an unknown mode.
  * The environment variable TG_FUSED_EXCHANGE=0 sets the default to COPY. */

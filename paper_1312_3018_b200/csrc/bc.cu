@@ -16,6 +16,10 @@
 //   bc[v] += delta[v]; the source (level 0) is never updated (line 34).
 // The backward sum uses the tile kernel in reduce mode: per-row sums in shared
 // memory, rows that span tiles accumulate with fp64 atomics.
+// Fused exchange (Engine::fused, default): forward sigma partial sums are
+// RED.ADD straight into the owner's inbox slot; backward, owners store c of
+// their boundary vertices straight into the referencing partitions' ghost
+// slots (arena_rev, double-buffered by level parity).
 #include <cstdio>
 
 #include "frontier.cuh"
@@ -34,6 +38,8 @@ struct BcFwdOp {
   const uint32_t* omark;
   uint32_t* onew;
   double* osigma;
+  RemoteOut rout;  // fused: sigma partial sums RED.ADD straight into the owner's inbox slot
+  bool fused;
   __device__ __forceinline__ Aux aux(uint32_t v) const { return sigma[v]; }
   // split walker (frontier.cuh): column, then the target's state words, then
   // the sigma reductions
@@ -58,7 +64,7 @@ struct BcFwdOp {
     if (t & kRemote) {
       const uint32_t s = t & ~kRemote, m = 1u << (s & 31);
       if (!(q.a & m)) {
-        atomicAdd(&osigma[s], sv);
+        atomicAdd(fused ? rout.slot<double>(s) : &osigma[s], sv);
         if (!(q.b & m)) atomicOr(&onew[s >> 5], m);
       }
     } else {
@@ -77,12 +83,13 @@ struct BcBwdOp {
   const uint32_t* col;
   const uint32_t* succ;  // F[L+1]
   const double* c;
-  const double* ghost;
+  const double* ghost;  // owners' c of boundary targets (arena_rev; stride 2 when fused)
+  uint32_t gstride;
   double* dsum;
   __device__ __forceinline__ Aux aux(uint32_t) const { return {}; }
   __device__ __forceinline__ double edge_val(uint64_t e) const {
     const uint32_t t = __ldcs(col + e);
-    if (t & kRemote) return ghost[t & ~kRemote];
+    if (t & kRemote) return ghost[(uint64_t)(t & ~kRemote) * gstride];
     return bit_test(succ, t) ? c[t] : 0.0;
   }
   __device__ __forceinline__ void vertex_done(uint32_t v, double acc, bool whole) const {
@@ -180,12 +187,16 @@ __global__ void k_or_clear(uint32_t* mark, uint32_t* nw, uint64_t words) {
 }
 
 // owner side of the backward pull: c of boundary vertices in F[L+1], else 0
+// fused (pack == nullptr): stored straight into the referencing partition's
+// ghost slot (RemoteOut over the inbox, arena_rev double-buffered by parity)
 __global__ void k_bc_pack(const uint32_t* lid, uint64_t I, const uint32_t* succ, const double* c,
-                          double* pack) {
+                          double* pack, RemoteOut rin, int parity) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < I; j += stride) {
     const uint32_t v = lid[j];
-    pack[j] = (v != kInf && bit_test(succ, v)) ? c[v] : 0.0;
+    const double x = (v != kInf && bit_test(succ, v)) ? c[v] : 0.0;
+    if (pack) pack[j] = x;
+    else reinterpret_cast<double*>(rin.slot<double2>((uint32_t)j))[parity] = x;
   }
 }
 
@@ -276,6 +287,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         TG_CK(cudaMemsetAsync(f.obox_new.get(), 0, p.S / 8, s));
         TG_CK(cudaMemsetAsync(b.obox_sigma.get(), 0, p.S * 8, s));
       }
+      // fused: inbox sigma sums start at 0 (peers write only after the vote below)
+      if (eng.fused && p.I) TG_CK(cudaMemsetAsync(p.arena_fwd.get(), 0, p.I * 8, s));
       if (p.id == ps) {
         k_bc_seed<<<1, 1, 0, s>>>(F0, ls, b.sigma.get());
         eng.launches++;
@@ -312,7 +325,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           eng.launches++;
         } else {
           BcFwdOp op{p.col.get(), f.visited.get(), next, b.sigma.get(), f.obox_mark.get(),
-                     f.obox_new.get(), b.obox_sigma.get()};
+                     f.obox_new.get(), b.obox_sigma.get(), p.rout(), eng.fused};
           launch_expand(eng, p, p.ts, b.level_bm[L].get(), op, TG_K_BCF_EXPAND,
                         f.counters.get() + 1);
         }
@@ -320,7 +333,12 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       supersteps++;
       if (eng.P > 1) {
         eng.prof_begin(TG_K_EXCHANGE);
-        exchange(eng, send_osigma, recv_isigma, 8, false);
+        if (eng.fused) {
+          fused_arrival(eng);
+          for (auto& pp : eng.parts) eng.comm_bytes += pp->S * 8;
+        } else {
+          exchange(eng, send_osigma, recv_isigma, 8, false);
+        }
         for (auto& pp : eng.parts) {
           Part& p = *pp;
           FrontierState& f = p.fs;
@@ -328,7 +346,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           if (p.S) {
             k_or_clear<<<grid_for(p.S / 32, 256), 256, 0, s>>>(f.obox_mark.get(), f.obox_new.get(),
                                                                p.S / 32);
-            TG_CK(cudaMemsetAsync(b.obox_sigma.get(), 0, p.S * 8, s));
+            if (!eng.fused) TG_CK(cudaMemsetAsync(b.obox_sigma.get(), 0, p.S * 8, s));
             eng.launches++;
           }
           if (p.I) {
@@ -337,6 +355,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
                                                             f.visited.get(), b.sigma.get(),
                                                             b.level_bm[L + 1].get());
             eng.launches++;
+            // fused: consumed; zero for the next superstep (peers write after the vote)
+            if (eng.fused) TG_CK(cudaMemsetAsync(p.arena_fwd.get(), 0, p.I * 8, s));
           }
           TG_CK(cudaGetLastError());
         }
@@ -384,13 +404,21 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           for (auto& pp : eng.parts) {
             Part& p = *pp;
             if (!p.I) continue;
-            k_bc_pack<<<grid_for(p.I, 256), 256, 0, s>>>(p.ibox_lid.get(), p.I,
-                                                         p.bcs.level_bm[L + 1].get(), p.bcs.c.get(),
-                                                         p.bcs.ibox_pack.get());
+            k_bc_pack<<<grid_for(p.I, 256), 256, 0, s>>>(
+                p.ibox_lid.get(), p.I, p.bcs.level_bm[L + 1].get(), p.bcs.c.get(),
+                eng.fused ? nullptr : p.bcs.ibox_pack.get(), p.rin(), (int)(L & 1));
             eng.launches++;
           }
           TG_CK(cudaGetLastError());
-          exchange(eng, send_pack, recv_ghost, 8, true);
+          // fused: the owners stored c into the referencing partitions' ghost
+          // slots (buffer L & 1); one arrival barrier, and the next level writes
+          // the other buffer, whose readers finished before this barrier
+          if (eng.fused) {
+            fused_arrival(eng);
+            for (auto& pp : eng.parts) eng.comm_bytes += pp->I * 8;
+          } else {
+            exchange(eng, send_pack, recv_ghost, 8, true);
+          }
         }
         // direction per level: pull over the out-edges of F[L] (cost ~ their
         // count) or push c[w] over the in-edges of F[L+1] (fp64 atomics, ~2x
@@ -409,8 +437,9 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
             if (!p.ntiles) continue;
             launch_mark_tiles(eng, out_tiles(p), p.Vp, p.bcs.level_bm[L].get(), p.ts);
             launch_compact(eng, p.ts);
+            const double* ghost = reinterpret_cast<const double*>(p.arena_rev.get());
             BcBwdOp op{p.col.get(), p.bcs.level_bm[L + 1].get(), p.bcs.c.get(),
-                       reinterpret_cast<const double*>(p.arena_rev.get()),
+                       eng.fused ? ghost + (L & 1) : ghost, eng.fused ? 2u : 1u,
                        p.bcs.dsum.get()};
             launch_expand(eng, p, p.ts, p.bcs.level_bm[L].get(), op, TG_K_BCB_EXPAND,
                           p.fs.counters.get() + 1);

@@ -711,6 +711,22 @@ void setup_peers(Engine& eng) {
     TG_CK(cudaMemcpy(p.rmt_owner.get(), owner.data(), owner.size(), cudaMemcpyHostToDevice));
     TG_CK(cudaMemcpy(p.rmt_arena.get(), arena.data(), eng.P * sizeof(uint8_t*), cudaMemcpyHostToDevice));
     TG_CK(cudaMemcpy(p.rmt_delta.get(), delta.data(), eng.P * sizeof(int64_t), cudaMemcpyHostToDevice));
+    // reverse: inbox entry j of segment p' -> p''s arena_rev at its outbox index
+    std::vector<uint8_t> iowner(std::max<uint64_t>(p.I / 32, 1), 0);
+    std::vector<uint8_t*> iarena(eng.P, nullptr);
+    std::vector<int64_t> idelta(eng.P, 0);
+    for (int q = 0; q < eng.P; ++q) {
+      for (uint64_t w = p.ibox_off[q] / 32; w < p.ibox_off[q + 1] / 32; ++w) iowner[w] = (uint8_t)q;
+      if (q == p.id) continue;
+      iarena[q] = eng.peers[q].arena_rev;
+      idelta[q] = (int64_t)eng.peers[q].obox_off[p.id] - (int64_t)p.ibox_off[q];
+    }
+    p.rin_owner.alloc(iowner.size());
+    p.rin_arena.alloc(eng.P);
+    p.rin_delta.alloc(eng.P);
+    TG_CK(cudaMemcpy(p.rin_owner.get(), iowner.data(), iowner.size(), cudaMemcpyHostToDevice));
+    TG_CK(cudaMemcpy(p.rin_arena.get(), iarena.data(), eng.P * sizeof(uint8_t*), cudaMemcpyHostToDevice));
+    TG_CK(cudaMemcpy(p.rin_delta.get(), idelta.data(), eng.P * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
   if (const char* f = std::getenv("TG_FUSED_EXCHANGE")) eng.fused = f[0] != '0';
 }
@@ -801,7 +817,7 @@ void build_engine(Engine& eng, const EdgeInput& in) {
     build_inbox(eng, *pt, g);
     // receive arenas + collection staging (8 bytes per slot / vertex)
     pt->arena_fwd.alloc(std::max<uint64_t>(pt->I, 1) * 16);  // 2 x 8 B: double-buffered PR sums
-    pt->arena_rev.alloc(std::max<uint64_t>(pt->S, 1) * 8);
+    pt->arena_rev.alloc(std::max<uint64_t>(pt->S, 1) * 16);  // 2 x 8 B: double-buffered BC ghosts
     pt->staging.alloc(std::max<uint64_t>(pt->Vp, 1) * 8);
   }
   TG_CK(cudaStreamSynchronize(s));

@@ -22,6 +22,10 @@
 //               partitions' slots (the pull path of BC), which lower
 //               the local sources of that slot's in-CSR row;
 //   advance   : next-active bitmap -> vote; stop when no label moved.
+// Fused exchange (Engine::fused, default): the push kernel RED.MINs outbox
+// improvements straight into the owners' inbox slots, and the owners' pack
+// kernel stores the published labels straight into the referencing
+// partitions' ghost slots; the communication phase is the arrival barrier.
 // Labels only decrease and every label is the id of a vertex in the same
 // component, so any interleaving reaches the same fixed point: the minimum.
 #include <cstdio>
@@ -39,12 +43,17 @@ struct CcPushOp {  // out-CSR
   uint32_t* label;
   uint32_t* next;
   uint32_t* obox;
+  RemoteOut rout;  // fused: improvements of the local outbox minimum also go
+  bool fused;      // straight to the owner's inbox slot (RED.MIN, running minimum)
   __device__ __forceinline__ Aux aux(uint32_t v) const { return label[v]; }
   __device__ __forceinline__ void edge(const Aux& l, uint64_t e) const {
     const uint32_t t = __ldcs(col + e);
     if (t & kRemote) {
       const uint32_t s = t & ~kRemote;
-      if (l < obox[s]) atomicMin(&obox[s], l);
+      if (l < obox[s]) {
+        atomicMin(&obox[s], l);
+        if (fused) atomicMin(rout.slot<uint32_t>(s), l);
+      }
     } else if (l < label[t]) {
       atomicMin(&label[t], l);
       atomicOr(&next[t >> 5], 1u << (t & 31));
@@ -96,12 +105,16 @@ __global__ void k_cc_scatter(const uint32_t* msg, const uint32_t* lid, uint64_t 
 }
 
 // owner side of the reverse exchange: label of each active boundary vertex
+// (fused, pack == nullptr: stored straight into the referencing partitions'
+// ghost slots through the reverse RemoteOut)
 __global__ void k_cc_pack(const uint32_t* lid, uint64_t I, const uint32_t* active,
-                          const uint32_t* label, uint32_t* pack) {
+                          const uint32_t* label, uint32_t* pack, RemoteOut rin) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < I; j += stride) {
     const uint32_t v = lid[j];
-    pack[j] = (v != kInf && bit_test(active, v)) ? label[v] : kInf;
+    const uint32_t x = (v != kInf && bit_test(active, v)) ? label[v] : kInf;
+    if (pack) pack[j] = x;
+    else *rin.slot<uint32_t>((uint32_t)j) = x;
   }
 }
 
@@ -159,6 +172,7 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
     TG_CK(cudaMemsetAsync(f.cur.get(), 0, nw * 4, s));
     TG_CK(cudaMemsetAsync(f.next.get(), 0, nw * 4, s));
     if (p.S) TG_CK(cudaMemsetAsync(f.obox_u32.get(), 0xFF, p.S * 4, s));
+    if (eng.fused && p.I) TG_CK(cudaMemsetAsync(p.arena_fwd.get(), 0xFF, p.I * 4, s));
     if (p.Vp) {
       k_cc_init<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.global_of.get(), p.Vp, f.vals.get(), f.next.get());
       TG_CK(cudaGetLastError());
@@ -167,6 +181,7 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
     launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get());
     std::swap(f.cur, f.next);
   }
+  if (eng.fused && eng.multi()) fused_arrival(eng);  // inboxes at INF before any peer writes
   uint64_t supersteps = 0, frontier = eng.V, processed = 0, activations = eng.V;
   for (;;) {
     reset_vote(eng);
@@ -174,7 +189,7 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
       Part& p = *pp;
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
-      CcPushOp op{p.col.get(), f.vals.get(), f.next.get(), f.obox_u32.get()};
+      CcPushOp op{p.col.get(), f.vals.get(), f.next.get(), f.obox_u32.get(), p.rout(), eng.fused};
       launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_CC_EXPAND, f.counters.get() + 1);
       if (p.in_ntiles) {
         launch_mark_tiles(eng, in_tiles(p), p.Vp, f.cur.get(), p.ts_in);
@@ -191,12 +206,21 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
         Part& p = *pp;
         if (!p.I) continue;
         k_cc_pack<<<grid_for(p.I, 256), 256, 0, s>>>(p.ibox_lid.get(), p.I, p.fs.cur.get(),
-                                                     p.fs.vals.get(), p.fs.ibox_u32.get());
+                                                     p.fs.vals.get(),
+                                                     eng.fused ? nullptr : p.fs.ibox_u32.get(),
+                                                     p.rin());
         eng.launches++;
       }
       TG_CK(cudaGetLastError());
-      exchange(eng, send_obox, recv_ibox, 4, false);
-      exchange(eng, send_pack, recv_ghost, 4, true);
+      // fused: forward minima and reverse ghost labels are already in the
+      // receivers' arenas; readers finish before the vote, writers start after it
+      if (eng.fused) {
+        fused_arrival(eng);
+        for (auto& pp : eng.parts) eng.comm_bytes += (pp->S + pp->I) * 4;
+      } else {
+        exchange(eng, send_obox, recv_ibox, 4, false);
+        exchange(eng, send_pack, recv_ghost, 4, true);
+      }
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         FrontierState& f = p.fs;

@@ -67,7 +67,7 @@ struct TileSched {
 // is s + delta[q]; both offsets are multiples of 32, so bitmap words map whole.
 struct RemoteOut {
   const uint8_t* owner = nullptr;   // [S/32] owner partition of each 32-slot word
-  uint8_t* const* arena = nullptr;  // [P] owners' arena_fwd
+  uint8_t* const* arena = nullptr;  // [P] owners' arena_fwd (arena_rev for rin())
   const int64_t* delta = nullptr;   // [P] inbox index at q minus outbox index at p
   template <class T>
   __device__ __forceinline__ T* slot(uint32_t s) const {
@@ -142,6 +142,12 @@ struct Part {
   DevBuf<uint8_t*> rmt_arena;
   DevBuf<int64_t> rmt_delta;
   RemoteOut rout() const { return {rmt_owner.get(), rmt_arena.get(), rmt_delta.get()}; }
+  // reverse direction (pull messages, BC backward): this partition's inbox
+  // entry j (segment of peer p) -> p's arena_rev at p's outbox index of it
+  DevBuf<uint8_t> rin_owner;
+  DevBuf<uint8_t*> rin_arena;
+  DevBuf<int64_t> rin_delta;
+  RemoteOut rin() const { return {rin_owner.get(), rin_arena.get(), rin_delta.get()}; }
   // algorithm state (lazily allocated)
   TileSched ts;     // tiles of the out-CSR
   TileSched ts_in;  // tiles of the in-CSR (BC backward push)
@@ -169,8 +175,8 @@ struct Engine {
   tg_comm comm{};
   bool multi() const { return world > 1; }
   // boundary messages written by the compute kernels into the owners' arenas
-  // (RemoteOut) for BFS, SSSP and PageRank; TG_FUSED_EXCHANGE=0 selects the
-  // outbox + copy communication phase instead
+  // (RemoteOut) for BFS, SSSP, PageRank and BC; TG_FUSED_EXCHANGE=0 selects
+  // the outbox + copy communication phase instead
   bool fused = true;
   std::vector<PeerView> peers;  // indexed by partition id (all P)
   uint64_t V = 0, E = 0;

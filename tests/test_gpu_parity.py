@@ -146,7 +146,9 @@ def test_partition_invariance_rmat12(tg, P):
 def test_exchange_modes_rmat13(tg, P, mode):
     """Both communication-phase transports (tg_engine_set_exchange): outbox +
     segment copies, and boundary messages written by the compute kernels
-    straight into the owners' arenas.  Same oracle results either way."""
+    straight into the receivers' arenas.  Same oracle results either way, for
+    all five algorithms, interleaved (each reuses the arenas the previous one
+    wrote)."""
     scale = 13
     src, dst, w = inputs.rmat_edges(scale, weights=True)
     V = 1 << scale
@@ -157,6 +159,10 @@ def test_exchange_modes_rmat13(tg, P, mode):
     # twice in a row: arenas left by one run (and by another algorithm) must not leak
     check_all(tg, G, eng, bfs_src=srcs, sssp_src=srcs[:3], pr_T=(5, 6), bc_src=srcs[:2])
     check_all(tg, G, eng, bfs_src=srcs[:2], sssp_src=srcs[:2], pr_T=(1,))
+    cc_ref = G.cc()
+    for _ in range(2):
+        assert np.array_equal(eng.cc()[0], cc_ref), "CC mismatch"
+    check_all(tg, G, eng, bfs_src=srcs[:1], pr_T=(), bc_src=srcs[2:4])
     _, st = eng.bfs(int(srcs[0]))
     assert st.comm_bytes > 0
 
