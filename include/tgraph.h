@@ -263,7 +263,9 @@ int tg_engine_set_profiling(tg_engine* eng, int on);   /* also resets the ledger
  *     segment into the owners' arenas (the paper's outbox -> inbox transfer).
  * Results are identical in both modes.  Engines
  * spanning processes: every rank must select the same mode before its next
- * algorithm call (SPMD).  TG_EINVAL for NULL or an unknown mode.
+ * algorithm call (SPMD).  TG_EINVAL for NULL, an unknown mode, or FUSED on a
+ * multi-process engine whose GPUs lack native peer atomics (such an engine
+ * starts in COPY mode).
  * The environment variable TG_FUSED_EXCHANGE=0 sets the default to COPY. */
 enum { TG_EXCHANGE_COPY = 0, TG_EXCHANGE_FUSED = 1 };
 int tg_engine_set_exchange(tg_engine* eng, int mode);

@@ -626,7 +626,10 @@ int tg_engine_set_exchange(tg_engine* e, int mode) {
     TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");
     TG_REQUIRE(mode == TG_EXCHANGE_COPY || mode == TG_EXCHANGE_FUSED, TG_EINVAL,
                "tg_engine_set_exchange: unknown mode");
-    reinterpret_cast<Engine*>(e)->fused = mode == TG_EXCHANGE_FUSED;
+    Engine& eng = *reinterpret_cast<Engine*>(e);
+    TG_REQUIRE(mode == TG_EXCHANGE_COPY || eng.peer_atomics, TG_EINVAL,
+               "tg_engine_set_exchange: FUSED needs native peer atomics between the ranks' GPUs");
+    eng.fused = mode == TG_EXCHANGE_FUSED;
   });
 }
 

@@ -664,6 +664,7 @@ void build_inbox(Engine& eng, Part& pt, const EdgeGen& g) {
 // mapped with CUDA IPC (peer access over NVLink between GPUs).
 struct PeerMeta {
   cudaIpcMemHandle_t h_fwd, h_rev, h_stage, h_gof;
+  char pci[32];  // PCI bus id of the rank's GPU (device ordinals are per process)
   uint64_t Vp;
   uint64_t obox_off[TG_MAX_PARTITIONS + 1];
   uint64_t ibox_off[TG_MAX_PARTITIONS + 1];
@@ -728,7 +729,7 @@ void setup_peers(Engine& eng) {
     TG_CK(cudaMemcpy(p.rin_arena.get(), iarena.data(), eng.P * sizeof(uint8_t*), cudaMemcpyHostToDevice));
     TG_CK(cudaMemcpy(p.rin_delta.get(), idelta.data(), eng.P * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
-  if (const char* f = std::getenv("TG_FUSED_EXCHANGE")) eng.fused = f[0] != '0';
+  if (const char* f = std::getenv("TG_FUSED_EXCHANGE")) eng.fused = f[0] != '0' && eng.peer_atomics;
 }
 
 void map_remote_peers(Engine& eng) {
@@ -739,6 +740,7 @@ void map_remote_peers(Engine& eng) {
   TG_CK(cudaIpcGetMemHandle(&mine.h_stage, me.staging.get()));
   TG_CK(cudaIpcGetMemHandle(&mine.h_gof, me.global_of.get()));
   mine.Vp = me.Vp;
+  TG_CK(cudaDeviceGetPCIBusId(mine.pci, sizeof(mine.pci), eng.device));
   for (int q = 0; q <= eng.P; ++q) {
     mine.obox_off[q] = me.obox_off[q];
     mine.ibox_off[q] = me.ibox_off[q];
@@ -765,6 +767,32 @@ void map_remote_peers(Engine& eng) {
     v.obox_off.assign(all[q].obox_off, all[q].obox_off + eng.P + 1);
     v.ibox_off.assign(all[q].ibox_off, all[q].ibox_off + eng.P + 1);
   }
+  // The fused exchange issues reductions (atomicOr / atomicMin / fp64 add) on
+  // peer memory: that needs native peer atomics between every pair of GPUs
+  // (NVLink / NVSwitch).  Otherwise every rank falls back to the copy
+  // transport (agreed with a min-allreduce: SPMD).
+  uint64_t ok = 1;
+  for (int q = 0; q < eng.world; ++q) {
+    if (q == eng.rank) continue;
+    int pd = -1;
+    if (cudaDeviceGetByPCIBusId(&pd, all[q].pci) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      continue;
+    }
+    if (pd == eng.device) continue;  // same GPU (ranks sharing a device)
+    int atom = 0;
+    if (cudaDeviceGetP2PAttribute(&atom, cudaDevP2PAttrNativeAtomicSupported, eng.device, pd) !=
+            cudaSuccess ||
+        !atom) {
+      cudaGetLastError();
+      ok = 0;
+    }
+  }
+  TG_REQUIRE(eng.comm.allreduce_u64(eng.comm.ctx, &ok, 1, 1) == 0, TG_ENCCL,
+             "tg_comm.allreduce_u64 failed");
+  eng.peer_atomics = ok != 0;
+  if (!eng.peer_atomics) eng.fused = false;
 }
 
 }  // namespace

@@ -178,6 +178,7 @@ struct Engine {
   // (RemoteOut) for BFS, SSSP, PageRank and BC; TG_FUSED_EXCHANGE=0 selects
   // the outbox + copy communication phase instead
   bool fused = true;
+  bool peer_atomics = true;  // every peer GPU supports native atomics on its memory
   std::vector<PeerView> peers;  // indexed by partition id (all P)
   uint64_t V = 0, E = 0;
   bool weighted = false, has_in = false;
