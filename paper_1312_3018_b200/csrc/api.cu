@@ -25,6 +25,11 @@ Engine::~Engine() {
     cudaEventDestroy(p.b);
   }
   for (auto e : ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (side[i]) cudaStreamDestroy(side[i]);
+    if (join_ev[i]) cudaEventDestroy(join_ev[i]);
+  }
+  if (fork_ev) cudaEventDestroy(fork_ev);
   if (prof_open) cudaEventDestroy(prof_open);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -233,6 +238,25 @@ static cudaEvent_t pool_get(Engine& eng) {
   cudaEvent_t e;
   TG_CK(cudaEventCreate(&e));
   return e;
+}
+
+void Engine::fork() {
+  if (!fork_ev) {
+    TG_CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      TG_CK(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+      TG_CK(cudaEventCreateWithFlags(&join_ev[i], cudaEventDisableTiming));
+    }
+  }
+  TG_CK(cudaEventRecord(fork_ev, stream));
+  for (int i = 0; i < 2; ++i) TG_CK(cudaStreamWaitEvent(side[i], fork_ev, 0));
+}
+
+void Engine::join() {
+  for (int i = 0; i < 2; ++i) {
+    TG_CK(cudaEventRecord(join_ev[i], side[i]));
+    TG_CK(cudaStreamWaitEvent(stream, join_ev[i], 0));
+  }
 }
 
 void Engine::prof_begin(int kid) {

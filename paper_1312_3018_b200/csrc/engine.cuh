@@ -184,6 +184,12 @@ struct Engine {
   bool weighted = false, has_in = false;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // fork/join side streams (independent kernels of one phase run concurrently,
+  // so one kernel's tail overlaps the next one's work); created on first use
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
+  void fork();   // side streams wait for the main stream's work so far
+  void join();   // the main stream waits for the side streams' work
   DevBuf<uint32_t> rank_of;  // global id -> degree-order position
   DevBuf<uint8_t> scratch;   // device staging of host-bound results (V x 8 max)
   std::vector<std::unique_ptr<Part>> parts;

@@ -177,16 +177,25 @@ __global__ void k_pr_finalize(const double* acc, const uint32_t* outdeg, uint64_
   }
 }
 
-void launch_pull(Engine& eng, Part& p, const float* contrib, const PullOut& o) {
-  cudaStream_t s = eng.stream;
+// The three row classes touch disjoint rows and read only the previous
+// round's contributions, so with `concurrent` they run on fork/join side
+// streams: the long hub rows of k_pull_cta overlap the other classes instead
+// of leaving the GPU to their tail.
+void launch_pull(Engine& eng, Part& p, const float* contrib, const PullOut& o, bool concurrent) {
+  cudaStream_t s = eng.stream, s_cta = s, s_warp = s;
+  if (concurrent) {
+    eng.fork();
+    s_cta = eng.side[0];
+    s_warp = eng.side[1];
+  }
   const uint64_t R = p.Vp + p.S;
   if (p.n_cta) {
-    k_pull_cta<<<(unsigned)p.n_cta, kCtaThreads, 0, s>>>(p.in_off.get(), p.in_col.get(), contrib,
-                                                         p.pr_cta.get(), o);
+    k_pull_cta<<<(unsigned)p.n_cta, kCtaThreads, 0, s_cta>>>(p.in_off.get(), p.in_col.get(),
+                                                             contrib, p.pr_cta.get(), o);
     eng.launches++;
   }
   if (p.n_warp) {
-    k_pull_warp<<<grid_for(p.n_warp * 32, 256, 148u * 16u), 256, 0, s>>>(
+    k_pull_warp<<<grid_for(p.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(
         p.in_off.get(), p.in_col.get(), contrib, p.pr_warp.get(), p.n_warp, o);
     eng.launches++;
   }
@@ -195,6 +204,7 @@ void launch_pull(Engine& eng, Part& p, const float* contrib, const PullOut& o) {
                                                                contrib, 0, R, o);
     eng.launches++;
   }
+  if (concurrent) eng.join();
   TG_CK(cudaGetLastError());
 }
 
@@ -231,6 +241,9 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   // in profiles/r01_pr_hot_sweep.txt: 0 -> 28.2, 16M -> 20.35, all -> 21.0 ms)
   uint32_t hot = 16u << 20;
   if (const char* h = std::getenv("TG_PR_HOT")) hot = (uint32_t)std::strtoul(h, nullptr, 10);
+  // row classes on fork/join streams (TG_PR_CONCURRENT=0: one stream)
+  const bool concurrent =
+      !(std::getenv("TG_PR_CONCURRENT") && std::getenv("TG_PR_CONCURRENT")[0] == '0');
   time_begin(eng);
   for (auto& pp : eng.parts) {
     Part& p = *pp;
@@ -248,7 +261,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       PullOut o{eng.P == 1, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
                 r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, p.rout(), eng.fused, it & 1};
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
-      launch_pull(eng, p, r.contrib[cur].get(), o);
+      launch_pull(eng, p, r.contrib[cur].get(), o, concurrent);
     }
     eng.prof_end(TG_K_PR_PULL);
     // pull: in_col 4 + contrib gather 4 per edge; in_off 8 + outdeg 4 + rank 4 +
