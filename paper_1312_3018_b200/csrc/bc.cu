@@ -20,7 +20,9 @@
 // RED.ADD straight into the owner's inbox slot; backward, owners store c of
 // their boundary vertices straight into the referencing partitions' ghost
 // slots (arena_rev, double-buffered by level parity).
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "frontier.cuh"
 
@@ -152,8 +154,32 @@ struct BcBwdPushOp {
   };
   __device__ __forceinline__ Pre pre(uint64_t e) const { return {__ldcs(in_col + e)}; }
   __device__ __forceinline__ St st(const Pre& p) const { return {FL[p.v >> 5]}; }
+  // Hub targets [0, priv) accumulate in a per-CTA shared-memory copy of dsum,
+  // flushed once per CTA: contended global RED.ADD.F64 on a few hot addresses
+  // runs at 11-31 G/s vs ~185 G/s spread out (profiles/r01_atomic_probe.txt),
+  // and the backward push's targets are mostly hubs (ids are in out-degree order).
+  uint32_t priv;
+  static constexpr bool kBlockHooks = true;
+  size_t smem_bytes() const { return (size_t)priv * sizeof(double); }
+  __device__ __forceinline__ void block_begin() const {
+    extern __shared__ double s_dsum[];
+    for (uint32_t i = threadIdx.x; i < priv; i += blockDim.x) s_dsum[i] = 0.0;
+    __syncthreads();
+  }
+  __device__ __forceinline__ void block_end() const {
+    extern __shared__ double s_dsum[];
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < priv; i += blockDim.x)
+      if (s_dsum[i] != 0.0) atomicAdd(&dsum[i], s_dsum[i]);
+  }
   __device__ __forceinline__ void fin(const Aux& cw, const Pre& p, const St& q) const {
-    if ((q.word >> (p.v & 31)) & 1u) atomicAdd(&dsum[p.v], cw);
+    if (!((q.word >> (p.v & 31)) & 1u)) return;
+    if (p.v < priv) {
+      extern __shared__ double s_dsum[];
+      atomicAdd(&s_dsum[p.v], cw);
+    } else {
+      atomicAdd(&dsum[p.v], cw);
+    }
   }
 };
 
@@ -260,6 +286,9 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
   eng.comm_bytes = 0;
   double total_ms = 0;
   const DirectionPolicy dir = direction_policy(eng);
+  // hub targets privatized per CTA in the backward push (TG_BC_PRIV, 0 = off)
+  uint32_t bc_priv = 512;  // RMAT-28 sweep: profiles/r01_bc_priv_sweep.txt
+  if (const char* e = std::getenv("TG_BC_PRIV")) bc_priv = (uint32_t)std::strtoul(e, nullptr, 10);
   uint64_t supersteps = 0, traversed = 0, bytes = 0, bm_bytes = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   for (int si = 0; si < k; ++si) {
@@ -430,7 +459,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           if (push) {
             launch_mark_tiles(eng, in_tiles(p), p.Vp, p.bcs.level_bm[L + 1].get(), p.ts_in);
             launch_compact(eng, p.ts_in);
-            BcBwdPushOp op{p.in_col.get(), p.bcs.level_bm[L].get(), p.bcs.c.get(), p.bcs.dsum.get()};
+            BcBwdPushOp op{p.in_col.get(), p.bcs.level_bm[L].get(), p.bcs.c.get(), p.bcs.dsum.get(),
+                           (uint32_t)std::min<uint64_t>(bc_priv, p.Vp)};
             launch_expand_on(eng, in_tiles(p), p.ts_in, p.bcs.level_bm[L + 1].get(), op,
                              TG_K_BCB_EXPAND, p.fs.counters.get() + 1);
           } else {

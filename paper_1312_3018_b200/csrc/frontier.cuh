@@ -64,6 +64,24 @@ constexpr unsigned kExpandThreads = 256;
 // and the walker runs U consecutive 32-edge steps per batch: U column loads in
 // flight, then U gathers, then the reductions (memory-level parallelism for the
 // latency-bound walk: ncu shows long-scoreboard stalls dominating).
+// Block hooks: an Op with kBlockHooks = true owns `smem_bytes()` of dynamic
+// shared memory per CTA and gets block_begin() before the first tile and
+// block_end() after the last (e.g. per-CTA privatized accumulators of hub
+// targets, flushed once per CTA).
+template <class Op, class = void>
+struct has_block_hooks {
+  static constexpr bool value = false;
+};
+template <class Op>
+struct has_block_hooks<Op, std::void_t<decltype(Op::kBlockHooks)>> {
+  static constexpr bool value = Op::kBlockHooks;
+};
+template <class Op>
+size_t smem_of(const Op& op) {
+  if constexpr (has_block_hooks<Op>::value) return op.smem_bytes();
+  else return 0;
+}
+
 template <class Op, class = void>
 struct is_split {
   static constexpr bool value = false;
@@ -88,6 +106,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_warp_expand(TileArgs a, Op o
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const unsigned long long ntl = *a.tile_count;
   unsigned long long edges = 0;
+  if constexpr (has_block_hooks<Op>::value) op.block_begin();
   for (uint64_t it = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; it < ntl; it += nwarps) {
     const uint32_t t = a.tile_list[it];
     const uint32_t vf = a.tile_vf[t], vl = a.tile_vl[t];
@@ -208,6 +227,7 @@ __global__ void __launch_bounds__(kExpandThreads) k_warp_expand(TileArgs a, Op o
     }
   }
   if (a.edges && lane == 0 && edges) atomicAdd(a.edges, edges);
+  if constexpr (has_block_hooks<Op>::value) op.block_end();
 }
 
 // tile bitmap -> list (clears the bitmap)
@@ -300,12 +320,19 @@ template <class Op, int U>
 void launch_walker(Engine& eng, const TileArgs& a, const Op& op) {
   // persistent grid = exactly the resident CTAs (static tile striding assumes residency)
   static int per_sm = 0;
-  if (!per_sm) {
+  static size_t per_sm_smem = ~(size_t)0;
+  const size_t smem = smem_of(op);
+  if (!per_sm || smem != per_sm_smem) {
+    if (smem > 48 * 1024)
+      TG_CK(cudaFuncSetAttribute(k_warp_expand<Op, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
     TG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_warp_expand<Op, U>,
-                                                        kExpandThreads, 0));
+                                                        kExpandThreads, smem));
     if (per_sm < 1) per_sm = 1;
+    per_sm_smem = smem;
   }
-  k_warp_expand<Op, U><<<expand_grid() / 8u * (unsigned)per_sm, kExpandThreads, 0, eng.stream>>>(a, op);
+  k_warp_expand<Op, U><<<expand_grid() / 8u * (unsigned)per_sm, kExpandThreads, smem, eng.stream>>>(
+      a, op);
 }
 
 template <class Op>
