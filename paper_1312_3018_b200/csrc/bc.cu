@@ -134,6 +134,91 @@ __global__ void __launch_bounds__(256) k_bc_pull(const uint64_t* in_off, const u
   if (lane == 0 && cnt) atomicAdd(edges, cnt);
 }
 
+// Pull-sigma by in-degree class (the PageRank row classes of the in-CSR): the
+// thread-per-vertex k_bc_pull walks a hub row's in-edges serially in one
+// thread; here rows of in-degree >= 2048 get a CTA, 32..2047 a warp (lanes
+// stride the row: coalesced in_col, independent gathers), < 32 a thread.
+// Visited rows are skipped; a non-zero sum sets sigma[v] and v's F[L+1] bit.
+struct PullSigma {
+  const uint64_t* in_off;
+  const uint32_t* in_col;
+  const uint32_t* F;        // F[L]
+  const uint32_t* visited;
+  double* sigma;
+  uint32_t* next;           // F[L+1]
+  unsigned long long* edges;
+  __device__ __forceinline__ bool skip(uint64_t v) const { return bit_test(visited, (uint32_t)v); }
+  __device__ __forceinline__ double sum(uint64_t i, uint64_t e, uint32_t step) const {
+    double s0 = 0.0, s1 = 0.0;
+    for (; i + step < e; i += 2ull * step) {
+      const uint32_t u0 = __ldg(in_col + i), u1 = __ldg(in_col + i + step);
+      const uint32_t w0 = __ldg(F + (u0 >> 5)), w1 = __ldg(F + (u1 >> 5));
+      if ((w0 >> (u0 & 31)) & 1u) s0 += sigma[u0];
+      if ((w1 >> (u1 & 31)) & 1u) s1 += sigma[u1];
+    }
+    if (i < e) {
+      const uint32_t u = __ldg(in_col + i);
+      if (bit_test(F, u)) s0 += sigma[u];
+    }
+    return s0 + s1;
+  }
+  __device__ __forceinline__ void put(uint64_t v, double x) const {
+    if (x > 0.0) {
+      sigma[v] = x;
+      atomicOr(&next[v >> 5], 1u << (v & 31));
+    }
+  }
+};
+
+__global__ void __launch_bounds__(256) k_bc_pull_cta(PullSigma o, const uint32_t* rows) {
+  __shared__ double s_part[8];
+  const uint64_t v = rows[blockIdx.x];
+  if (o.skip(v)) return;  // uniform over the CTA
+  const uint64_t b = o.in_off[v], e = o.in_off[v + 1];
+  double x = o.sum(b + threadIdx.x, e, 256);
+  for (int k = 16; k; k >>= 1) x += __shfl_xor_sync(0xffffffffu, x, k);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < 8; ++k) t += s_part[k];
+    o.put(v, t);
+    atomicAdd(o.edges, (unsigned long long)(e - b));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bc_pull_warp(PullSigma o, const uint32_t* rows, uint64_t n) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long cnt = 0;
+  for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; k < n; k += nw) {
+    const uint64_t v = rows[k];
+    if (o.skip(v)) continue;  // uniform over the warp
+    const uint64_t b = o.in_off[v], e = o.in_off[v + 1];
+    double x = o.sum(b + lane, e, 32);
+    for (int m = 16; m; m >>= 1) x += __shfl_xor_sync(0xffffffffu, x, m);
+    if (lane == 0) {
+      o.put(v, x);
+      cnt += e - b;
+    }
+  }
+  if (lane == 0 && cnt) atomicAdd(o.edges, cnt);
+}
+
+__global__ void __launch_bounds__(256) k_bc_pull_thread(PullSigma o, uint64_t Vp) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long cnt = 0;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < Vp; v += stride) {
+    if (o.skip(v)) continue;  // visited bitmap first: sparse levels skip the offsets
+    const uint64_t b = o.in_off[v], e = o.in_off[v + 1];
+    if (e - b >= 32) continue;
+    o.put(v, o.sum(b, e, 1));
+    cnt += e - b;
+  }
+  for (int m = 16; m; m >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, m);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(o.edges, cnt);
+}
+
 // Backward push over the in-CSR (direction-optimized backward level): for each
 // w in F[L+1] (Aux = c[w]) and in-edge (v, w) with v in F[L]: dsum[v] += c[w].
 struct BcBwdPushOp {
@@ -287,6 +372,9 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
   double total_ms = 0;
   const DirectionPolicy dir = direction_policy(eng);
   // hub targets privatized per CTA in the backward push (TG_BC_PRIV, 0 = off)
+  // pull-sigma by in-degree class (TG_BC_PULL_CLASSES=0: thread per vertex)
+  const bool pull_classes =
+      !(std::getenv("TG_BC_PULL_CLASSES") && std::getenv("TG_BC_PULL_CLASSES")[0] == '0');
   uint32_t bc_priv = 512;  // RMAT-28 sweep: profiles/r01_bc_priv_sweep.txt
   if (const char* e = std::getenv("TG_BC_PRIV")) bc_priv = (uint32_t)std::strtoul(e, nullptr, 10);
   uint64_t supersteps = 0, traversed = 0, bytes = 0, bm_bytes = 0;
@@ -344,7 +432,27 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         uint32_t* next = level_bitmap(p, L + 1);
         TG_CK(cudaMemsetAsync(next, 0, words_for(p.Vp) * 4, s));
         launch_compact(eng, p.ts);
-        if (pull) {
+        if (pull && pull_classes) {
+          // rows by in-degree class on fork/join streams (disjoint rows)
+          PullSigma o{p.in_off.get(), p.in_col.get(), b.level_bm[L].get(), f.visited.get(),
+                      b.sigma.get(), next, f.counters.get() + 1};
+          eng.prof_begin(TG_K_BCF_EXPAND);
+          eng.fork();
+          if (p.n_cta) {
+            k_bc_pull_cta<<<(unsigned)p.n_cta, 256, 0, eng.side[0]>>>(o, p.pr_cta.get());
+            eng.launches++;
+          }
+          if (p.n_warp) {
+            k_bc_pull_warp<<<grid_for(p.n_warp * 32, 256, 148u * 16u), 256, 0, eng.side[1]>>>(
+                o, p.pr_warp.get(), p.n_warp);
+            eng.launches++;
+          }
+          k_bc_pull_thread<<<grid_for(p.Vp, 256, 148u * 16u), 256, 0, s>>>(o, p.Vp);
+          eng.launches++;
+          eng.join();
+          eng.prof_end(TG_K_BCF_EXPAND);
+          TG_CK(cudaGetLastError());
+        } else if (pull) {
           eng.prof_begin(TG_K_BCF_EXPAND);
           k_bc_pull<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
               p.in_off.get(), p.in_col.get(), b.level_bm[L].get(), f.visited.get(), b.sigma.get(),
