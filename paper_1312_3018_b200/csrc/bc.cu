@@ -219,6 +219,113 @@ __global__ void __launch_bounds__(256) k_bc_pull_thread(PullSigma o, uint64_t Vp
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(o.edges, cnt);
 }
 
+// Backward pull by out-degree class: for v in F[L], dsum[v] = sum over its
+// out-edges (v, t) with t in F[L+1] of c[t] (remote t: the owner's published c
+// in the ghost slot).  Local ids are in out-degree order, so the classes are
+// id ranges: [0, n_big) a CTA per row, [n_big, n_mid) a warp, the rest a
+// thread; rows not in F[L] are skipped.  Replaces the reduce-mode tile walker
+// (segmented fp64 shuffles per 32 edges) on the dense backward levels.
+struct PullDelta {
+  const uint64_t* row_off;
+  const uint32_t* col;
+  const uint32_t* FL;    // F[L]
+  const uint32_t* succ;  // F[L+1]
+  const double* c;
+  const double* ghost;
+  uint32_t gstride;
+  double* dsum;
+  unsigned long long* edges;
+  __device__ __forceinline__ double val(uint32_t t) const {
+    if (t & kRemote) return ghost[(uint64_t)(t & ~kRemote) * gstride];
+    return bit_test(succ, t) ? c[t] : 0.0;
+  }
+  __device__ __forceinline__ double sum(uint64_t i, uint64_t e, uint32_t step) const {
+    double s0 = 0.0, s1 = 0.0;
+    for (; i + step < e; i += 2ull * step) {
+      const uint32_t t0 = __ldcs(col + i), t1 = __ldcs(col + i + step);
+      s0 += val(t0);
+      s1 += val(t1);
+    }
+    if (i < e) s0 += val(__ldcs(col + i));
+    return s0 + s1;
+  }
+};
+
+__global__ void __launch_bounds__(256) k_bc_bwd_cta(PullDelta o, uint64_t n) {
+  __shared__ double s_part[8];
+  for (uint64_t v = blockIdx.x; v < n; v += gridDim.x) {
+    if (!bit_test(o.FL, (uint32_t)v)) continue;  // uniform over the CTA
+    const uint64_t b = o.row_off[v], e = o.row_off[v + 1];
+    double x = o.sum(b + threadIdx.x, e, 256);
+    for (int k = 16; k; k >>= 1) x += __shfl_xor_sync(0xffffffffu, x, k);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int k = 0; k < 8; ++k) t += s_part[k];
+      o.dsum[v] = t;
+      atomicAdd(o.edges, (unsigned long long)(e - b));
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bc_bwd_warp(PullDelta o, uint64_t r0, uint64_t r1) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long cnt = 0;
+  for (uint64_t v = r0 + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5); v < r1; v += nw) {
+    if (!bit_test(o.FL, (uint32_t)v)) continue;  // uniform over the warp
+    const uint64_t b = o.row_off[v], e = o.row_off[v + 1];
+    double x = o.sum(b + lane, e, 32);
+    for (int m = 16; m; m >>= 1) x += __shfl_xor_sync(0xffffffffu, x, m);
+    if (lane == 0) {
+      o.dsum[v] = x;
+      cnt += e - b;
+    }
+  }
+  if (lane == 0 && cnt) atomicAdd(o.edges, cnt);
+}
+
+__global__ void __launch_bounds__(256) k_bc_bwd_thread(PullDelta o, uint64_t r0, uint64_t r1) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long cnt = 0;
+  for (uint64_t v = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < r1; v += stride) {
+    if (!bit_test(o.FL, (uint32_t)v)) continue;
+    const uint64_t b = o.row_off[v], e = o.row_off[v + 1];
+    o.dsum[v] = o.sum(b, e, 1);
+    cnt += e - b;
+  }
+  for (int m = 16; m; m >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, m);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(o.edges, cnt);
+}
+
+// first local id with out-degree < deg (ids sorted by out-degree descending)
+__global__ void k_first_below(const uint64_t* row_off, uint64_t n, uint32_t deg, uint64_t* out) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (row_off[mid + 1] - row_off[mid] >= deg) lo = mid + 1;
+    else hi = mid;
+  }
+  *out = lo;
+}
+
+void degree_classes(Engine& eng, Part& p) {
+  BCState& b = p.bcs;
+  if (b.classes) return;
+  DevBuf<uint64_t> d(2);
+  k_first_below<<<1, 1, 0, eng.stream>>>(p.row_off.get(), p.nz_end, 2048, d.get());
+  k_first_below<<<1, 1, 0, eng.stream>>>(p.row_off.get(), p.nz_end, 32, d.get() + 1);
+  TG_CK(cudaGetLastError());
+  uint64_t h[2];
+  TG_CK(cudaMemcpyAsync(h, d.get(), 16, cudaMemcpyDeviceToHost, eng.stream));
+  TG_CK(cudaStreamSynchronize(eng.stream));
+  b.n_big = h[0];
+  b.n_mid = h[1];
+  b.classes = true;
+}
+
 // Backward push over the in-CSR (direction-optimized backward level): for each
 // w in F[L+1] (Aux = c[w]) and in-edge (v, w) with v in F[L]: dsum[v] += c[w].
 struct BcBwdPushOp {
@@ -311,22 +418,32 @@ __global__ void k_bc_pack(const uint32_t* lid, uint64_t I, const uint32_t* succ,
   }
 }
 
-// delta, bc and c for the vertices of level L (one warp per bitmap word)
+// delta, bc and c for the vertices of level L.  A warp loads 32 consecutive
+// bitmap words (coalesced), then visits only the non-zero ones, one lane per
+// vertex of the word: sparse levels cost one pass over the bitmap, dense ones
+// touch sigma / dsum / bc / c in 32-vertex runs.
 __global__ void k_bc_level(const uint32_t* F, uint64_t Vp, uint64_t nz_end, const double* sigma,
                            const double* dsum, double* bc, double* c, unsigned long long* inexact) {
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t nwords = words_for(Vp);
-  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < nwords; w += nwarps) {
-    const uint32_t x = F[w];
-    if (!((x >> lane) & 1u)) continue;
-    const uint64_t v = w * 32 + lane;
-    const double sv = sigma[v];
-    // reading A11: path counts are exact fp64 integers only below 2^53
-    if (sv >= 9007199254740992.0) atomicOr(inexact, 1ull);
-    const double delta = v < nz_end ? sv * dsum[v] : 0.0;
-    bc[v] += delta;
-    c[v] = (1.0 + delta) / sv;
+  for (uint64_t w0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32; w0 < nwords;
+       w0 += nwarps * 32) {
+    const uint32_t mine = (w0 + lane < nwords) ? F[w0 + lane] : 0u;
+    uint32_t nz = __ballot_sync(0xffffffffu, mine != 0u);
+    while (nz) {
+      const int j = __ffs(nz) - 1;
+      nz &= nz - 1;
+      const uint32_t x = __shfl_sync(0xffffffffu, mine, j);
+      if (!((x >> lane) & 1u)) continue;
+      const uint64_t v = (w0 + j) * 32 + lane;
+      const double sv = sigma[v];
+      // reading A11: path counts are exact fp64 integers only below 2^53
+      if (sv >= 9007199254740992.0) atomicOr(inexact, 1ull);
+      const double delta = v < nz_end ? sv * dsum[v] : 0.0;
+      bc[v] += delta;
+      c[v] = (1.0 + delta) / sv;
+    }
   }
 }
 
@@ -335,11 +452,24 @@ void* recv_isigma(Part& p) { return p.arena_fwd.get(); }
 void* send_pack(Part& p) { return p.bcs.ibox_pack.get(); }
 void* recv_ghost(Part& p) { return p.arena_rev.get(); }
 
-uint32_t* level_bitmap(Part& p, size_t L) {
+// Level bitmaps F[L] are allocated ahead of use (kLevelReserve up front, then
+// kLevelReserve more whenever a source reaches past them): cudaMalloc
+// synchronizes the device, so growing one level at a time inside a run put an
+// allocation (and a stall) in the timed region of every source deeper than
+// all earlier ones.
+constexpr size_t kLevelReserve = 16;
+
+void reserve_levels(Part& p, size_t L) {
   BCState& b = p.bcs;
+  if (b.level_bm.size() > L) return;
   const uint64_t nw = std::max<uint64_t>(words_for(p.Vp), 1);
-  while (b.level_bm.size() <= L) b.level_bm.emplace_back(nw);
-  return b.level_bm[L].get();
+  const size_t want = (L / kLevelReserve + 1) * kLevelReserve;
+  while (b.level_bm.size() < want) b.level_bm.emplace_back(nw);
+}
+
+uint32_t* level_bitmap(Part& p, size_t L) {
+  reserve_levels(p, L);
+  return p.bcs.level_bm[L].get();
 }
 
 }  // namespace
@@ -349,6 +479,14 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
   TG_REQUIRE(out != nullptr || (eng.multi() && eng.rank != 0), TG_EINVAL, "tg_bc: NULL output");
   for (int i = 0; i < k; ++i) TG_REQUIRE(sources[i] < eng.V, TG_EINVAL, "tg_bc: source >= V");
   ensure_frontier_state(eng);
+  // outside the timed region: level bitmaps, out-degree class bounds
+  for (auto& pp : eng.parts) {
+    reserve_levels(*pp, 0);
+    degree_classes(eng, *pp);
+  }
+  // backward pull by out-degree class (TG_BC_BWD_CLASSES=0: reduce-mode walker)
+  const bool bwd_classes =
+      !(std::getenv("TG_BC_BWD_CLASSES") && std::getenv("TG_BC_BWD_CLASSES")[0] == '0');
   cudaStream_t s = eng.stream;
   for (auto& pp : eng.parts) {
     Part& p = *pp;
@@ -432,7 +570,10 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         uint32_t* next = level_bitmap(p, L + 1);
         TG_CK(cudaMemsetAsync(next, 0, words_for(p.Vp) * 4, s));
         launch_compact(eng, p.ts);
-        if (pull && pull_classes) {
+        // class kernels when the unexplored edges (~ the pull's work) are a
+        // large share; otherwise the per-word kernel's cheaper full scan wins
+        const bool dense = (eng.E - std::min(explored, eng.E)) * 16 > eng.E;
+        if (pull && pull_classes && dense) {
           // rows by in-degree class on fork/join streams (disjoint rows)
           PullSigma o{p.in_off.get(), p.in_col.get(), b.level_bm[L].get(), f.visited.get(),
                       b.sigma.get(), next, f.counters.get() + 1};
@@ -571,6 +712,35 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
                            (uint32_t)std::min<uint64_t>(bc_priv, p.Vp)};
             launch_expand_on(eng, in_tiles(p), p.ts_in, p.bcs.level_bm[L + 1].get(), op,
                              TG_K_BCB_EXPAND, p.fs.counters.get() + 1);
+          } else if (bwd_classes && lvl_out[L] * 16 > eng.E) {
+            // dense level (F[L]'s out-edges > |E|/16): class kernels; sparse
+            // levels keep the tile walker, which only visits active tiles
+            if (!p.nz_end) continue;
+            const double* ghost = reinterpret_cast<const double*>(p.arena_rev.get());
+            PullDelta o{p.row_off.get(), p.col.get(), p.bcs.level_bm[L].get(),
+                        p.bcs.level_bm[L + 1].get(), p.bcs.c.get(),
+                        eng.fused ? ghost + (L & 1) : ghost, eng.fused ? 2u : 1u,
+                        p.bcs.dsum.get(), p.fs.counters.get() + 1};
+            const uint64_t nb = p.bcs.n_big, nm = p.bcs.n_mid;
+            eng.prof_begin(TG_K_BCB_EXPAND);
+            eng.fork();
+            if (nb) {
+              k_bc_bwd_cta<<<grid_for(nb, 1, 148u * 8u), 256, 0, eng.side[0]>>>(o, nb);
+              eng.launches++;
+            }
+            if (nm > nb) {
+              k_bc_bwd_warp<<<grid_for((nm - nb) * 32, 256, 148u * 16u), 256, 0, eng.side[1]>>>(
+                  o, nb, nm);
+              eng.launches++;
+            }
+            if (p.nz_end > nm) {
+              k_bc_bwd_thread<<<grid_for(p.nz_end - nm, 256, 148u * 16u), 256, 0, s>>>(o, nm,
+                                                                                      p.nz_end);
+              eng.launches++;
+            }
+            eng.join();
+            eng.prof_end(TG_K_BCB_EXPAND);
+            TG_CK(cudaGetLastError());
           } else {
             if (!p.ntiles) continue;
             launch_mark_tiles(eng, out_tiles(p), p.Vp, p.bcs.level_bm[L].get(), p.ts);
@@ -596,7 +766,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         if (!p.Vp) continue;
-        k_bc_level<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
+        k_bc_level<<<grid_for(words_for(p.Vp), 256, 148u * 16u), 256, 0, s>>>(
             p.bcs.level_bm[L].get(), p.Vp, p.nz_end, p.bcs.sigma.get(), p.bcs.dsum.get(),
             p.bcs.bc.get(), p.bcs.c.get(), p.fs.counters.get() + 4);
         TG_CK(cudaGetLastError());

@@ -101,6 +101,10 @@ struct BCState {
   DevBuf<double> obox_sigma;              // forward partial sigma sums (send)
   DevBuf<double> ibox_pack;               // backward pull: owner-packed c (send)
   std::vector<DevBuf<uint32_t>> level_bm; // frontier bitmap per level
+  // out-degree class bounds of the local ids (ids are in out-degree order):
+  // [0, n_big) >= 2048, [n_big, n_mid) >= 32; computed once (backward pull)
+  bool classes = false;
+  uint64_t n_big = 0, n_mid = 0;
 };
 
 struct Part {
