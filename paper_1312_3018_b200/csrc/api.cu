@@ -43,7 +43,7 @@ uint64_t Engine::device_bytes() const {
   uint64_t t = b(rank_of);
   for (auto& pp : parts) {
     const Part& p = *pp;
-    t += b(p.row_off) + b(p.col) + b(p.w) + b(p.global_of) + b(p.tile_vf) + b(p.tile_vl) +
+    t += b(p.row_off) + b(p.col) + b(p.w) + b(p.w8) + b(p.global_of) + b(p.tile_vf) + b(p.tile_vl) +
          b(p.obox_rid) + b(p.ibox_lid) + b(p.in_off) + b(p.in_col) + b(p.outdeg) + b(p.pr_cta) +
          b(p.pr_warp) + b(p.in_tile_vf) + b(p.in_tile_vl) + b(p.arena_fwd) + b(p.arena_rev) +
          b(p.staging);

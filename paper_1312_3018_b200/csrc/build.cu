@@ -373,6 +373,12 @@ void sort_rows(const uint64_t* row_off, uint64_t nrows, uint32_t* keys, uint32_t
   }
 }
 
+__global__ void k_u32_to_u8(const uint32_t* in, uint64_t n, uint8_t* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = (uint8_t)in[i];
+}
+
 void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
                 const uint32_t* outdeg) {
   cudaStream_t s = eng.stream;
@@ -487,6 +493,25 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
   nrem.release();
   ukeys.release();
   sort_rows(pt.row_off.get(), Vp, pt.col.get(), eng.weighted ? pt.w.get() : nullptr, s);
+  // weights that fit a byte (RMAT weights are in [1, 63], reading A17) are
+  // kept as u8: SSSP streams 1 B instead of 4 B of weight per relaxation
+  if (eng.weighted && pt.Ep) {
+    DevBuf<uint32_t> mx(1);
+    size_t tmp = 0;
+    TG_CK(cub::DeviceReduce::Max(nullptr, tmp, pt.w.get(), mx.get(), (int64_t)pt.Ep, s));
+    DevBuf<uint8_t> t(tmp ? tmp : 1);
+    TG_CK(cub::DeviceReduce::Max(t.get(), tmp, pt.w.get(), mx.get(), (int64_t)pt.Ep, s));
+    uint32_t hmax = 0;
+    TG_CK(cudaMemcpyAsync(&hmax, mx.get(), 4, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaStreamSynchronize(s));
+    if (hmax < 256 && !(std::getenv("TG_W32") && std::getenv("TG_W32")[0] == '1')) {
+      pt.w8.alloc(pt.Ep);
+      k_u32_to_u8<<<G(pt.Ep), kB, 0, s>>>(pt.w.get(), pt.Ep, pt.w8.get());
+      TG_CK(cudaGetLastError());
+      TG_CK(cudaStreamSynchronize(s));
+      pt.w.release();
+    }
+  }
 
   // tiles
   pt.ntiles = (pt.Ep + kTile - 1) / kTile;

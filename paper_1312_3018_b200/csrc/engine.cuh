@@ -114,6 +114,7 @@ struct Part {
   uint32_t hub_deg = 0, hub_end = 0;  // cached: first local id with out-degree < hub_deg
   DevBuf<uint64_t> row_off;
   DevBuf<uint32_t> col, w, global_of;
+  DevBuf<uint8_t> w8;  // weights as bytes when every weight < 256 (then w is released)
   // tiles
   uint64_t ntiles = 0;
   DevBuf<uint32_t> tile_vf, tile_vl;  // first / last row touched by tile t

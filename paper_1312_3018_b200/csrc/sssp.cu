@@ -32,11 +32,12 @@ namespace tg {
 
 namespace {
 
+template <class W>  // weight storage: uint8_t when every weight < 256, else uint32_t
 struct SsspOp {
   using Aux = uint32_t;
   static constexpr bool kReduce = false, kFilter = true;
   const uint32_t* col;
-  const uint32_t* w;
+  const W* w;
   uint32_t* dist;
   uint32_t* next;
   uint32_t* obox;
@@ -60,7 +61,9 @@ struct SsspOp {
   struct St {
     uint32_t cur;
   };
-  __device__ __forceinline__ Pre pre(uint64_t e) const { return {__ldcs(col + e), __ldcs(w + e)}; }
+  __device__ __forceinline__ Pre pre(uint64_t e) const {
+    return {__ldcs(col + e), (uint32_t)__ldcs(w + e)};
+  }
   __device__ __forceinline__ St st(const Pre& p) const {
     return {(p.t & kRemote) ? obox[p.t & ~kRemote] : dist[p.t]};
   }
@@ -192,9 +195,17 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
       Part& p = *eng.parts[i];
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
-      SsspOp op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
-                f.counters.get() + 4, p.rout(), eng.fused, thresh, hub_deg ? hubs[i] : kInf};
-      launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
+      if (p.w8.get()) {
+        SsspOp<uint8_t> op{p.col.get(), p.w8.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
+                           f.counters.get() + 4, p.rout(), eng.fused, thresh,
+                           hub_deg ? hubs[i] : kInf};
+        launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
+      } else {
+        SsspOp<uint32_t> op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
+                            f.counters.get() + 4, p.rout(), eng.fused, thresh,
+                            hub_deg ? hubs[i] : kInf};
+        launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
+      }
     }
     supersteps++;
     if (eng.P > 1) {

@@ -411,3 +411,25 @@ def test_c3_rmat26_pagerank_bc_partitions(tg):
             eng.set_exchange(tg.TG_EXCHANGE_FUSED)
         assert_bc(eng.bc(srcs)[0], bc_ref)
         eng.close()
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_sssp_wide_weights_and_overflow(tg, P):
+    """Weights >= 256 keep the 4-byte weight array (the byte form is used only
+    when every weight fits); a distance past 2^32 - 1 is TG_EINTERNAL (reading
+    A18), not a wrapped value."""
+    from paper_1312_3018_b200 import tgraph
+
+    rng = np.random.default_rng(21)
+    V, E = 600, 5000
+    src, dst = rng.integers(0, V, E), rng.integers(0, V, E)
+    w = rng.integers(1, 1 << 20, E)
+    G, eng = both(tg, V, src, dst, w, P=P)
+    for s in (0, 7, 311):
+        assert np.array_equal(eng.sssp(s)[0], G.sssp(s)), s
+    # 0 -> 1 -> 2 with weights 2^31 each: dist(2) = 2^32 does not fit u32
+    eng2 = tg.Engine.from_edges(3, np.array([0, 1], np.uint32), np.array([1, 2], np.uint32),
+                                np.array([1 << 31, 1 << 31], np.uint32), partitions=P)
+    with pytest.raises(tgraph.TGraphError) as e:
+        eng2.sssp(0)
+    assert e.value.code == tgraph.TG_EINTERNAL
