@@ -348,6 +348,39 @@ void scatter_global(Engine& eng, const void* vals, const uint32_t* gof, uint64_t
   TG_CK(cudaGetLastError());
 }
 
+// Single-process collection as a gather: out[g] = vals_p[l] with (p, l) =
+// deal(rank_of[g]) -- coalesced writes in global order, so the output can be
+// produced chunk by chunk and each chunk's host copy overlaps the next gather.
+struct PartVals {
+  const void* v[TG_MAX_PARTITIONS];
+  int P;
+};
+
+template <typename T>
+__global__ void k_gather_global(PartVals pv, const uint32_t* rank_of, uint64_t g0, uint64_t g1,
+                                T* out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t g = g0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < g1; g += stride) {
+    int p;
+    uint32_t l;
+    deal(rank_of[g], pv.P, &p, &l);
+    out[g] = static_cast<const T*>(pv.v[p])[l];
+  }
+}
+
+void gather_global(Engine& eng, const PartVals& pv, size_t elem, uint64_t g0, uint64_t g1, void* out,
+                   cudaStream_t s) {
+  if (g1 <= g0) return;
+  const unsigned grid = grid_for(g1 - g0, 256);
+  if (elem == 4)
+    k_gather_global<uint32_t><<<grid, 256, 0, s>>>(pv, eng.rank_of.get(), g0, g1,
+                                                    static_cast<uint32_t*>(out));
+  else
+    k_gather_global<unsigned long long><<<grid, 256, 0, s>>>(
+        pv, eng.rank_of.get(), g0, g1, static_cast<unsigned long long*>(out));
+  TG_CK(cudaGetLastError());
+}
+
 uint64_t reached(Engine& eng, bool bitmap, uint64_t* nreached) {
   DevBuf<unsigned long long> acc(2);
   TG_CK(cudaMemsetAsync(acc.get(), 0, 16, eng.stream));
@@ -384,8 +417,35 @@ void collect(Engine& eng, ValsOf vals, size_t elem, void* out, int mem) {
     if (eng.scratch.bytes() < eng.V * elem) eng.scratch.alloc(eng.V * elem);
     dout = eng.scratch.get();
   }
-  if (!eng.multi()) {
+  // TG_COLLECT: 0 scatter + one copy, 1 gather + one copy, 2 gather chunks
+  // with overlapped copies
+  int mode = 2;
+  if (const char* c = std::getenv("TG_COLLECT")) mode = std::atoi(c);
+  if (!eng.multi() && mode == 0) {
     for (auto& pp : eng.parts) scatter_global(eng, vals(*pp), pp->global_of.get(), pp->Vp, elem, dout);
+  } else if (!eng.multi()) {
+    PartVals pv{};
+    pv.P = eng.P;
+    for (auto& pp : eng.parts) pv.v[pp->id] = vals(*pp);
+    if (mem == TG_MEM_HOST && mode == 2) {
+      // chunked: gather chunk k on the engine stream, copy it to the host on a
+      // side stream while chunk k+1 is gathered
+      const uint64_t chunk = 1ull << 25;
+      eng.fork();  // side streams start after the algorithm's last kernel
+      for (uint64_t g0 = 0; g0 < eng.V; g0 += chunk) {
+        const uint64_t g1 = std::min<uint64_t>(eng.V, g0 + chunk);
+        gather_global(eng, pv, elem, g0, g1, dout, s);
+        TG_CK(cudaEventRecord(eng.fork_ev, s));
+        TG_CK(cudaStreamWaitEvent(eng.side[0], eng.fork_ev, 0));
+        TG_CK(cudaMemcpyAsync(static_cast<uint8_t*>(out) + g0 * elem,
+                              static_cast<uint8_t*>(dout) + g0 * elem, (g1 - g0) * elem,
+                              cudaMemcpyDeviceToHost, eng.side[0]));
+      }
+      eng.join();
+      TG_CK(cudaStreamSynchronize(s));
+      return;
+    }
+    gather_global(eng, pv, elem, 0, eng.V, dout, s);
   } else {
     // stage my values, then rank 0 scatters every rank's staging (IPC-mapped)
     Part& me = *eng.parts[0];
