@@ -17,7 +17,10 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active",
         "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
-        "launch__registers_per_thread", "smsp__inst_executed.sum"]
+        "launch__registers_per_thread", "smsp__inst_executed.sum",
+        # sector efficiency: useful bytes per 32-byte sector
+        "smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio",
+        "smsp__sass_average_data_bytes_per_sector_mem_global_op_st.ratio"]
 STALLS = ["long_scoreboard", "barrier", "wait", "short_scoreboard", "lg_throttle", "mio_throttle",
           "math_pipe_throttle", "not_selected", "selected", "branch_resolving", "membar", "drain"]
 LEDGER = {"prof_pr": "pr_pull", "prof_bfs": "bfs_expand", "prof_sssp": "sssp_expand",
