@@ -98,8 +98,8 @@ struct is_split<Op, std::void_t<decltype(Op::kSplit)>> {
 //   void edge(const Aux&, uint64_t e) const;                   (!kReduce)
 //   double edge_val(uint64_t e) const;                         (kReduce)
 //   void vertex_done(uint32_t v, double sum, bool whole_row) const;  (kReduce)
-template <class Op, int U>
-__global__ void __launch_bounds__(kExpandThreads) k_warp_expand(TileArgs a, Op op) {
+template <class Op, int U, int MB = 0>  // MB 0: no min-blocks bound (ptxas default, <= 64 regs here)
+__global__ void __launch_bounds__(kExpandThreads, MB) k_warp_expand(TileArgs a, Op op) {
   using Aux = typename Op::Aux;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t lowm = lane == 31 ? kFull : ((2u << lane) - 1u);
@@ -316,7 +316,7 @@ void launch_expand(Engine& eng, Part& p, TileSched& ts, const uint32_t* frontier
   launch_expand_on(eng, out_tiles(p), ts, frontier, op, kid, edges);
 }
 
-template <class Op, int U>
+template <class Op, int U, int MB = 0>
 void launch_walker(Engine& eng, const TileArgs& a, const Op& op) {
   // persistent grid = exactly the resident CTAs (static tile striding assumes residency)
   static int per_sm = 0;
@@ -324,14 +324,14 @@ void launch_walker(Engine& eng, const TileArgs& a, const Op& op) {
   const size_t smem = smem_of(op);
   if (!per_sm || smem != per_sm_smem) {
     if (smem > 48 * 1024)
-      TG_CK(cudaFuncSetAttribute(k_warp_expand<Op, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      TG_CK(cudaFuncSetAttribute(k_warp_expand<Op, U, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    TG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_warp_expand<Op, U>,
+    TG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_warp_expand<Op, U, MB>,
                                                         kExpandThreads, smem));
     if (per_sm < 1) per_sm = 1;
     per_sm_smem = smem;
   }
-  k_warp_expand<Op, U><<<expand_grid() / 8u * (unsigned)per_sm, kExpandThreads, smem, eng.stream>>>(
+  k_warp_expand<Op, U, MB><<<expand_grid() / 8u * (unsigned)per_sm, kExpandThreads, smem, eng.stream>>>(
       a, op);
 }
 
@@ -349,7 +349,18 @@ void launch_expand_on(Engine& eng, const CsrTiles& c, TileSched& ts, const uint3
       const char* u = std::getenv("TG_UNROLL");
       unroll = u ? std::atoi(u) : Op::kUnroll;
     }
-    if (unroll == 1) launch_walker<Op, 1>(eng, a, op);
+    // TG_WALK_MINB (experiment): __launch_bounds__ min blocks 5 / 6 caps the
+    // registers (48 / 40) for more resident warps
+    static int minb = -1;
+    if (minb < 0) {
+      const char* m = std::getenv("TG_WALK_MINB");
+      minb = m ? std::atoi(m) : 0;
+    }
+    if (minb == 5 && unroll == 4) launch_walker<Op, 4, 5>(eng, a, op);
+    else if (minb == 6 && unroll == 4) launch_walker<Op, 4, 6>(eng, a, op);
+    else if (minb == 5 && unroll == 2) launch_walker<Op, 2, 5>(eng, a, op);
+    else if (unroll == 1) launch_walker<Op, 1>(eng, a, op);
+    else if (unroll == 3) launch_walker<Op, 3>(eng, a, op);
     else if (unroll == 4) launch_walker<Op, 4>(eng, a, op);
     else if (unroll == 8) launch_walker<Op, 8>(eng, a, op);
     else launch_walker<Op, 2>(eng, a, op);
