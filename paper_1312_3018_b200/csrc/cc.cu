@@ -46,15 +46,28 @@ struct CcPushOp {  // out-CSR
   RemoteOut rout;  // fused: improvements of the local outbox minimum also go
   bool fused;      // straight to the owner's inbox slot (RED.MIN, running minimum)
   __device__ __forceinline__ Aux aux(uint32_t v) const { return label[v]; }
-  __device__ __forceinline__ void edge(const Aux& l, uint64_t e) const {
-    const uint32_t t = __ldcs(col + e);
+  // split walker (frontier.cuh): column, then the target's label (or outbox
+  // minimum), then the min-reductions
+  static constexpr bool kSplit = true;
+  static constexpr int kUnroll = 4;
+  struct Pre {
+    uint32_t t;
+  };
+  struct St {
+    uint32_t cur;
+  };
+  __device__ __forceinline__ Pre pre(uint64_t e) const { return {__ldcs(col + e)}; }
+  __device__ __forceinline__ St st(const Pre& p) const {
+    return {(p.t & kRemote) ? obox[p.t & ~kRemote] : label[p.t]};
+  }
+  __device__ __forceinline__ void fin(const Aux& l, const Pre& p, const St& q) const {
+    if (!(l < q.cur)) return;
+    const uint32_t t = p.t;
     if (t & kRemote) {
       const uint32_t s = t & ~kRemote;
-      if (l < obox[s]) {
-        atomicMin(&obox[s], l);
-        if (fused) atomicMin(rout.slot<uint32_t>(s), l);
-      }
-    } else if (l < label[t]) {
+      atomicMin(&obox[s], l);
+      if (fused) atomicMin(rout.slot<uint32_t>(s), l);
+    } else {
       atomicMin(&label[t], l);
       atomicOr(&next[t >> 5], 1u << (t & 31));
     }
@@ -68,11 +81,20 @@ struct CcRevOp {  // in-CSR local rows: v active, entries = local sources u
   uint32_t* label;
   uint32_t* next;
   __device__ __forceinline__ Aux aux(uint32_t v) const { return label[v]; }
-  __device__ __forceinline__ void edge(const Aux& l, uint64_t e) const {
-    const uint32_t u = __ldcs(in_col + e);
-    if (l < label[u]) {
-      atomicMin(&label[u], l);
-      atomicOr(&next[u >> 5], 1u << (u & 31));
+  static constexpr bool kSplit = true;  // in_col, then the source's label, then the min
+  static constexpr int kUnroll = 4;
+  struct Pre {
+    uint32_t u;
+  };
+  struct St {
+    uint32_t cur;
+  };
+  __device__ __forceinline__ Pre pre(uint64_t e) const { return {__ldcs(in_col + e)}; }
+  __device__ __forceinline__ St st(const Pre& p) const { return {label[p.u]}; }
+  __device__ __forceinline__ void fin(const Aux& l, const Pre& p, const St& q) const {
+    if (l < q.cur) {
+      atomicMin(&label[p.u], l);
+      atomicOr(&next[p.u >> 5], 1u << (p.u & 31));
     }
   }
 };
