@@ -318,6 +318,7 @@ def main():
         ds_h = torch.empty(V, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
         pr_h = torch.empty(V, dtype=torch.float32, pin_memory=True).numpy()
         bc_h = torch.empty(V, dtype=torch.float64, pin_memory=True).numpy()
+        step(args.warmup + 2 * args.steps, (lv_h, ds_h, pr_h, bc_h))  # untimed e2e warm-up
         barrier()
         t0 = time.perf_counter()
         tr = 0

@@ -414,7 +414,9 @@ void collect(Engine& eng, ValsOf vals, size_t elem, void* out, int mem) {
   cudaStream_t s = eng.stream;
   void* dout = out;
   if (root && mem == TG_MEM_HOST) {  // device staging for the host copy, kept across calls
-    if (eng.scratch.bytes() < eng.V * elem) eng.scratch.alloc(eng.V * elem);
+    // sized for the widest result (8 B) on first use: no re-allocation (a
+    // device-wide synchronizing cudaMalloc) when a wider result follows
+    if (eng.scratch.bytes() < eng.V * elem) eng.scratch.alloc(eng.V * 8);
     dout = eng.scratch.get();
   }
   // TG_COLLECT: 0 scatter + one copy, 1 gather + one copy, 2 gather chunks
