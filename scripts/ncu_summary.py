@@ -10,6 +10,10 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
+try:
+    PEAK = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+except (OSError, KeyError, ValueError):
+    PEAK = 6537.3
 WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -62,6 +66,18 @@ for rep in sorted(f for f in os.listdir(OUT) if f.endswith(".ncu-rep")):
                 st.append((int(float(d[k])), s))
         st.sort(reverse=True)
         lines.append("- top stall samples: " + ", ".join(f"{s}={n}" for n, s in st[:6]))
+        try:  # derived: achieved DRAM bandwidth and load sector efficiency
+            t_ms = float(d["gpu__time_duration.sum"]) * {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3,
+                                                           "usecond": 1e-3}.get(
+                u["gpu__time_duration.sum"], 1.0)
+            by = (to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) +
+                  to_bytes(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"]))
+            gbs = by / (t_ms * 1e-3) / 1e9
+            eff = float(d["smsp__sass_average_data_bytes_per_sector_mem_global_op_ld.ratio"]) / 32
+            lines.append(f"- derived: DRAM {gbs:.0f} GB/s = {gbs / PEAK:.2f} of {PEAK:.0f} GB/s "
+                         f"(cold, serialised replay); load sector efficiency {eff:.2f}")
+        except (KeyError, ValueError, ZeroDivisionError):
+            pass
         lines.append("")
         try:
             per_launch.append(to_bytes(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) +
