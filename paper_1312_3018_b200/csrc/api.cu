@@ -44,7 +44,7 @@ uint64_t Engine::device_bytes() const {
   for (auto& pp : parts) {
     const Part& p = *pp;
     t += b(p.row_off) + b(p.col) + b(p.w) + b(p.w8) + b(p.global_of) + b(p.tile_vf) + b(p.tile_vl) +
-         b(p.obox_rid) + b(p.ibox_lid) + b(p.in_off) + b(p.in_col) + b(p.outdeg) + b(p.pr_cta) +
+         b(p.obox_rid) + b(p.ibox_lid) + b(p.in_off) + b(p.in_col) + b(p.outdeg) + b(p.in_nz) + b(p.pr_cta) +
          b(p.pr_warp) + b(p.in_tile_vf) + b(p.in_tile_vl) + b(p.arena_fwd) + b(p.arena_rev) +
          b(p.staging);
   }

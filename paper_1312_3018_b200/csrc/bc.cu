@@ -144,10 +144,13 @@ struct PullSigma {
   const uint32_t* in_col;
   const uint32_t* F;        // F[L]
   const uint32_t* visited;
+  const uint32_t* has_in;   // rows with an in-edge
   double* sigma;
   uint32_t* next;           // F[L+1]
   unsigned long long* edges;
-  __device__ __forceinline__ bool skip(uint64_t v) const { return bit_test(visited, (uint32_t)v); }
+  __device__ __forceinline__ bool skip(uint64_t v) const {
+    return bit_test(visited, (uint32_t)v) || !bit_test(has_in, (uint32_t)v);
+  }
   __device__ __forceinline__ double sum(uint64_t i, uint64_t e, uint32_t step) const {
     double s0 = 0.0, s1 = 0.0;
     for (; i + step < e; i += 2ull * step) {
@@ -576,7 +579,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         if (pull && pull_classes && dense) {
           // rows by in-degree class on fork/join streams (disjoint rows)
           PullSigma o{p.in_off.get(), p.in_col.get(), b.level_bm[L].get(), f.visited.get(),
-                      b.sigma.get(), next, f.counters.get() + 1};
+                      p.in_nz.get(), b.sigma.get(), next, f.counters.get() + 1};
           eng.prof_begin(TG_K_BCF_EXPAND);
           eng.fork();
           if (p.n_cta) {

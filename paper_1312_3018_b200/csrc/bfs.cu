@@ -82,16 +82,19 @@ __global__ void k_bfs_scatter(const uint32_t* ibits, const uint32_t* lid, uint64
 // warp owns its word of `next`, so no atomics.  Same levels as top-down.
 __global__ void __launch_bounds__(256) k_bfs_bottom_up(const uint64_t* in_off,
                                                        const uint32_t* in_col, const uint32_t* cur,
-                                                       const uint32_t* visited, uint32_t* next,
+                                                       const uint32_t* visited,
+                                                       const uint32_t* has_in, uint32_t* next,
                                                        uint64_t Vp, unsigned long long* edges) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t nwords = words_for(Vp);
   unsigned long long cnt = 0;
   for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < nwords; w += nwarps) {
-    const uint32_t vis = visited[w];
+    // candidates: unvisited vertices with an in-edge (no offset reads for the
+    // ~half of RMAT vertices that have none)
+    const uint32_t open = ~visited[w] & has_in[w];
     const uint64_t v = w * 32 + lane;
-    const bool cand = v < Vp && !((vis >> lane) & 1u);
+    const bool cand = v < Vp && ((open >> lane) & 1u);
     if (!__ballot_sync(0xffffffffu, cand)) continue;
     bool found = false;
     if (cand) {
@@ -174,8 +177,8 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
       if (bottom_up) {
         eng.prof_begin(TG_K_BFS_EXPAND);
         k_bfs_bottom_up<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
-            p.in_off.get(), p.in_col.get(), f.cur.get(), f.visited.get(), f.next.get(), p.Vp,
-            f.counters.get() + 1);
+            p.in_off.get(), p.in_col.get(), f.cur.get(), f.visited.get(), p.in_nz.get(),
+            f.next.get(), p.Vp, f.counters.get() + 1);
         eng.prof_end(TG_K_BFS_EXPAND);
         TG_CK(cudaGetLastError());
         eng.launches++;

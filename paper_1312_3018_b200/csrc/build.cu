@@ -379,6 +379,19 @@ __global__ void k_u32_to_u8(const uint32_t* in, uint64_t n, uint8_t* out) {
     out[i] = (uint8_t)in[i];
 }
 
+// bitmap of the local rows with at least one in-edge (thread per word)
+__global__ void k_has_in(const uint64_t* in_off, uint64_t Vp, uint32_t* bm) {
+  const uint64_t nw = words_for(Vp);
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < nw; w += stride) {
+    uint32_t x = 0;
+    const uint64_t v0 = w * 32, v1 = v0 + 32 < Vp ? v0 + 32 : Vp;
+    for (uint64_t v = v0; v < v1; ++v)
+      if (in_off[v + 1] > in_off[v]) x |= 1u << (v - v0);
+    bm[w] = x;
+  }
+}
+
 void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
                 const uint32_t* outdeg) {
   cudaStream_t s = eng.stream;
@@ -578,6 +591,11 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
     indeg.release();
     sort_rows(pt.in_off.get(), R, pt.in_col.get(), nullptr, s);
     // edge tiles over the local rows of the in-CSR (BC backward push)
+    pt.in_nz.alloc(std::max<uint64_t>(words_for(Vp), 1));
+    if (Vp) {
+      k_has_in<<<G(words_for(Vp)), kB, 0, s>>>(pt.in_off.get(), Vp, pt.in_nz.get());
+      TG_CK(cudaGetLastError());
+    }
     pt.in_E_local = Vp ? d2h(pt.in_off.get() + Vp, s) : 0;
     pt.in_ntiles = (pt.in_E_local + kTile - 1) / kTile;
     pt.in_tile_vf.alloc(std::max<uint64_t>(pt.in_ntiles, 1));

@@ -129,6 +129,7 @@ struct Part {
   DevBuf<uint64_t> in_off;          // Vp + S + 1
   DevBuf<uint32_t> in_col;          // in-order position of the local source
   DevBuf<uint32_t> outdeg;          // out-degree per local id (Vp)
+  DevBuf<uint32_t> in_nz;           // bitmap over [0, Vp): in-degree > 0 (pull candidates)
   uint64_t in_E_local = 0;          // in-edges of the local rows [0, Vp)
   uint64_t in_ntiles = 0;           // edge tiles of the in-CSR local rows
   DevBuf<uint32_t> in_tile_vf, in_tile_vl;
