@@ -269,6 +269,20 @@ int tg_engine_set_profiling(tg_engine* eng, int on);   /* also resets the ledger
  * The environment variable TG_FUSED_EXCHANGE=0 sets the default to COPY. */
 enum { TG_EXCHANGE_COPY = 0, TG_EXCHANGE_FUSED = 1 };
 int tg_engine_set_exchange(tg_engine* eng, int mode);
+
+/* PageRank communication (PAPER.md:182 vs P:945-946; reading A8).
+ *   TG_PR_PUSH (default): each partition sums its sources' contributions per
+ *     remote target (outbox row of the in-CSR) and sends one partial sum per
+ *     target; the owner adds them (source-side reduction).
+ *   TG_PR_PULL: TOTEM_COMM_PULL -- each partition publishes the contribution
+ *     of every source with an out-edge into a peer, into ghost slots appended
+ *     to that peer's contribution array, and pulls over a ghost-indexed in-CSR
+ *     (built on the first PULL run, outside the timed region).  Engines with
+ *     all partitions in one process only.
+ * Results equal up to fp64 summation order (1e-5 relative per vertex).
+ * TG_EINVAL for NULL, an unknown mode, or PULL on a multi-process engine. */
+enum { TG_PR_PUSH = 0, TG_PR_PULL = 1 };
+int tg_engine_set_pagerank_comm(tg_engine* eng, int mode);
 int tg_engine_kernel_stat(const tg_engine* eng, int kernel_id, tg_kernel_stat* out);
 const char* tg_kernel_name(int kernel_id);
 

@@ -8,6 +8,8 @@ from .tgraph import (  # noqa: F401
     TG_EXCHANGE_COPY,
     TG_EXCHANGE_FUSED,
     TG_INF32,
+    TG_PR_PULL,
+    TG_PR_PUSH,
     TG_MEM_DEVICE,
     TG_MEM_HOST,
     Engine,
@@ -27,6 +29,7 @@ from .tgraph import (  # noqa: F401
     tg_engine_info,
     tg_engine_partition_info,
     tg_engine_set_exchange,
+    tg_engine_set_pagerank_comm,
     tg_pagerank,
     tg_rmat_edges,
     tg_sssp,

@@ -719,6 +719,18 @@ int tg_engine_set_exchange(tg_engine* e, int mode) {
   });
 }
 
+int tg_engine_set_pagerank_comm(tg_engine* e, int mode) {
+  return guard([&] {
+    TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");
+    TG_REQUIRE(mode == TG_PR_PUSH || mode == TG_PR_PULL, TG_EINVAL,
+               "tg_engine_set_pagerank_comm: unknown mode");
+    Engine& eng = *reinterpret_cast<Engine*>(e);
+    TG_REQUIRE(mode == TG_PR_PUSH || !eng.multi(), TG_EINVAL,
+               "tg_engine_set_pagerank_comm: PULL needs every partition in one process");
+    eng.pr_comm = mode;
+  });
+}
+
 int tg_engine_kernel_stat(const tg_engine* e, int kid, tg_kernel_stat* out) {
   return guard([&] {
     TG_REQUIRE(e && out, TG_EINVAL, "NULL argument");

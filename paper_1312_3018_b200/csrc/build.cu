@@ -838,6 +838,59 @@ void map_remote_peers(Engine& eng) {
   if (!eng.peer_atomics) eng.fused = false;
 }
 
+// ---- ghost-pull PageRank layout (build_pr_ghost) --------------------------
+// p's inbox entry j from q <-> q's outbox slot s: j = ibox_base + s.
+// Per slot s of Q's segment for p: the row v = lid[s] of p gets one entry per
+// source of Q's outbox row Vq + s.
+__global__ void k_gh_count(const uint64_t* q_in_off, uint64_t qVp, uint64_t s0, uint64_t s1,
+                           const uint32_t* lid_by_slot, uint32_t* cnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = s0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < s1; s += stride) {
+    const uint32_t v = lid_by_slot[s];
+    if (v == kInf) continue;
+    const uint64_t n = q_in_off[qVp + s + 1] - q_in_off[qVp + s];
+    if (n) atomicAdd(&cnt[v], (uint32_t)n);
+  }
+}
+__global__ void k_gh_local(const uint64_t* in_off, const uint32_t* in_col, uint64_t Vp,
+                           const uint64_t* off, uint32_t* col, uint32_t* cursor) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < Vp; v += stride) {
+    const uint64_t b = in_off[v], e = in_off[v + 1], o = off[v];
+    for (uint64_t i = b; i < e; ++i) col[o + (i - b)] = in_col[i];
+    cursor[v] = (uint32_t)(e - b);
+  }
+}
+__global__ void k_gh_fill(const uint64_t* q_in_off, const uint32_t* q_in_col, uint64_t qVp,
+                          uint64_t s0, uint64_t s1, const uint32_t* lid_by_slot,
+                          const uint32_t* pub, uint64_t npub, uint32_t ghost_base,
+                          const uint64_t* off, uint32_t* col, uint32_t* cursor) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t s = s0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < s1; s += stride) {
+    const uint32_t v = lid_by_slot[s];
+    if (v == kInf) continue;
+    for (uint64_t i = q_in_off[qVp + s], e = q_in_off[qVp + s + 1]; i < e; ++i) {
+      const uint32_t u = q_in_col[i];
+      uint64_t lo = 0, hi = npub;  // position of u in Q's publish list for p
+      while (lo < hi) {
+        const uint64_t m = (lo + hi) >> 1;
+        if (pub[m] < u) lo = m + 1;
+        else hi = m;
+      }
+      col[off[v] + atomicAdd(&cursor[v], 1u)] = ghost_base + (uint32_t)lo;
+    }
+  }
+}
+__global__ void k_deg_sum(const uint64_t* in_off, const uint32_t* cnt, uint64_t Vp, uint64_t* deg64,
+                          uint32_t* deg32) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v <= Vp; v += stride) {
+    const uint64_t d = v < Vp ? (in_off[v + 1] - in_off[v]) + cnt[v] : 0;
+    deg64[v] = d;
+    if (v < Vp) deg32[v] = (uint32_t)(d < 0xFFFFFFFFull ? d : 0xFFFFFFFFull);
+  }
+}
+
 }  // namespace
 
 void build_engine(Engine& eng, const EdgeInput& in) {
@@ -896,6 +949,134 @@ void build_engine(Engine& eng, const EdgeInput& in) {
   eng.build_ms = (uint64_t)std::chrono::duration_cast<std::chrono::milliseconds>(
                      std::chrono::steady_clock::now() - t0)
                      .count();
+}
+
+void build_pr_ghost(Engine& eng) {
+  TG_REQUIRE(!eng.multi(), TG_EINVAL,
+             "ghost-pull PageRank needs every partition in one process");
+  TG_REQUIRE(eng.has_in, TG_EINVAL, "ghost-pull PageRank needs the in-CSR");
+  bool all = true;
+  for (auto& pp : eng.parts) all = all && pp->gh.built;
+  if (all) return;
+  cudaStream_t s = eng.stream;
+  const int P = eng.P;
+  std::vector<Part*> by(P, nullptr);
+  for (auto& pp : eng.parts) by[pp->id] = pp.get();
+  // 1. publish lists: distinct sources of p's outbox rows for q, ascending
+  for (Part* pt : by) {
+    Part& p = *pt;
+    PRGhost& g = p.gh;
+    g.pub_off.assign(P + 1, 0);
+    std::vector<DevBuf<uint32_t>> seg(P);
+    std::vector<uint64_t> cnt(P, 0);
+    for (int q = 0; q < P; ++q) {
+      if (q == p.id || p.obox_off[q + 1] == p.obox_off[q]) continue;
+      const uint64_t e0 = d2h(p.in_off.get() + p.Vp + p.obox_off[q], s);
+      const uint64_t e1 = d2h(p.in_off.get() + p.Vp + p.obox_off[q + 1], s);
+      const uint64_t n = e1 - e0;
+      if (!n) continue;
+      TG_REQUIRE(n < (1ull << 31), TG_ECAPACITY, "publish list too large");
+      DevBuf<uint32_t> sorted(n);
+      seg[q].alloc(n);
+      size_t tmp = 0;
+      TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, p.in_col.get() + e0, sorted.get(), (int)n, 0,
+                                           32, s));
+      DevBuf<uint8_t> t1(tmp ? tmp : 1);
+      TG_CK(cub::DeviceRadixSort::SortKeys(t1.get(), tmp, p.in_col.get() + e0, sorted.get(), (int)n,
+                                           0, 32, s));
+      DevBuf<unsigned long long> nsel(1);
+      tmp = 0;
+      TG_CK(cub::DeviceSelect::Unique(nullptr, tmp, sorted.get(), seg[q].get(), nsel.get(), (int)n, s));
+      DevBuf<uint8_t> t2(tmp ? tmp : 1);
+      TG_CK(cub::DeviceSelect::Unique(t2.get(), tmp, sorted.get(), seg[q].get(), nsel.get(), (int)n, s));
+      cnt[q] = d2h(nsel.get(), s);
+    }
+    for (int q = 0; q < P; ++q) g.pub_off[q + 1] = g.pub_off[q] + cnt[q];
+    g.pub_lid.alloc(std::max<uint64_t>(g.pub_off[P], 1));
+    for (int q = 0; q < P; ++q)
+      if (cnt[q])
+        TG_CK(cudaMemcpyAsync(g.pub_lid.get() + g.pub_off[q], seg[q].get(), cnt[q] * 4,
+                              cudaMemcpyDeviceToDevice, s));
+    TG_CK(cudaStreamSynchronize(s));
+  }
+  // 2. ghost segments of p: q's publish list for p
+  for (Part* pt : by) {
+    PRGhost& g = pt->gh;
+    g.gh_off.assign(P + 1, 0);
+    for (int q = 0; q < P; ++q)
+      g.gh_off[q + 1] = g.gh_off[q] + (q == pt->id ? 0 : by[q]->gh.pub_off[pt->id + 1] -
+                                                             by[q]->gh.pub_off[pt->id]);
+    g.G = g.gh_off[P];
+    TG_REQUIRE(pt->Vp + g.G < (1ull << 31), TG_ECAPACITY, "ghost index space exceeds 2^31");
+  }
+  // 3. ghost in-CSR of every partition: local entries + one ghost entry per
+  //    remote in-edge (u in q, v in p), from q's outbox rows for p
+  for (Part* pt : by) {
+    Part& p = *pt;
+    PRGhost& g = p.gh;
+    const uint64_t Vp = p.Vp;
+    DevBuf<uint32_t> cnt(std::max<uint64_t>(Vp, 1)), deg32(std::max<uint64_t>(Vp, 1));
+    TG_CK(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
+    for (int q = 0; q < P; ++q) {
+      if (q == p.id) continue;
+      Part& Q = *by[q];
+      const uint64_t s0 = Q.obox_off[p.id], s1 = Q.obox_off[p.id + 1];
+      if (s1 == s0) continue;
+      const uint32_t* lid_by_slot = p.ibox_lid.get() + p.ibox_off[q] - s0;
+      k_gh_count<<<G(s1 - s0), kB, 0, s>>>(Q.in_off.get(), Q.Vp, s0, s1, lid_by_slot, cnt.get());
+    }
+    DevBuf<uint64_t> deg64(Vp + 1);
+    k_deg_sum<<<G(Vp + 1), kB, 0, s>>>(p.in_off.get(), cnt.get(), Vp, deg64.get(), deg32.get());
+    TG_CK(cudaGetLastError());
+    g.off.alloc(Vp + 1);
+    exclusive_scan_u64(deg64.get(), g.off.get(), Vp + 1, s);
+    const uint64_t n = d2h(g.off.get() + Vp, s);
+    g.col.alloc(std::max<uint64_t>(n, 1));
+    if (Vp) {
+      k_gh_local<<<G(Vp), kB, 0, s>>>(p.in_off.get(), p.in_col.get(), Vp, g.off.get(), g.col.get(),
+                                      cnt.get());  // cnt becomes the fill cursor
+      TG_CK(cudaGetLastError());
+    }
+    for (int q = 0; q < P; ++q) {
+      if (q == p.id) continue;
+      Part& Q = *by[q];
+      const uint64_t s0 = Q.obox_off[p.id], s1 = Q.obox_off[p.id + 1];
+      if (s1 == s0) continue;
+      const uint32_t* lid_by_slot = p.ibox_lid.get() + p.ibox_off[q] - s0;
+      k_gh_fill<<<G(s1 - s0), kB, 0, s>>>(Q.in_off.get(), Q.in_col.get(), Q.Vp, s0, s1, lid_by_slot,
+                                          Q.gh.pub_lid.get() + Q.gh.pub_off[p.id],
+                                          Q.gh.pub_off[p.id + 1] - Q.gh.pub_off[p.id],
+                                          (uint32_t)(Vp + g.gh_off[q]), g.off.get(), g.col.get(),
+                                          cnt.get());
+      TG_CK(cudaGetLastError());
+    }
+    sort_rows(g.off.get(), Vp, g.col.get(), nullptr, s);
+    // row classes of the ghost in-CSR
+    DevBuf<unsigned long long> c2(2);
+    TG_CK(cudaMemsetAsync(c2.get(), 0, 16, s));
+    DevBuf<uint32_t> lc(std::max<uint64_t>(Vp, 1)), lw(std::max<uint64_t>(Vp, 1));
+    k_class_list<<<G(Vp), kB, 0, s>>>(deg32.get(), Vp, kPrCta, 0xFFFFFFFFu, lc.get(), c2.get());
+    k_class_list<<<G(Vp), kB, 0, s>>>(deg32.get(), Vp, 32u, kPrCta, lw.get(), c2.get() + 1);
+    TG_CK(cudaGetLastError());
+    unsigned long long hc[2];
+    TG_CK(cudaMemcpyAsync(hc, c2.get(), 16, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaStreamSynchronize(s));
+    g.n_cta = hc[0];
+    g.n_warp = hc[1];
+    g.cta.alloc(std::max<uint64_t>(g.n_cta, 1));
+    g.warp.alloc(std::max<uint64_t>(g.n_warp, 1));
+    auto sort_list = [&](DevBuf<uint32_t>& src, DevBuf<uint32_t>& dst, uint64_t m) {
+      if (!m) return;
+      size_t tmp = 0;
+      TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, src.get(), dst.get(), (int)m, 0, 32, s));
+      DevBuf<uint8_t> t(tmp ? tmp : 1);
+      TG_CK(cub::DeviceRadixSort::SortKeys(t.get(), tmp, src.get(), dst.get(), (int)m, 0, 32, s));
+    };
+    sort_list(lc, g.cta, g.n_cta);
+    sort_list(lw, g.warp, g.n_warp);
+    TG_CK(cudaStreamSynchronize(s));
+    g.built = true;
+  }
 }
 
 }  // namespace tg

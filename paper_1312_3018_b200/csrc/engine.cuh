@@ -87,6 +87,23 @@ struct PRState {  // PageRank (local-id order)
   DevBuf<double> obox;  // partial sums per outbox slot (send)
 };
 
+// Ghost-pull PageRank (TOTEM_COMM_PULL):
+// instead of pushing per-target partial sums, every partition publishes the
+// contributions of its sources that have out-edges into a peer, into ghost
+// slots appended to the peer's contribution array, and each partition pulls
+// over a ghost-indexed in-CSR (local sources < Vp, ghost g at Vp + g).
+// Single-process engines; built on first use from the push layout.
+struct PRGhost {
+  bool built = false;
+  uint64_t G = 0;                          // ghost slots of this partition
+  std::vector<uint64_t> pub_off, gh_off;   // P+1 each: publish segments / ghost segments
+  DevBuf<uint32_t> pub_lid;                // local ids published to each peer, ascending
+  DevBuf<uint64_t> off;                    // Vp + 1
+  DevBuf<uint32_t> col;                    // local id, or Vp + ghost index
+  DevBuf<uint32_t> cta, warp;              // row classes (in-degree >= 2048 / 32..2047)
+  uint64_t n_cta = 0, n_warp = 0;
+};
+
 struct FrontierState {  // BFS / SSSP / BC-forward (messages arrive in Part::arena_fwd)
   DevBuf<uint32_t> cur, next, visited;            // bitmaps over local ids
   DevBuf<uint32_t> vals;                          // BFS level or SSSP dist (u32, Vp)
@@ -155,6 +172,7 @@ struct Part {
   DevBuf<int64_t> rin_delta;
   RemoteOut rin() const { return {rin_owner.get(), rin_arena.get(), rin_delta.get()}; }
   // algorithm state (lazily allocated)
+  PRGhost gh;       // ghost-pull PageRank layout (lazy)
   TileSched ts;     // tiles of the out-CSR
   TileSched ts_in;  // tiles of the in-CSR (BC backward push)
   FrontierState fs;
@@ -185,6 +203,7 @@ struct Engine {
   // the outbox + copy communication phase instead
   bool fused = true;
   bool peer_atomics = true;  // every peer GPU supports native atomics on its memory
+  int pr_comm = 0;           // TG_PR_PUSH (partial sums) or TG_PR_PULL (ghost contributions)
   std::vector<PeerView> peers;  // indexed by partition id (all P)
   uint64_t V = 0, E = 0;
   bool weighted = false, has_in = false;
@@ -239,6 +258,8 @@ struct EdgeInput {
   int scramble = 1;
 };
 void build_engine(Engine& eng, const EdgeInput& in);
+// ghost-pull PageRank layout of every hosted partition (single process; idempotent)
+void build_pr_ghost(Engine& eng);
 
 // Implemented per algorithm TU
 void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st);

@@ -181,27 +181,70 @@ __global__ void k_pr_finalize(const double* acc, const uint32_t* outdeg, uint64_
 // round's contributions, so with `concurrent` they run on fork/join side
 // streams: the long hub rows of k_pull_cta overlap the other classes instead
 // of leaving the GPU to their tail.
-void launch_pull(Engine& eng, Part& p, const float* contrib, const PullOut& o, bool concurrent) {
+// the in-CSR a pull walks: the push layout (rows [0, Vp + S)) or the
+// ghost-pull layout (rows [0, Vp), ghost sources at Vp + g)
+struct PullCsr {
+  const uint64_t* off;
+  const uint32_t* col;
+  const uint32_t* cta;
+  uint64_t n_cta;
+  const uint32_t* warp;
+  uint64_t n_warp;
+  uint64_t R;
+};
+PullCsr push_csr(const Part& p) {
+  return {p.in_off.get(), p.in_col.get(), p.pr_cta.get(), p.n_cta, p.pr_warp.get(), p.n_warp,
+          p.Vp + p.S};
+}
+PullCsr ghost_csr(const Part& p) {
+  const PRGhost& g = p.gh;
+  return {g.off.get(), g.col.get(), g.cta.get(), g.n_cta, g.warp.get(), g.n_warp, p.Vp};
+}
+
+// ghost-pull: p's published contributions -> q's ghost slots (Vq + gh_off[p] + k)
+__global__ void k_publish(const uint32_t* lid, uint64_t n, const float* src, float* dst) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += stride)
+    dst[k] = src[lid[k]];
+}
+
+void publish(Engine& eng, int buf) {
+  std::vector<Part*> by(eng.P, nullptr);
+  for (auto& pp : eng.parts) by[pp->id] = pp.get();
+  for (Part* p : by)
+    for (int q = 0; q < eng.P; ++q) {
+      const uint64_t n = q == p->id ? 0 : p->gh.pub_off[q + 1] - p->gh.pub_off[q];
+      if (!n) continue;
+      Part& Q = *by[q];
+      k_publish<<<grid_for(n, 256), 256, 0, eng.stream>>>(
+          p->gh.pub_lid.get() + p->gh.pub_off[q], n, p->pr.contrib[buf].get(),
+          Q.pr.contrib[buf].get() + Q.Vp + Q.gh.gh_off[p->id]);
+      eng.launches++;
+      eng.comm_bytes += n * sizeof(float);
+    }
+  TG_CK(cudaGetLastError());
+}
+
+void launch_pull(Engine& eng, const PullCsr& c, const float* contrib, const PullOut& o,
+                 bool concurrent) {
   cudaStream_t s = eng.stream, s_cta = s, s_warp = s;
   if (concurrent) {
     eng.fork();
     s_cta = eng.side[0];
     s_warp = eng.side[1];
   }
-  const uint64_t R = p.Vp + p.S;
-  if (p.n_cta) {
-    k_pull_cta<<<(unsigned)p.n_cta, kCtaThreads, 0, s_cta>>>(p.in_off.get(), p.in_col.get(),
-                                                             contrib, p.pr_cta.get(), o);
+  const uint64_t R = c.R;
+  if (c.n_cta) {
+    k_pull_cta<<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o);
     eng.launches++;
   }
-  if (p.n_warp) {
-    k_pull_warp<<<grid_for(p.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(
-        p.in_off.get(), p.in_col.get(), contrib, p.pr_warp.get(), p.n_warp, o);
+  if (c.n_warp) {
+    k_pull_warp<<<grid_for(c.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(c.off, c.col, contrib,
+                                                                            c.warp, c.n_warp, o);
     eng.launches++;
   }
   if (R) {
-    k_pull_thread<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(p.in_off.get(), p.in_col.get(),
-                                                               contrib, 0, R, o);
+    k_pull_thread<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
     eng.launches++;
   }
   if (concurrent) eng.join();
@@ -219,13 +262,19 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   TG_REQUIRE(out != nullptr || (eng.multi() && eng.rank != 0), TG_EINVAL,
              "tg_pagerank: NULL output");
   cudaStream_t s = eng.stream;
+  // ghost-pull (TG_PR_PULL, single process, P > 1): outside the timed region
+  const bool ghost = eng.pr_comm == TG_PR_PULL && eng.P > 1;
+  if (ghost) build_pr_ghost(eng);
   for (auto& pp : eng.parts) {
     Part& p = *pp;
     PRState& r = p.pr;
     const uint64_t Vn = std::max<uint64_t>(p.Vp, 1);
+    const uint64_t Cn = std::max<uint64_t>(p.Vp + (ghost ? p.gh.G : 0), 1);  // + ghost slots
+    if (r.contrib[0].n < Cn) {
+      r.contrib[0].alloc(Cn);
+      r.contrib[1].alloc(Cn);
+    }
     if (r.rank.n < Vn) {
-      r.contrib[0].alloc(Vn);
-      r.contrib[1].alloc(Vn);
       r.rank.alloc(Vn);
       if (eng.P > 1) {
         r.acc.alloc(Vn);
@@ -252,22 +301,29 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
                                                   p.pr.rank.get());
     eng.launches++;
   }
+  if (ghost) publish(eng, 0);
   int cur = 0;
   for (int it = 0; it < iters; ++it) {
     eng.prof_begin(TG_K_PR_PULL);
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       PRState& r = p.pr;
-      PullOut o{eng.P == 1, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
+      // P == 1 and ghost-pull: every in-edge is in the row, finalize in the pull
+      PullOut o{eng.P == 1 || ghost, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
                 r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, p.rout(), eng.fused, it & 1};
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
-      launch_pull(eng, p, r.contrib[cur].get(), o, concurrent);
+      launch_pull(eng, ghost ? ghost_csr(p) : push_csr(p), r.contrib[cur].get(), o, concurrent);
     }
     eng.prof_end(TG_K_PR_PULL);
+    if (ghost) {  // communication: contributions of boundary sources -> peers' ghosts
+      eng.prof_begin(TG_K_EXCHANGE);
+      if (it + 1 < iters) publish(eng, cur ^ 1);
+      eng.prof_end(TG_K_EXCHANGE);
+    }
     // pull: in_col 4 + contrib gather 4 per edge; in_off 8 + outdeg 4 + rank 4 +
     // next contrib 4 per row
     eng.prof_bytes(TG_K_PR_PULL, 8.0 * eng.E + 20.0 * eng.V);
-    if (eng.P > 1) {
+    if (eng.P > 1 && !ghost) {
       eng.prof_begin(TG_K_EXCHANGE);
       // fused: the pull wrote this round's sums into the owners' arenas (buffer
       // it & 1); one barrier per round orders them before the scatters, and the

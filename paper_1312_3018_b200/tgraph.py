@@ -160,6 +160,7 @@ def lib():
         L.tg_partition_size.restype = i32
         L.tg_engine_set_profiling.argtypes = [p, i32]
         L.tg_engine_set_exchange.argtypes = [p, i32]
+        L.tg_engine_set_pagerank_comm.argtypes = [p, i32]
         L.tg_engine_kernel_stat.argtypes = [p, i32, C.POINTER(tg_kernel_stat)]
         L.tg_kernel_name.argtypes = [i32]
         L.tg_kernel_name.restype = C.c_char_p
@@ -173,7 +174,7 @@ def lib():
         L.tg_rmat_edges.argtypes = [i32, i32, dbl, dbl, dbl, u64, i32, u64, u64, u64, p, p, p, i32]
         for f in ("tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
                   "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc",
-                  "tg_cc", "tg_engine_set_profiling", "tg_engine_set_exchange", "tg_engine_kernel_stat", "tg_graph_from_edges",
+                  "tg_cc", "tg_engine_set_profiling", "tg_engine_set_exchange", "tg_engine_set_pagerank_comm", "tg_engine_kernel_stat", "tg_graph_from_edges",
                   "tg_graph_load_edge_list", "tg_graph_info", "tg_graph_edges", "tg_engine_create",
                   "tg_rmat_edges"):
             getattr(L, f).restype = i32
@@ -390,6 +391,11 @@ def tg_engine_set_profiling(h, on: bool) -> None:
 
 
 TG_EXCHANGE_COPY, TG_EXCHANGE_FUSED = 0, 1
+TG_PR_PUSH, TG_PR_PULL = 0, 1
+
+
+def tg_engine_set_pagerank_comm(h, mode: int) -> None:
+    _check(lib().tg_engine_set_pagerank_comm(h, int(mode)))
 
 
 def tg_engine_set_exchange(h, mode: int) -> None:
@@ -464,6 +470,10 @@ class Engine:
 
     def kernel_stats(self):
         return tg_engine_kernel_stats(self.h)
+
+    def set_pagerank_comm(self, mode):
+        """TG_PR_PUSH (default) or TG_PR_PULL (tg_engine_set_pagerank_comm)."""
+        tg_engine_set_pagerank_comm(self.h, mode)
 
     def set_exchange(self, mode):
         """TG_EXCHANGE_FUSED (default) or TG_EXCHANGE_COPY (tg_engine_set_exchange)."""

@@ -81,6 +81,11 @@ def engine_worker(rank, world, port, scale, device, exchange=1):
     eng_g = tg.Engine.rmat(scale, rank=rank, world=world, comm=comm, device=device)
     srcs = [int(x) for x in inputs.list_sources(src, 4)]
     results = []
+    try:  # ghost-pull PageRank needs every partition in one process
+        eng_e.set_pagerank_comm(tg.TG_PR_PULL)
+        raise AssertionError("PULL accepted on a multi-process engine")
+    except tg.TGraphError as err:
+        assert err.code == 2  # TG_EINVAL
     for eng in (eng_e, eng_g):
         eng.set_exchange(exchange)
         pi = eng.partition_info(rank)

@@ -167,12 +167,45 @@ def test_exchange_modes_rmat13(tg, P, mode):
     assert st.comm_bytes > 0
 
 
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_pagerank_ghost_pull(tg, P):
+    """Ghost-pull PageRank (TOTEM_COMM_PULL, tg_engine_set_pagerank_comm):
+    boundary sources publish their contributions into the peers' ghost slots
+    and every partition pulls over its ghost-indexed in-CSR; same oracle
+    result as the push partial sums, repeated and interleaved with push."""
+    scale = 13
+    src, dst, _ = inputs.rmat_edges(scale)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst)
+    eng = tg.Engine.from_edges(V, src, dst, partitions=P, weighted=False)
+    for T in (1, 5, 6):
+        ref = G.pagerank(T)
+        eng.set_pagerank_comm(tg.TG_PR_PULL)
+        r_pull, st = eng.pagerank(T)
+        assert_pr(r_pull, ref)
+        assert T == 1 or st.comm_bytes > 0
+        eng.set_pagerank_comm(tg.TG_PR_PUSH)
+        assert_pr(eng.pagerank(T)[0], ref)
+    # a multigraph with self-loops, duplicates and isolated vertices
+    rng = np.random.default_rng(8)
+    V2 = 400
+    s2 = np.concatenate([rng.integers(0, 200, 3000), [5, 5, 7]]).astype(np.uint32)
+    d2 = np.concatenate([rng.integers(0, 200, 3000), [5, 9, 9]]).astype(np.uint32)
+    G2 = oracle.Graph(V2, s2, d2)
+    e2 = tg.Engine.from_edges(V2, s2, d2, partitions=P, weighted=False)
+    e2.set_pagerank_comm(tg.TG_PR_PULL)
+    assert_pr(e2.pagerank(5)[0], G2.pagerank(5))
+
+
 def test_set_exchange_rejects_unknown_mode(tg):
     from paper_1312_3018_b200 import tgraph
 
     eng = tg.Engine.rmat(8, partitions=2)
     with pytest.raises(tgraph.TGraphError) as e:
         eng.set_exchange(7)
+    assert e.value.code == tgraph.TG_EINVAL
+    with pytest.raises(tgraph.TGraphError) as e:
+        eng.set_pagerank_comm(7)
     assert e.value.code == tgraph.TG_EINVAL
 
 
