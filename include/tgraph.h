@@ -277,10 +277,11 @@ int tg_engine_set_exchange(tg_engine* eng, int mode);
  *   TG_PR_PULL: TOTEM_COMM_PULL -- each partition publishes the contribution
  *     of every source with an out-edge into a peer, into ghost slots appended
  *     to that peer's contribution array, and pulls over a ghost-indexed in-CSR
- *     (built on the first PULL run, outside the timed region).  Engines with
- *     all partitions in one process only.
+ *     (built on the first PULL run, outside the timed region; across
+ *     processes the publish stores go to CUDA-IPC-mapped peer buffers and the
+ *     build is collective: every rank must select the same mode, SPMD).
  * Results equal up to fp64 summation order (1e-5 relative per vertex).
- * TG_EINVAL for NULL, an unknown mode, or PULL on a multi-process engine. */
+ * TG_EINVAL for NULL or an unknown mode. */
 enum { TG_PR_PUSH = 0, TG_PR_PULL = 1 };
 int tg_engine_set_pagerank_comm(tg_engine* eng, int mode);
 int tg_engine_kernel_stat(const tg_engine* eng, int kernel_id, tg_kernel_stat* out);

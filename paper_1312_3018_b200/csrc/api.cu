@@ -724,10 +724,7 @@ int tg_engine_set_pagerank_comm(tg_engine* e, int mode) {
     TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");
     TG_REQUIRE(mode == TG_PR_PUSH || mode == TG_PR_PULL, TG_EINVAL,
                "tg_engine_set_pagerank_comm: unknown mode");
-    Engine& eng = *reinterpret_cast<Engine*>(e);
-    TG_REQUIRE(mode == TG_PR_PUSH || !eng.multi(), TG_EINVAL,
-               "tg_engine_set_pagerank_comm: PULL needs every partition in one process");
-    eng.pr_comm = mode;
+    reinterpret_cast<Engine*>(e)->pr_comm = mode;
   });
 }
 

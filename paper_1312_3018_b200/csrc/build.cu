@@ -952,19 +952,16 @@ void build_engine(Engine& eng, const EdgeInput& in) {
 }
 
 void build_pr_ghost(Engine& eng) {
-  TG_REQUIRE(!eng.multi(), TG_EINVAL,
-             "ghost-pull PageRank needs every partition in one process");
   TG_REQUIRE(eng.has_in, TG_EINVAL, "ghost-pull PageRank needs the in-CSR");
   bool all = true;
   for (auto& pp : eng.parts) all = all && pp->gh.built;
   if (all) return;
   cudaStream_t s = eng.stream;
   const int P = eng.P;
-  std::vector<Part*> by(P, nullptr);
-  for (auto& pp : eng.parts) by[pp->id] = pp.get();
-  // 1. publish lists: distinct sources of p's outbox rows for q, ascending
-  for (Part* pt : by) {
-    Part& p = *pt;
+  // 1. publish lists of the hosted partitions: distinct sources of p's outbox
+  //    rows for q, ascending
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
     PRGhost& g = p.gh;
     g.pub_off.assign(P + 1, 0);
     std::vector<DevBuf<uint32_t>> seg(P);
@@ -999,31 +996,84 @@ void build_pr_ghost(Engine& eng) {
                               cudaMemcpyDeviceToDevice, s));
     TG_CK(cudaStreamSynchronize(s));
   }
-  // 2. ghost segments of p: q's publish list for p
-  for (Part* pt : by) {
-    PRGhost& g = pt->gh;
-    g.gh_off.assign(P + 1, 0);
-    for (int q = 0; q < P; ++q)
-      g.gh_off[q + 1] = g.gh_off[q] + (q == pt->id ? 0 : by[q]->gh.pub_off[pt->id + 1] -
-                                                             by[q]->gh.pub_off[pt->id]);
-    g.G = g.gh_off[P];
-    TG_REQUIRE(pt->Vp + g.G < (1ull << 31), TG_ECAPACITY, "ghost index space exceeds 2^31");
+  // 2. a view of every partition: hosted ones directly, the others through
+  //    CUDA IPC (their in-CSR and publish list, read by the fill kernels below)
+  struct View {
+    uint64_t Vp = 0;
+    std::vector<uint64_t> obox_off, pub_off;
+    const uint64_t* in_off = nullptr;
+    const uint32_t* in_col = nullptr;
+    const uint32_t* pub_lid = nullptr;
+  };
+  std::vector<View> view(P);
+  std::vector<void*> build_maps;
+  for (auto& pp : eng.parts)
+    view[pp->id] = {pp->Vp, pp->obox_off, pp->gh.pub_off, pp->in_off.get(), pp->in_col.get(),
+                    pp->gh.pub_lid.get()};
+  struct Meta {
+    cudaIpcMemHandle_t h_off, h_col, h_pub;
+    uint64_t Vp;
+    uint64_t obox_off[TG_MAX_PARTITIONS + 1], pub_off[TG_MAX_PARTITIONS + 1];
+  };
+  if (eng.multi()) {
+    Part& me = *eng.parts[0];
+    Meta mine{};
+    TG_CK(cudaIpcGetMemHandle(&mine.h_off, me.in_off.get()));
+    TG_CK(cudaIpcGetMemHandle(&mine.h_col, me.in_col.get()));
+    TG_CK(cudaIpcGetMemHandle(&mine.h_pub, me.gh.pub_lid.get()));
+    mine.Vp = me.Vp;
+    for (int q = 0; q <= P; ++q) {
+      mine.obox_off[q] = me.obox_off[q];
+      mine.pub_off[q] = me.gh.pub_off[q];
+    }
+    std::vector<Meta> all(eng.world);
+    TG_REQUIRE(eng.comm.allgather(eng.comm.ctx, &mine, all.data(), sizeof(Meta)) == 0, TG_ENCCL,
+               "tg_comm.allgather failed");
+    for (int q = 0; q < eng.world; ++q) {
+      if (q == eng.rank) continue;
+      auto open = [&](const cudaIpcMemHandle_t& h) {
+        void* ptr = nullptr;
+        TG_CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        build_maps.push_back(ptr);
+        return ptr;
+      };
+      View& v = view[q];
+      v.Vp = all[q].Vp;
+      v.obox_off.assign(all[q].obox_off, all[q].obox_off + P + 1);
+      v.pub_off.assign(all[q].pub_off, all[q].pub_off + P + 1);
+      v.in_off = static_cast<const uint64_t*>(open(all[q].h_off));
+      v.in_col = static_cast<const uint32_t*>(open(all[q].h_col));
+      v.pub_lid = static_cast<const uint32_t*>(open(all[q].h_pub));
+    }
   }
-  // 3. ghost in-CSR of every partition: local entries + one ghost entry per
-  //    remote in-edge (u in q, v in p), from q's outbox rows for p
-  for (Part* pt : by) {
-    Part& p = *pt;
+  // size of r's publish list for q = q's ghost segment of r
+  auto pubsz = [&](int r, int q) -> uint64_t {
+    return r == q ? 0 : view[r].pub_off[q + 1] - view[r].pub_off[q];
+  };
+  auto gh_off_of = [&](int q, int r) -> uint64_t {  // q's ghost offset of r
+    uint64_t o = 0;
+    for (int x = 0; x < r; ++x) o += pubsz(x, q);
+    return o;
+  };
+  // 3. ghost in-CSR of the hosted partitions: local entries + one ghost entry
+  //    per remote in-edge (u in q, v in p), from q's outbox rows for p
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
     PRGhost& g = p.gh;
+    g.gh_off.assign(P + 1, 0);
+    for (int q = 0; q < P; ++q) g.gh_off[q + 1] = g.gh_off[q] + pubsz(q, p.id);
+    g.G = g.gh_off[P];
+    TG_REQUIRE(p.Vp + g.G < (1ull << 31), TG_ECAPACITY, "ghost index space exceeds 2^31");
     const uint64_t Vp = p.Vp;
     DevBuf<uint32_t> cnt(std::max<uint64_t>(Vp, 1)), deg32(std::max<uint64_t>(Vp, 1));
     TG_CK(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s));
     for (int q = 0; q < P; ++q) {
       if (q == p.id) continue;
-      Part& Q = *by[q];
+      const View& Q = view[q];
       const uint64_t s0 = Q.obox_off[p.id], s1 = Q.obox_off[p.id + 1];
       if (s1 == s0) continue;
       const uint32_t* lid_by_slot = p.ibox_lid.get() + p.ibox_off[q] - s0;
-      k_gh_count<<<G(s1 - s0), kB, 0, s>>>(Q.in_off.get(), Q.Vp, s0, s1, lid_by_slot, cnt.get());
+      k_gh_count<<<G(s1 - s0), kB, 0, s>>>(Q.in_off, Q.Vp, s0, s1, lid_by_slot, cnt.get());
     }
     DevBuf<uint64_t> deg64(Vp + 1);
     k_deg_sum<<<G(Vp + 1), kB, 0, s>>>(p.in_off.get(), cnt.get(), Vp, deg64.get(), deg32.get());
@@ -1039,13 +1089,12 @@ void build_pr_ghost(Engine& eng) {
     }
     for (int q = 0; q < P; ++q) {
       if (q == p.id) continue;
-      Part& Q = *by[q];
+      const View& Q = view[q];
       const uint64_t s0 = Q.obox_off[p.id], s1 = Q.obox_off[p.id + 1];
       if (s1 == s0) continue;
       const uint32_t* lid_by_slot = p.ibox_lid.get() + p.ibox_off[q] - s0;
-      k_gh_fill<<<G(s1 - s0), kB, 0, s>>>(Q.in_off.get(), Q.in_col.get(), Q.Vp, s0, s1, lid_by_slot,
-                                          Q.gh.pub_lid.get() + Q.gh.pub_off[p.id],
-                                          Q.gh.pub_off[p.id + 1] - Q.gh.pub_off[p.id],
+      k_gh_fill<<<G(s1 - s0), kB, 0, s>>>(Q.in_off, Q.in_col, Q.Vp, s0, s1, lid_by_slot,
+                                          Q.pub_lid + Q.pub_off[p.id], pubsz(q, p.id),
                                           (uint32_t)(Vp + g.gh_off[q]), g.off.get(), g.col.get(),
                                           cnt.get());
       TG_CK(cudaGetLastError());
@@ -1075,8 +1124,45 @@ void build_pr_ghost(Engine& eng) {
     sort_list(lc, g.cta, g.n_cta);
     sort_list(lw, g.warp, g.n_warp);
     TG_CK(cudaStreamSynchronize(s));
+    // contribution buffers [local | ghost slots]
+    const uint64_t Cn = std::max<uint64_t>(Vp + g.G, 1);
+    for (int b2 = 0; b2 < 2; ++b2)
+      if (p.pr.contrib[b2].n < Cn) p.pr.contrib[b2].alloc(Cn);
+  }
+  for (void* ptr : build_maps) cudaIpcCloseMemHandle(ptr);
+  // 4. publish destinations: q's contribution buffer + Vq + q's ghost offset of p
+  std::vector<float*> base[2];
+  base[0].assign(P, nullptr);
+  base[1].assign(P, nullptr);
+  for (auto& pp : eng.parts)
+    for (int b2 = 0; b2 < 2; ++b2) base[b2][pp->id] = pp->pr.contrib[b2].get();
+  if (eng.multi()) {
+    Part& me = *eng.parts[0];
+    struct CMeta {
+      cudaIpcMemHandle_t h[2];
+    } mine{};
+    for (int b2 = 0; b2 < 2; ++b2) TG_CK(cudaIpcGetMemHandle(&mine.h[b2], me.pr.contrib[b2].get()));
+    std::vector<CMeta> all(eng.world);
+    TG_REQUIRE(eng.comm.allgather(eng.comm.ctx, &mine, all.data(), sizeof(CMeta)) == 0, TG_ENCCL,
+               "tg_comm.allgather failed");
+    for (int q = 0; q < eng.world; ++q) {
+      if (q == eng.rank) continue;
+      for (int b2 = 0; b2 < 2; ++b2) {
+        void* ptr = nullptr;
+        TG_CK(cudaIpcOpenMemHandle(&ptr, all[q].h[b2], cudaIpcMemLazyEnablePeerAccess));
+        eng.peers[q].opened.push_back(ptr);  // closed with the engine
+        base[b2][q] = static_cast<float*>(ptr);
+      }
+    }
+  }
+  for (auto& pp : eng.parts) {
+    PRGhost& g = pp->gh;
+    for (int b2 = 0; b2 < 2; ++b2) {
+      g.pub_dst[b2].assign(P, nullptr);
+      for (int q = 0; q < P; ++q)
+        if (q != pp->id) g.pub_dst[b2][q] = base[b2][q] + view[q].Vp + gh_off_of(q, pp->id);
+    }
     g.built = true;
   }
 }
-
 }  // namespace tg

@@ -92,7 +92,8 @@ struct PRState {  // PageRank (local-id order)
 // contributions of its sources that have out-edges into a peer, into ghost
 // slots appended to the peer's contribution array, and each partition pulls
 // over a ghost-indexed in-CSR (local sources < Vp, ghost g at Vp + g).
-// Single-process engines; built on first use from the push layout.
+// Built on first use from the push layout (across processes through CUDA-IPC
+// views of the peers' in-CSR and publish lists).
 struct PRGhost {
   bool built = false;
   uint64_t G = 0;                          // ghost slots of this partition
@@ -102,6 +103,9 @@ struct PRGhost {
   DevBuf<uint32_t> col;                    // local id, or Vp + ghost index
   DevBuf<uint32_t> cta, warp;              // row classes (in-degree >= 2048 / 32..2047)
   uint64_t n_cta = 0, n_warp = 0;
+  // publish destinations per buffer and peer: q's contribution array (local
+  // pointer, or CUDA-IPC-mapped across processes) + Vq + q's ghost offset of p
+  std::vector<float*> pub_dst[2];
 };
 
 struct FrontierState {  // BFS / SSSP / BC-forward (messages arrive in Part::arena_fwd)
@@ -258,7 +262,8 @@ struct EdgeInput {
   int scramble = 1;
 };
 void build_engine(Engine& eng, const EdgeInput& in);
-// ghost-pull PageRank layout of every hosted partition (single process; idempotent)
+// ghost-pull PageRank layout of every hosted partition (collective across
+// processes; idempotent); also sizes PRState::contrib to Vp + G
 void build_pr_ghost(Engine& eng);
 
 // Implemented per algorithm TU

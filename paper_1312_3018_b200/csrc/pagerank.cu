@@ -208,21 +208,24 @@ __global__ void k_publish(const uint32_t* lid, uint64_t n, const float* src, flo
     dst[k] = src[lid[k]];
 }
 
+// one barrier per round across processes: the peers' ghost slots of buffer
+// `buf` were last read by their pull two rounds ago, which precedes their
+// previous publish and that round's barrier
 void publish(Engine& eng, int buf) {
-  std::vector<Part*> by(eng.P, nullptr);
-  for (auto& pp : eng.parts) by[pp->id] = pp.get();
-  for (Part* p : by)
+  for (auto& pp : eng.parts) {
+    Part& p = *pp;
     for (int q = 0; q < eng.P; ++q) {
-      const uint64_t n = q == p->id ? 0 : p->gh.pub_off[q + 1] - p->gh.pub_off[q];
+      const uint64_t n = q == p.id ? 0 : p.gh.pub_off[q + 1] - p.gh.pub_off[q];
       if (!n) continue;
-      Part& Q = *by[q];
-      k_publish<<<grid_for(n, 256), 256, 0, eng.stream>>>(
-          p->gh.pub_lid.get() + p->gh.pub_off[q], n, p->pr.contrib[buf].get(),
-          Q.pr.contrib[buf].get() + Q.Vp + Q.gh.gh_off[p->id]);
+      k_publish<<<grid_for(n, 256), 256, 0, eng.stream>>>(p.gh.pub_lid.get() + p.gh.pub_off[q], n,
+                                                           p.pr.contrib[buf].get(),
+                                                           p.gh.pub_dst[buf][q]);
       eng.launches++;
       eng.comm_bytes += n * sizeof(float);
     }
+  }
   TG_CK(cudaGetLastError());
+  fused_arrival(eng);  // processes: published values land before any pull reads them
 }
 
 void launch_pull(Engine& eng, const PullCsr& c, const float* contrib, const PullOut& o,
