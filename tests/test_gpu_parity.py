@@ -427,7 +427,8 @@ def test_c3_rmat26_pagerank_bc_partitions(tg):
     """BASELINE configs[2]: RMAT-26, PageRank (T = 5) and BC from sampled
     sources over 1, 2 and 4 degree-aware partitions (one B200 hosts all of
     them here; the multi-process path is the same partition code), full oracle.
-    Fused exchange by default; PageRank at P = 4 also through the copy path."""
+    Fused exchange by default; PageRank at P = 4 also through the copy path
+    and with ghost-pull communication."""
     scale = 26
     src, dst, _ = inputs.rmat_edges(scale)
     G = oracle.Graph(1 << scale, src, dst)
@@ -442,6 +443,9 @@ def test_c3_rmat26_pagerank_bc_partitions(tg):
             eng.set_exchange(tg.TG_EXCHANGE_COPY)
             assert_pr(eng.pagerank(5)[0], pr_ref)
             eng.set_exchange(tg.TG_EXCHANGE_FUSED)
+            eng.set_pagerank_comm(tg.TG_PR_PULL)   # ghost-pull at scale
+            assert_pr(eng.pagerank(5)[0], pr_ref)
+            eng.set_pagerank_comm(tg.TG_PR_PUSH)
         assert_bc(eng.bc(srcs)[0], bc_ref)
         eng.close()
 
