@@ -118,3 +118,28 @@ def test_full_cc_local_certificate(full):
     isolated = (full["outdeg"] == 0) & (full["indeg"] == 0)
     assert np.array_equal(cc[isolated], np.flatnonzero(isolated).astype(np.uint32))
     assert full["st_cc"].traversed_edges == full["E"]
+
+
+@pytest.mark.skipif(os.environ.get("TG_RMAT30") != "1",
+                    reason="RMAT-30 (2^34 edges, ~15 min of host certificate work): TG_RMAT30=1")
+def test_rmat30_bfs_certificate_one_gpu():
+    """BASELINE configs[4]'s graph (RMAT-30, 17.2 G edges) on ONE B200: an
+    out-CSR-only engine (no weights, no in-CSR: ~100 GB) runs top-down BFS from
+    the bench's first source; the exact streaming certificate over the
+    regenerated 2^34-edge stream proves every level."""
+    import paper_1312_3018_b200 as tg
+
+    scale = 30
+    V, E = 1 << scale, 16 << scale
+    eng = tg.Engine.rmat(scale, weighted=False, in_csr=False)
+    s = int(inputs.rmat_sources(scale, 1)[0])
+    lv, st = eng.bfs(s)
+    eng.close()
+    cert = oracle.StreamingCertificate(V, s, lv, weighted=False)
+    chunk = 1 << 28
+    for first in range(0, E, chunk):
+        src, dst, _ = inputs.rmat_edges(scale, first=first, count=min(chunk, E - first))
+        cert.feed(src, dst)
+    assert cert.holds()
+    print(f"RMAT-30 BFS: {st.device_ms:.1f} ms, supersteps {st.supersteps}, "
+          f"{st.traversed_edges / st.device_ms / 1e6:.1f} GTEPS")
