@@ -165,6 +165,68 @@ def test_certificates_accept_truth_reject_perturbations():
             assert not G.bfs_certify(s, bad)
 
 
+def _raised_tight(G_src, G_dst, G_w, truth, v):
+    """The largest value of truth[u] + w over v's reached in-edges: a value for v
+    that still has a tight in-edge (certificate condition 3 holds) but is longer
+    than the shortest path, so only condition 2 ("no edge has val[u] + w <
+    val[v]", SURVEY 8(c)) can reject it."""
+    m = (G_dst == v) & (truth[G_src] != INF32)
+    return int((truth[G_src[m]].astype(np.uint64) + G_w[m]).max()) if m.any() else None
+
+
+def test_certificates_reject_longer_tight_paths():
+    """Hand-worked: s->a (1), a->v (1), s->b (5), b->v (1).  dist[v] = 6 is tight
+    via b, so the tightness condition alone accepts it; the relaxation condition
+    (a->v gives 2 < 6) must reject it.  BFS analog: s->v, s->a, a->v with
+    level[v] = 2 (tight via a; the edge s->v gives 1 < 2).  Then the same raise
+    on random graphs, in-memory and streaming."""
+    s, a, b, v = 0, 1, 2, 3
+    src = np.array([s, a, s, b], np.uint32)
+    dst = np.array([a, v, b, v], np.uint32)
+    w = np.array([1, 1, 5, 1], np.uint32)
+    G = oracle.Graph(4, src, dst, w)
+    d = G.sssp(s)
+    assert list(d) == [0, 1, 5, 2]
+    assert G.sssp_certify(s, d)
+    bad = d.copy(); bad[v] = 6
+    assert not G.sssp_certify(s, bad)
+    cert = oracle.StreamingCertificate(4, s, bad, True)
+    cert.feed(src, dst, w)
+    assert not cert.holds()
+    bsrc = np.array([s, s, a], np.uint32)
+    bdst = np.array([v, a, v], np.uint32)
+    GB = oracle.Graph(4, bsrc, bdst)
+    lv = GB.bfs(s)
+    assert list(lv) == [0, 1, INF32, 1]
+    badl = lv.copy(); badl[v] = 2
+    assert not GB.bfs_certify(s, badl)
+    cert = oracle.StreamingCertificate(4, s, badl, False)
+    cert.feed(bsrc, bdst, np.ones(3, np.uint32))
+    assert not cert.holds()
+
+    rng = np.random.default_rng(12)
+    n = 400
+    src, dst = random_multigraph(rng, n, 3000)
+    w = rng.integers(1, 64, len(src)).astype(np.uint32)
+    G = oracle.Graph(n, src, dst, w)
+    ones = np.ones(len(src), np.uint32)
+    raised = 0
+    for s in (0, 9, 77):
+        for weighted, truth, ww in ((True, G.sssp(s), w), (False, G.bfs(s), ones)):
+            for v in np.where((truth != INF32) & (np.arange(n) != s))[0][:40]:
+                t = _raised_tight(src, dst, ww, truth, v)
+                if t is None or t <= int(truth[v]):
+                    continue
+                bad = truth.copy(); bad[v] = t
+                raised += 1
+                inmem = G.sssp_certify(s, bad) if weighted else G.bfs_certify(s, bad)
+                assert not inmem
+                cert = oracle.StreamingCertificate(n, s, bad, weighted)
+                cert.feed(src, dst, ww)
+                assert not cert.holds()
+    assert raised > 50
+
+
 # ------------------------------------------------------------------- PageRank
 D = 0.85
 
