@@ -71,6 +71,22 @@ typedef struct {
   int (*allreduce_u64)(void* ctx, uint64_t* data, int n, int op);
 } tg_comm;
 
+/* The library's node-local host collective (the per-superstep termination
+ * vote of P:208 and App. 1, whose shared `finished` flag lives in
+ * host memory): a POSIX shared-memory segment mapped by the `world` processes
+ * of one node.  Multi-process engines create one internally; these entry
+ * points expose the same object for tests and tools.
+ *   tg_hostcomm_create: collective over the ranks of `comm` (allgather of the
+ *     segment name + one barrier).  TG_ENCCL if a rank could not map it.
+ *   tg_hostcomm_allreduce_u64: in place over n <= 16 values; ops[i] 0 = sum
+ *     (mod 2^64), 1 = min.  Collective, same n and ops on every rank.
+ *     TG_ENCCL if a peer does not arrive within 600 s; TG_EINVAL for bad n.
+ * The segment's name is unlinked once every rank has mapped it. */
+typedef struct tg_hostcomm tg_hostcomm;
+int tg_hostcomm_create(const tg_comm* comm, int rank, int world, tg_hostcomm** out);
+int tg_hostcomm_allreduce_u64(tg_hostcomm* h, uint64_t* data, int n, const int* ops);
+void tg_hostcomm_free(tg_hostcomm* h);
+
 /* Engine attributes (the paper's totem_attr_t, re-aimed at GPUs).
  *   num_partitions: logical partitions hosted on this process's device, >= 1
  *       (world == 1 only).  Vertices are dealt to partitions by the
@@ -85,8 +101,22 @@ typedef struct {
  *       partition `rank` of `world` (num_partitions must be 1); every process
  *       makes the same calls in the same order (SPMD), results are written on
  *       rank 0 only (other ranks may pass NULL outputs).
- *   comm: required when world > 1 (copied; must outlive the engine).
- *   reserved: must be zero. */
+ *   comm: required when world > 1 (copied; must outlive the engine).  Used
+ *       at setup (IPC handle exchange) and, where a node-local shared-memory
+ *       segment cannot be created, for the per-superstep vote; normally the
+ *       per-superstep vote and arrival barrier run in the library's own
+ *       shared-memory collective (no callback on the per-superstep path).
+ *   strategy: how vertices are dealt to partitions (§6.2
+ *       lists HIGH / LOW / RAND; Fig. 4 compares against "naive
+ *       random-based" partitioning):
+ *       TG_PART_DEGREE (0, default): degree-aware serpentine deal above;
+ *       TG_PART_RANDOM (1): partition of v = serpentine deal of v's position in
+ *       a seeded pseudo-random order (tg_inputs.h mix64 of (part_seed, v);
+ *       equal vertex counts, degree-blind).  Under both strategies local ids
+ *       inside a partition are in out-degree order (desc, id asc).
+ *   part_seed: seed of TG_PART_RANDOM (ignored otherwise).
+ * TG_EINVAL for an unknown strategy. */
+enum { TG_PART_DEGREE = 0, TG_PART_RANDOM = 1 };
 typedef struct {
   int num_partitions;
   int device;
@@ -95,7 +125,8 @@ typedef struct {
   int rank;
   int world;
   const tg_comm* comm;
-  int reserved[2];
+  int strategy;
+  int part_seed;
 } tg_attr;
 
 /* Build an engine from an explicit directed edge list (duplicates and
@@ -167,6 +198,10 @@ typedef struct {
   int weighted, has_in_csr;
   uint64_t device_bytes;     /* bytes of device memory held by the engine */
   uint64_t build_ms;         /* wall time of the build, milliseconds       */
+  int device;                /* CUDA device ordinal of this process's partition(s) */
+  int strategy;              /* TG_PART_DEGREE / TG_PART_RANDOM                */
+  int exchange;              /* current TG_EXCHANGE_* transport                */
+  int pr_comm;               /* current TG_PR_* PageRank communication         */
 } tg_info;
 int tg_engine_info(const tg_engine* eng, tg_info* info);
 
@@ -187,7 +222,19 @@ int tg_engine_partition_info(const tg_engine* eng, int p, tg_part_info* info, ui
  * BFS/SSSP = sum of out-degrees of reached vertices; BC = 2x that per source;
  * PageRank = |E| x iterations.  supersteps: BSP rounds executed.
  * algorithmic_bytes: DESIGN.md §Roofline count for the run.  comm_bytes:
- * inbox/outbox message bytes moved between partitions.  launches: kernels. */
+ * inbox/outbox message bytes moved between partitions.  launches: kernels.
+ * relaxations: edges the compute kernels examined (SSSP: every relaxation,
+ * repeats included, so relaxations / traversed_edges is Bellman-Ford's
+ * redundancy; BFS/BC: out-edges expanded plus in-edges scanned bottom-up;
+ * PageRank: |E| x iterations).
+ * The phase split of SURVEY 8(d) (compute / exchange / vote):
+ *   exchange_ms: communication phase (arrival or copies + scatter), summed
+ *     CUDA-event intervals -- filled only while the kernel ledger is on
+ *     (tg_engine_set_profiling), else 0;
+ *   compute_ms: the compute kernels' ledger time (same condition);
+ *   vote_ms: host wall time of the termination votes after the stream has
+ *     drained (device->host read of the counters + the cross-process
+ *     reduction), always filled. */
 typedef struct {
   double device_ms;
   uint64_t supersteps;
@@ -195,6 +242,8 @@ typedef struct {
   uint64_t algorithmic_bytes;
   uint64_t comm_bytes;
   uint64_t launches;
+  uint64_t relaxations;
+  double compute_ms, exchange_ms, vote_ms;
 } tg_stats;
 
 /* Level-synchronous BFS (Fig. 11; App. 1).  levels[v] =

@@ -18,6 +18,7 @@ _LIB = None
 RMAT_A, RMAT_B, RMAT_C = 0.57, 0.19, 0.19
 EDGE_FACTOR = 16
 GRAPH_SEED, WEIGHT_SEED, SOURCE_SEED = 1, 2, 3
+PART_SEED = 4  # TG_PART_RANDOM draw (tg_attr.part_seed default of the binding)
 
 
 def lib():
@@ -41,6 +42,8 @@ def lib():
         L.tgin_list_sources.restype = i32
         L.tgin_scramble_one.argtypes = [C.c_uint32, i32, u64]
         L.tgin_scramble_one.restype = C.c_uint32
+        L.tgin_part_keys.argtypes = [u64, u64, p32]
+        L.tgin_part_keys.restype = i32
         _LIB = L
     return _LIB
 
@@ -94,3 +97,11 @@ def list_sources(src: np.ndarray, k: int, sseed: int = SOURCE_SEED) -> np.ndarra
 
 def scramble_one(x: int, scale: int, seed: int = GRAPH_SEED) -> int:
     return int(lib().tgin_scramble_one(x, scale, seed))
+
+
+def part_keys(V: int, pseed: int = PART_SEED) -> np.ndarray:
+    """Sort keys of the TG_PART_RANDOM draw (tgin_part_key) for vertices [0, V)."""
+    out = np.empty(V, np.uint32)
+    if lib().tgin_part_keys(pseed, V, _ptr(out)) != 0:
+        raise ValueError("tgin_part_keys")
+    return out

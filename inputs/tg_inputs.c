@@ -61,3 +61,10 @@ int tgin_list_sources(uint64_t E, const uint32_t* src, uint64_t sseed, uint64_t 
 uint32_t tgin_scramble_one(uint32_t x, int scale, uint64_t seed) {
   return tgin_scramble(x, scale, seed);
 }
+
+/* Keys of the TG_PART_RANDOM partitioning draw for vertices [0, V). */
+int tgin_part_keys(uint64_t pseed, uint64_t V, uint32_t* out) {
+  if (V && !out) return TGIN_EINVAL;
+  for (uint64_t v = 0; v < V; ++v) out[v] = tgin_part_key(pseed, v);
+  return TGIN_OK;
+}

@@ -33,6 +33,7 @@ def lib():
         L.oracle_pagerank.argtypes = [u64, p, p, i32, dbl, p]
         L.oracle_bc.argtypes = [u64, p, p, p, i32, p]
         L.oracle_partition.argtypes = [u64, p, i32, p, p]
+        L.oracle_partition_random.argtypes = [u64, p, i32, p, p, p]
         L.oracle_beta.argtypes = [u64, u64, p, p, p, i32, p, p, p]
         L.oracle_bfs_certify.argtypes = [u64, p, p, u64, p, p]
         L.oracle_sssp_certify.argtypes = [u64, p, p, p, u64, p, p]
@@ -45,7 +46,7 @@ def lib():
         L.oracle_cc_edges.argtypes = [u64, p, u64, p, p]
         L.oracle_cc_finish.argtypes = [u64, p, p]
         for f in ("oracle_csr", "oracle_bfs", "oracle_sssp", "oracle_pagerank", "oracle_bc",
-                  "oracle_partition", "oracle_beta", "oracle_bfs_certify",
+                  "oracle_partition", "oracle_partition_random", "oracle_beta", "oracle_bfs_certify",
                   "oracle_sssp_certify", "oracle_outdeg_edges", "oracle_bfs_cert_edges",
                   "oracle_sssp_cert_edges", "oracle_cert_finish", "oracle_pr_sample_edges",
                   "oracle_cc", "oracle_cc_edges", "oracle_cc_finish"):
@@ -119,6 +120,15 @@ class Graph:
         local = np.empty(self.V, np.uint32)
         _check(lib().oracle_partition(self.V, _p(self.row_off), P, _p(part), _p(local)),
                "oracle_partition")
+        return part, local
+
+    def partition_random(self, P: int, key):
+        """RAND partitioning (oracle_partition_random); key = inputs.part_keys(V, seed)."""
+        key = np.ascontiguousarray(key, np.uint32)
+        part = np.empty(self.V, np.uint32)
+        local = np.empty(self.V, np.uint32)
+        _check(lib().oracle_partition_random(self.V, _p(self.row_off), P, _p(key), _p(part),
+                                             _p(local)), "oracle_partition_random")
         return part, local
 
     def bfs_certify(self, s: int, level) -> bool:

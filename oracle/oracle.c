@@ -269,6 +269,37 @@ int oracle_partition(uint64_t V, const uint64_t* row_off, int P, uint32_t* part,
   return OK;
 }
 
+static const uint32_t* g_cmp_key;
+static int cmp_key_asc(const void* a, const void* b) {
+  const uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+  if (g_cmp_key[x] != g_cmp_key[y]) return g_cmp_key[x] < g_cmp_key[y] ? -1 : 1;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+int oracle_partition_random(uint64_t V, const uint64_t* row_off, int P, const uint32_t* key,
+                            uint32_t* part, uint32_t* local) {
+  if (P < 1 || !row_off || (V && (!part || !local || !key))) return EINVAL_;
+  uint32_t* order = (uint32_t*)malloc((V ? V : 1) * sizeof(uint32_t));
+  uint64_t* next = (uint64_t*)calloc((size_t)P, sizeof(uint64_t));
+  if (!order || !next) { free(order); free(next); return ENOMEM_; }
+  /* 1. partition = serpentine deal of the position in (key, id) order */
+  for (uint64_t v = 0; v < V; ++v) order[v] = (uint32_t)v;
+  g_cmp_key = key;
+  qsort(order, V, sizeof(uint32_t), cmp_key_asc);
+  for (uint64_t i = 0; i < V; ++i) {
+    const uint64_t r = i / (uint64_t)P, j = i % (uint64_t)P;
+    part[order[i]] = (uint32_t)((r % 2 == 0) ? j : (uint64_t)P - 1 - j);
+  }
+  /* 2. local ids: out-degree desc, id asc, counted per partition */
+  for (uint64_t v = 0; v < V; ++v) order[v] = (uint32_t)v;
+  g_cmp_row_off = row_off;
+  qsort(order, V, sizeof(uint32_t), cmp_deg_desc);
+  for (uint64_t i = 0; i < V; ++i) local[order[i]] = (uint32_t)next[part[order[i]]]++;
+  free(order);
+  free(next);
+  return OK;
+}
+
 int oracle_beta(uint64_t V, uint64_t E, const uint32_t* src, const uint32_t* dst,
                 const uint32_t* part, int P, double* beta_raw, double* beta_reduced,
                 uint64_t* slots) {

@@ -78,6 +78,15 @@ int oracle_cc_finish(uint64_t V, uint32_t* parent, uint32_t* label);
  * j = i % P, part = (r even ? j : P-1-j), local id = r. */
 int oracle_partition(uint64_t V, const uint64_t* row_off, int P, uint32_t* part, uint32_t* local);
 
+/* The "naive random-based" partitioning the paper compares against
+ * (§3.4, Fig. 4; RAND of P:427): vertices ordered by a random key
+ * (key[v], ties by id), position i dealt serpentine as above (equal vertex
+ * counts, degree-blind); inside each partition the local ids follow out-degree
+ * desc, id asc (the same local order as the degree-aware rule).  key[] is the
+ * seeded draw of inputs/tg_inputs.h (tgin_part_key), passed in. */
+int oracle_partition_random(uint64_t V, const uint64_t* row_off, int P, const uint32_t* key,
+                            uint32_t* part, uint32_t* local);
+
 /* Boundary statistics (§3.4): beta_raw = cross-partition
  * edges / |E|; beta_reduced = distinct (part(src), dst) pairs with
  * part(dst) != part(src), / |E|.  slots (nullable, P*P, row-major [p][q]):

@@ -10,6 +10,8 @@ from .tgraph import (  # noqa: F401
     TG_INF32,
     TG_PR_PULL,
     TG_PR_PUSH,
+    TG_PART_DEGREE,
+    TG_PART_RANDOM,
     TG_MEM_DEVICE,
     TG_MEM_HOST,
     Engine,
@@ -17,6 +19,7 @@ from .tgraph import (  # noqa: F401
     Stats,
     TGraphError,
     TorchComm,
+    HostComm,
     tg_partition_size,
     lib,
     tg_bc,

@@ -1,5 +1,6 @@
 // api.cu -- the extern "C" boundary (include/tgraph.h) plus engine-wide helpers:
 // message exchange between partitions, result collection, statistics.
+#include <chrono>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -80,10 +81,36 @@ void ensure_frontier_state(Engine& eng) {
   }
 }
 
+// ops[i]: 0 sum, 1 min.  The shared-memory collective when the engine has
+// one (one round trip for mixed ops), else one callback per op kind.
+static void comm_allreduce_mixed(Engine& eng, uint64_t* data, int n, const int* ops) {
+  if (!eng.multi()) return;
+  if (eng.hc) {
+    TG_REQUIRE(eng.hc->allreduce(data, n, ops), TG_ENCCL,
+               "host collective: a peer process did not arrive within 600 s");
+    return;
+  }
+  for (int op = 0; op < 2; ++op) {
+    uint64_t tmp[16];
+    int idx[16], m = 0;
+    for (int i = 0; i < n; ++i)
+      if (ops[i] == op) {
+        idx[m] = i;
+        tmp[m++] = data[i];
+      }
+    if (!m) continue;
+    TG_REQUIRE(eng.comm.allreduce_u64(eng.comm.ctx, tmp, m, op) == 0, TG_ENCCL,
+               "tg_comm.allreduce_u64 failed");
+    for (int j = 0; j < m; ++j) data[idx[j]] = tmp[j];
+  }
+}
+
 void comm_allreduce(Engine& eng, uint64_t* data, int n, int op) {
   if (!eng.multi()) return;
-  TG_REQUIRE(eng.comm.allreduce_u64(eng.comm.ctx, data, n, op) == 0, TG_ENCCL,
-             "tg_comm.allreduce_u64 failed");
+  TG_REQUIRE(n >= 0 && n <= 16, TG_EINTERNAL, "comm_allreduce: n > 16");
+  int ops[16];
+  for (int i = 0; i < n; ++i) ops[i] = op;
+  comm_allreduce_mixed(eng, data, n, ops);
 }
 
 void comm_barrier(Engine& eng) {
@@ -170,6 +197,10 @@ unsigned long long read_counts(Engine& eng, int idx) {
 
 Vote read_vote(Engine& eng) {
   const int P = (int)eng.parts.size();
+  // the superstep's kernels drain first; vote_ms counts only the vote itself
+  // (counter read + cross-process reduction)
+  TG_CK(cudaStreamSynchronize(eng.stream));
+  const auto t0 = std::chrono::steady_clock::now();
   for (int i = 0; i < P; ++i)
     TG_CK(cudaMemcpyAsync(eng.h_counts + 6 * i, eng.parts[i]->fs.counters.get(), 48,
                           cudaMemcpyDeviceToHost, eng.stream));
@@ -183,16 +214,17 @@ Vote read_vote(Engine& eng) {
     v.indegsum += eng.h_counts[6 * i + 3];
     v.minval = std::min<unsigned long long>(v.minval, eng.h_counts[6 * i + 5]);
   }
-  if (eng.multi()) {  // the global vote: sums + the minimum, over all ranks
-    uint64_t s4[4] = {v.count, v.edges, v.degsum, v.indegsum}, mn = v.minval;
-    comm_allreduce(eng, s4, 4, 0);
-    comm_allreduce(eng, &mn, 1, 1);
-    v.count = s4[0];
-    v.edges = s4[1];
-    v.degsum = s4[2];
-    v.indegsum = s4[3];
-    v.minval = mn;
+  if (eng.multi()) {  // the global vote: sums + the minimum, one reduction
+    uint64_t x[5] = {v.count, v.edges, v.degsum, v.indegsum, v.minval};
+    static const int ops[5] = {0, 0, 0, 0, 1};
+    comm_allreduce_mixed(eng, x, 5, ops);
+    v.count = x[0];
+    v.edges = x[1];
+    v.degsum = x[2];
+    v.indegsum = x[3];
+    v.minval = x[4];
   }
+  eng.vote_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return v;
 }
 
@@ -496,7 +528,10 @@ static void init_engine(Engine& eng, const tg_attr* attr) {
   TG_REQUIRE(attr->num_partitions >= 1, TG_EINVAL, "num_partitions must be >= 1");
   TG_REQUIRE(attr->num_partitions <= TG_MAX_PARTITIONS, TG_ECAPACITY,
              "num_partitions > TG_MAX_PARTITIONS");
-  for (int r : attr->reserved) TG_REQUIRE(r == 0, TG_EINVAL, "tg_attr.reserved must be zero");
+  TG_REQUIRE(attr->strategy == TG_PART_DEGREE || attr->strategy == TG_PART_RANDOM, TG_EINVAL,
+             "tg_attr.strategy: unknown partitioning strategy");
+  eng.strategy = attr->strategy;
+  eng.part_seed = (uint32_t)attr->part_seed;
   const int world = attr->world < 1 ? 1 : attr->world;
   TG_REQUIRE(world <= TG_MAX_PARTITIONS, TG_ECAPACITY, "world > TG_MAX_PARTITIONS");
   if (world > 1) {
@@ -506,6 +541,22 @@ static void init_engine(Engine& eng, const tg_attr* attr) {
     TG_REQUIRE(attr->comm && attr->comm->allgather && attr->comm->allreduce_u64, TG_EINVAL,
                "world > 1 requires tg_attr.comm with allgather and allreduce_u64");
     eng.comm = *attr->comm;
+  }
+  if (world > 1 && !(std::getenv("TG_HOSTCOMM") && std::getenv("TG_HOSTCOMM")[0] == '0')) {
+    Engine* e = &eng;
+    e->rank = attr->rank;
+    e->world = world;
+    eng.hc = HostComm::create(
+        attr->rank, world,
+        [e](const void* send, void* recv, uint64_t bytes) {
+          TG_REQUIRE(e->comm.allgather(e->comm.ctx, send, recv, bytes) == 0, TG_ENCCL,
+                     "tg_comm.allgather failed");
+        },
+        [e]() {
+          uint64_t x = 0;
+          TG_REQUIRE(e->comm.allreduce_u64(e->comm.ctx, &x, 1, 0) == 0, TG_ENCCL,
+                     "tg_comm.allreduce_u64 failed");
+        });
   }
   eng.rank = world > 1 ? attr->rank : 0;
   eng.world = world;
@@ -538,6 +589,40 @@ static void init_engine(Engine& eng, const tg_attr* attr) {
     }
   }
 }
+
+// SPMD check: every rank must run an algorithm with the same
+// exchange transport and PageRank communication, or their barrier counts
+// and message layouts disagree.  One small reduction per algorithm call.
+static void agree_settings(Engine& eng) {
+  if (!eng.multi()) return;
+  uint64_t x[2] = {eng.fused ? 1ull : 0ull, (uint64_t)eng.pr_comm};
+  comm_allreduce(eng, x, 2, 0);
+  const uint64_t w = (uint64_t)eng.world;
+  TG_REQUIRE((x[0] == 0 || x[0] == w) && (x[1] == 0 || x[1] == w), TG_EINVAL,
+             "ranks disagree on the exchange transport or the PageRank communication "
+             "(tg_engine_set_exchange / tg_engine_set_pagerank_comm must be called on every rank)");
+}
+
+// compute / exchange split of one call from the kernel ledger (profiling on)
+struct RunLedger {
+  Engine& eng;
+  double ms0[TG_K_COUNT];
+  explicit RunLedger(Engine& e) : eng(e) {
+    eng.prof_flush();
+    for (int k = 0; k < TG_K_COUNT; ++k) ms0[k] = eng.kstat[k].ms;
+    eng.vote_ms = 0;
+  }
+  void fill(tg_stats* st) {
+    eng.prof_flush();
+    st->vote_ms = eng.vote_ms;
+    if (!eng.prof) return;
+    for (int k = 0; k < TG_K_COUNT; ++k) {
+      const double d = eng.kstat[k].ms - ms0[k];
+      if (k == TG_K_EXCHANGE) st->exchange_ms += d;
+      else st->compute_ms += d;
+    }
+  }
+};
 
 }  // namespace tg
 
@@ -641,6 +726,10 @@ int tg_engine_info(const tg_engine* e, tg_info* info) {
     info->has_in_csr = eng->has_in;
     info->device_bytes = eng->device_bytes();
     info->build_ms = eng->build_ms;
+    info->device = eng->device;
+    info->strategy = eng->strategy;
+    info->exchange = eng->fused ? TG_EXCHANGE_FUSED : TG_EXCHANGE_COPY;
+    info->pr_comm = eng->pr_comm;
   });
 }
 
@@ -664,35 +753,45 @@ int tg_engine_partition_info(const tg_engine* e, int p, tg_part_info* info, uint
   });
 }
 
+// Every algorithm call: stats always computed (a NULL `stats` gets a local
+// one, so multi-process ranks run the same collectives whatever they pass),
+// the ranks' transport settings checked equal (SPMD), and the phase split
+// filled from the kernel ledger and the vote timer.
 #define TG_RUN(body)                                                     \
   return guard([&] {                                                     \
     TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");                  \
     Engine& eng = *reinterpret_cast<Engine*>(e);                         \
     TG_REQUIRE(mem == TG_MEM_HOST || mem == TG_MEM_DEVICE, TG_EINVAL, "bad mem kind"); \
     TG_CK(cudaSetDevice(eng.device));                                    \
-    if (st) std::memset(st, 0, sizeof(*st));                             \
+    tg_stats local_st;                                                   \
+    tg_stats* st = user_st ? user_st : &local_st;                        \
+    std::memset(st, 0, sizeof(*st));                                     \
+    agree_settings(eng);                                                 \
+    RunLedger led(eng);                                                  \
     body;                                                                \
+    led.fill(st);                                                        \
   })
 
 // NULL outputs are rejected inside run_* except on non-root ranks of a
 // multi-process engine (results are written on rank 0 only).
-int tg_bfs(tg_engine* e, uint64_t source, uint32_t* levels, int mem, tg_stats* st) {
+int tg_bfs(tg_engine* e, uint64_t source, uint32_t* levels, int mem, tg_stats* user_st) {
   TG_RUN({ run_bfs(eng, source, levels, mem, st); });
 }
 
-int tg_sssp(tg_engine* e, uint64_t source, uint32_t* dist, int mem, tg_stats* st) {
+int tg_sssp(tg_engine* e, uint64_t source, uint32_t* dist, int mem, tg_stats* user_st) {
   TG_RUN({ run_sssp(eng, source, dist, mem, st); });
 }
 
-int tg_cc(tg_engine* e, uint32_t* labels, int mem, tg_stats* st) {
+int tg_cc(tg_engine* e, uint32_t* labels, int mem, tg_stats* user_st) {
   TG_RUN({ run_cc(eng, labels, mem, st); });
 }
 
-int tg_pagerank(tg_engine* e, int iterations, double damping, float* rank, int mem, tg_stats* st) {
+int tg_pagerank(tg_engine* e, int iterations, double damping, float* rank, int mem,
+                tg_stats* user_st) {
   TG_RUN({ run_pagerank(eng, iterations, damping, rank, mem, st); });
 }
 
-int tg_bc(tg_engine* e, const uint64_t* sources, int k, double* bc, int mem, tg_stats* st) {
+int tg_bc(tg_engine* e, const uint64_t* sources, int k, double* bc, int mem, tg_stats* user_st) {
   TG_RUN({ run_bc(eng, sources, k, bc, mem, st); });
 }
 
@@ -735,6 +834,40 @@ int tg_engine_kernel_stat(const tg_engine* e, int kid, tg_kernel_stat* out) {
     *out = reinterpret_cast<const Engine*>(e)->kstat[kid];
   });
 }
+
+int tg_hostcomm_create(const tg_comm* comm, int rank, int world, tg_hostcomm** out) {
+  return guard([&] {
+    TG_REQUIRE(out != nullptr, TG_EINVAL, "NULL out");
+    *out = nullptr;
+    TG_REQUIRE(comm && comm->allgather && comm->allreduce_u64, TG_EINVAL, "bad tg_comm");
+    TG_REQUIRE(world >= 2 && world <= TG_MAX_PARTITIONS && rank >= 0 && rank < world, TG_EINVAL,
+               "rank / world out of range");
+    const tg_comm c = *comm;
+    auto hc = HostComm::create(
+        rank, world,
+        [c](const void* send, void* recv, uint64_t bytes) {
+          TG_REQUIRE(c.allgather(c.ctx, send, recv, bytes) == 0, TG_ENCCL, "tg_comm.allgather failed");
+        },
+        [c]() {
+          uint64_t x = 0;
+          TG_REQUIRE(c.allreduce_u64(c.ctx, &x, 1, 0) == 0, TG_ENCCL, "tg_comm.allreduce_u64 failed");
+        });
+    TG_REQUIRE(hc != nullptr, TG_ENCCL, "a rank could not map the shared-memory segment");
+    *out = reinterpret_cast<tg_hostcomm*>(hc.release());
+  });
+}
+
+int tg_hostcomm_allreduce_u64(tg_hostcomm* h, uint64_t* data, int n, const int* ops) {
+  return guard([&] {
+    TG_REQUIRE(h && (n == 0 || (data && ops)), TG_EINVAL, "NULL argument");
+    TG_REQUIRE(n >= 0 && n <= 16, TG_EINVAL, "n must be in [0, 16]");
+    for (int i = 0; i < n; ++i) TG_REQUIRE(ops[i] == 0 || ops[i] == 1, TG_EINVAL, "op must be 0 or 1");
+    TG_REQUIRE(reinterpret_cast<HostComm*>(h)->allreduce(data, n, ops), TG_ENCCL,
+               "host collective: a peer process did not arrive within 600 s");
+  });
+}
+
+void tg_hostcomm_free(tg_hostcomm* h) { delete reinterpret_cast<HostComm*>(h); }
 
 const char* tg_kernel_name(int kid) {
   static const char* names[TG_K_COUNT] = {"bfs_expand",  "sssp_expand", "bc_fwd_expand",

@@ -518,7 +518,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       !(std::getenv("TG_BC_PULL_CLASSES") && std::getenv("TG_BC_PULL_CLASSES")[0] == '0');
   uint32_t bc_priv = 512;  // RMAT-28 sweep: profiles/r01_bc_priv_sweep.txt
   if (const char* e = std::getenv("TG_BC_PRIV")) bc_priv = (uint32_t)std::strtoul(e, nullptr, 10);
-  uint64_t supersteps = 0, traversed = 0, bytes = 0, bm_bytes = 0;
+  uint64_t supersteps = 0, traversed = 0, bytes = 0, bm_bytes = 0, relax = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   for (int si = 0; si < k; ++si) {
     int ps;
@@ -650,6 +650,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
                        0, f.counters.get(), f.counters.get() + 2, f.counters.get() + 3);
       }
       const Vote v = read_vote(eng);
+      relax += v.edges;
       mf = v.degsum;
       explored += mf;
       lvl_out.push_back(v.degsum);
@@ -778,7 +779,9 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     }
     total_ms += time_end(eng);
     eng.l2_window(nullptr, 0);
-    eng.prof_bytes(TG_K_BCB_EXPAND, 4.0 * read_vote(eng).edges);
+    const uint64_t bwd_edges = read_vote(eng).edges;
+    relax += bwd_edges;
+    eng.prof_bytes(TG_K_BCB_EXPAND, 4.0 * bwd_edges);
     uint64_t nreached = 0;
     const uint64_t tr = reached_outdeg_bitmap(eng, &nreached);
     traversed += 2 * tr;
@@ -792,6 +795,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
   if (st) {
     st->device_ms = total_ms;
     st->supersteps = supersteps;
+    st->relaxations = relax;
     st->traversed_edges = traversed;
     st->algorithmic_bytes = bytes;
     st->comm_bytes = eng.comm_bytes;

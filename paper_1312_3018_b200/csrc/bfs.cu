@@ -248,6 +248,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
   if (st) {
     st->device_ms = ms;
     st->supersteps = supersteps;
+    st->relaxations = edges_total;
     uint64_t nreached = 0;
     st->traversed_edges = reached_outdeg_u32(eng, &nreached);
     TG_REQUIRE(bu_steps || st->traversed_edges == edges_total, TG_EINTERNAL,

@@ -264,6 +264,43 @@ __global__ void k_outdeg_local(const uint64_t* row_off, uint64_t Vp, uint32_t* o
     outdeg[i] = (uint32_t)(row_off[i + 1] - row_off[i]);
 }
 
+// ---- TG_PART_RANDOM (the "naive random-based" partitioning of P:178) ----
+__global__ void k_iota(uint64_t V, uint32_t* ids) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V; v += stride)
+    ids[v] = (uint32_t)v;
+}
+__global__ void k_part_keys(uint64_t V, uint32_t pseed, uint32_t* keys, uint32_t* vals) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < V; v += stride) {
+    keys[v] = tgin_part_key(pseed, v);
+    vals[v] = (uint32_t)v;
+  }
+}
+// perm = vertices in (key, id) order; composite key of v = (partition << 32) |
+// ~outdeg, so a stable sort groups partitions and orders each by degree desc,
+// id asc (values start in id order)
+__global__ void k_part_composite(const uint32_t* perm, uint64_t V, int P, const uint32_t* outdeg,
+                                 unsigned long long* key) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += stride) {
+    int p;
+    uint32_t l;
+    deal(i, P, &p, &l);
+    const uint32_t v = perm[i];
+    key[v] = ((unsigned long long)p << 32) | (unsigned long long)(~outdeg[v]);
+  }
+}
+// sorted[start_p + l] = the vertex with local id l in p -> order position undeal(l, p)
+__global__ void k_part_order(const uint32_t* sorted, const unsigned long long* skey, uint64_t V, int P,
+                             const uint64_t* start, uint32_t* order) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < V; i += stride) {
+    const int p = (int)(skey[i] >> 32);
+    order[undeal((uint32_t)(i - start[p]), p, P)] = sorted[i];
+  }
+}
+
 template <typename T>
 T d2h(const T* p, cudaStream_t s) {
   T v;
@@ -915,8 +952,39 @@ void build_engine(Engine& eng, const EdgeInput& in) {
   }
   TG_REQUIRE(d2h(bad.get(), s) == 0, TG_EINVAL, "edge endpoint id >= V");
 
+  // order[i] = the vertex dealt from position i (deal(i) -> (partition, local id))
   DevBuf<uint32_t> order(V);
-  {
+  if (eng.strategy == TG_PART_RANDOM && eng.P > 1) {
+    TG_REQUIRE(V < (1ull << 31), TG_ECAPACITY, "sort: more than 2^31 items");
+    DevBuf<uint32_t> perm(V);
+    {
+      DevBuf<uint32_t> keys(V), keys_out(V), vals(V);
+      k_part_keys<<<G(V), kB, 0, s>>>(V, eng.part_seed, keys.get(), vals.get());
+      TG_CK(cudaGetLastError());
+      sort_pairs_u32(keys.get(), keys_out.get(), vals.get(), perm.get(), V, s);
+    }
+    DevBuf<unsigned long long> key(V), key_out(V);
+    DevBuf<uint32_t> ids(V), sorted(V);
+    k_part_composite<<<G(V), kB, 0, s>>>(perm.get(), V, eng.P, outdeg.get(), key.get());
+    k_iota<<<G(V), kB, 0, s>>>(V, ids.get());
+    TG_CK(cudaGetLastError());
+    size_t tmp = 0;
+    TG_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), key_out.get(), ids.get(),
+                                          sorted.get(), (int)V, 0, 64, s));
+    {
+      DevBuf<uint8_t> t(tmp ? tmp : 1);
+      TG_CK(cub::DeviceRadixSort::SortPairs(t.get(), tmp, key.get(), key_out.get(), ids.get(),
+                                            sorted.get(), (int)V, 0, 64, s));
+    }
+    std::vector<uint64_t> start(eng.P + 1, 0);
+    for (int p = 0; p < eng.P; ++p) start[p + 1] = start[p] + part_size(V, p, eng.P);
+    DevBuf<uint64_t> d_start(eng.P + 1);
+    TG_CK(cudaMemcpyAsync(d_start.get(), start.data(), (eng.P + 1) * 8, cudaMemcpyHostToDevice, s));
+    k_part_order<<<G(V), kB, 0, s>>>(sorted.get(), key_out.get(), V, eng.P, d_start.get(),
+                                     order.get());
+    TG_CK(cudaGetLastError());
+    TG_CK(cudaStreamSynchronize(s));
+  } else {
     DevBuf<uint32_t> keys(V), keys_out(V), vals(V);
     k_neg_iota<<<G(V), kB, 0, s>>>(outdeg.get(), V, keys.get(), vals.get());
     TG_CK(cudaGetLastError());

@@ -286,6 +286,7 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
   if (st) {
     st->device_ms = ms;
     st->supersteps = supersteps;
+    st->relaxations = processed;
     st->traversed_edges = eng.E;  // every input edge, once (undirected reading A29)
     st->algorithmic_bytes = 8 * processed + 40 * activations + 3 * bm_bytes * supersteps;
     st->comm_bytes = eng.comm_bytes;

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "hostcomm.h"
 
 namespace tg {
 
@@ -201,7 +202,13 @@ struct Engine {
   int P = 1;          // total partitions (world when multi-process)
   int rank = 0, world = 1;
   tg_comm comm{};
+  // node-local shared-memory collective (hostcomm.cu): the per-superstep vote
+  // and barriers of multi-process engines; nullptr -> the tg_comm callbacks
+  std::unique_ptr<HostComm> hc;
   bool multi() const { return world > 1; }
+  int strategy = TG_PART_DEGREE;
+  uint32_t part_seed = 0;
+  double vote_ms = 0;  // host time of the votes of the current run (tg_stats.vote_ms)
   // boundary messages written by the compute kernels into the owners' arenas
   // (RemoteOut) for BFS, SSSP, PageRank and BC; TG_FUSED_EXCHANGE=0 selects
   // the outbox + copy communication phase instead

@@ -365,6 +365,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   if (st) {
     st->device_ms = ms;
     st->supersteps = (uint64_t)iters;
+    st->relaxations = eng.E * (uint64_t)iters;
     st->traversed_edges = eng.E * (uint64_t)iters;
     // per iteration: 8 B per edge (in_col + contrib gather) + 20 B per vertex
     // (in_off 8, outdeg 4, rank 4, contrib 4) -- DESIGN.md "Roofline"

@@ -257,6 +257,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     uint64_t nreached = 0;
     st->device_ms = ms;
     st->supersteps = supersteps;
+    st->relaxations = relax;
     st->traversed_edges = reached_outdeg_u32(eng, &nreached);
     st->algorithmic_bytes = 12 * relax + 20 * activations + 2 * bm_bytes * supersteps;
     st->comm_bytes = eng.comm_bytes;

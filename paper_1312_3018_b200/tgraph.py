@@ -38,7 +38,7 @@ class tg_comm(C.Structure):
 class tg_attr(C.Structure):
     _fields_ = [("num_partitions", C.c_int), ("device", C.c_int), ("weighted", C.c_int),
                 ("build_in_csr", C.c_int), ("rank", C.c_int), ("world", C.c_int),
-                ("comm", C.POINTER(tg_comm)), ("reserved", C.c_int * 2)]
+                ("comm", C.POINTER(tg_comm)), ("strategy", C.c_int), ("part_seed", C.c_int)]
 
 
 _U64_MAX = (1 << 64) - 1
@@ -94,7 +94,8 @@ class TorchComm:
 class tg_info(C.Structure):
     _fields_ = [("V", C.c_uint64), ("E", C.c_uint64), ("num_partitions", C.c_int),
                 ("weighted", C.c_int), ("has_in_csr", C.c_int), ("device_bytes", C.c_uint64),
-                ("build_ms", C.c_uint64)]
+                ("build_ms", C.c_uint64), ("device", C.c_int), ("strategy", C.c_int),
+                ("exchange", C.c_int), ("pr_comm", C.c_int)]
 
 
 class tg_part_info(C.Structure):
@@ -105,7 +106,9 @@ class tg_part_info(C.Structure):
 class tg_stats(C.Structure):
     _fields_ = [("device_ms", C.c_double), ("supersteps", C.c_uint64),
                 ("traversed_edges", C.c_uint64), ("algorithmic_bytes", C.c_uint64),
-                ("comm_bytes", C.c_uint64), ("launches", C.c_uint64)]
+                ("comm_bytes", C.c_uint64), ("launches", C.c_uint64),
+                ("relaxations", C.c_uint64), ("compute_ms", C.c_double),
+                ("exchange_ms", C.c_double), ("vote_ms", C.c_double)]
 
 
 class tg_kernel_stat(C.Structure):
@@ -123,11 +126,14 @@ class Stats:
     algorithmic_bytes: int
     comm_bytes: int
     launches: int
+    relaxations: int = 0
+    compute_ms: float = 0.0
+    exchange_ms: float = 0.0
+    vote_ms: float = 0.0
 
     @staticmethod
     def of(s: tg_stats) -> "Stats":
-        return Stats(s.device_ms, s.supersteps, s.traversed_edges, s.algorithmic_bytes,
-                     s.comm_bytes, s.launches)
+        return Stats(*(getattr(s, f) for f, _ in tg_stats._fields_))
 
 
 _LIB = None
@@ -172,7 +178,11 @@ def lib():
         L.tg_graph_free.restype = None
         L.tg_engine_create.argtypes = [p, C.POINTER(tg_attr), C.POINTER(p)]
         L.tg_rmat_edges.argtypes = [i32, i32, dbl, dbl, dbl, u64, i32, u64, u64, u64, p, p, p, i32]
-        for f in ("tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
+        L.tg_hostcomm_create.argtypes = [C.POINTER(tg_comm), i32, i32, C.POINTER(p)]
+        L.tg_hostcomm_allreduce_u64.argtypes = [p, p, i32, p]
+        L.tg_hostcomm_free.argtypes = [p]
+        L.tg_hostcomm_free.restype = None
+        for f in ("tg_hostcomm_create", "tg_hostcomm_allreduce_u64", "tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
                   "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc",
                   "tg_cc", "tg_engine_set_profiling", "tg_engine_set_exchange", "tg_engine_set_pagerank_comm", "tg_engine_kernel_stat", "tg_graph_from_edges",
                   "tg_graph_load_edge_list", "tg_graph_info", "tg_graph_edges", "tg_engine_create",
@@ -197,17 +207,22 @@ def _arr(a, dtype):
     return arr.ctypes.data_as(C.c_void_p), TG_MEM_HOST, arr
 
 
-def _attr(partitions, device, weighted, in_csr, rank=0, world=1, comm=None) -> tg_attr:
+TG_PART_DEGREE, TG_PART_RANDOM = 0, 1
+
+
+def _attr(partitions, device, weighted, in_csr, rank=0, world=1, comm=None, strategy=TG_PART_DEGREE,
+          part_seed=4) -> tg_attr:
     at = tg_attr()
     at.num_partitions, at.device, at.weighted, at.build_in_csr = partitions, device, int(weighted), int(in_csr)
     at.rank, at.world = rank, world
+    at.strategy, at.part_seed = int(strategy), int(part_seed)
     if comm is not None:
         at.comm = C.pointer(comm.struct)
     return at
 
 
 def tg_engine_create_edges(V, src, dst, w=None, partitions=1, device=0, weighted=None, in_csr=True,
-                           rank=0, world=1, comm=None):
+                           rank=0, world=1, comm=None, strategy=TG_PART_DEGREE, part_seed=4):
     ps, ms, k1 = _arr(src, np.uint32)
     pd, md, k2 = _arr(dst, np.uint32)
     pw, mw, k3 = _arr(w, np.uint32)
@@ -216,7 +231,7 @@ def tg_engine_create_edges(V, src, dst, w=None, partitions=1, device=0, weighted
         raise ValueError("src and dst must live in the same memory")
     if weighted is None:
         weighted = w is not None
-    at = _attr(partitions, device, weighted, in_csr, rank, world, comm)
+    at = _attr(partitions, device, weighted, in_csr, rank, world, comm, strategy, part_seed)
     h = C.c_void_p()
     _check(lib().tg_engine_create_edges(V, E, ps, pd, pw, ms, C.byref(at), C.byref(h)))
     return h
@@ -224,8 +239,8 @@ def tg_engine_create_edges(V, src, dst, w=None, partitions=1, device=0, weighted
 
 def tg_engine_create_rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1, scramble=True,
                           wseed=2, partitions=1, device=0, weighted=True, in_csr=True, rank=0,
-                          world=1, comm=None):
-    at = _attr(partitions, device, weighted, in_csr, rank, world, comm)
+                          world=1, comm=None, strategy=TG_PART_DEGREE, part_seed=4):
+    at = _attr(partitions, device, weighted, in_csr, rank, world, comm, strategy, part_seed)
     h = C.c_void_p()
     _check(lib().tg_engine_create_rmat(scale, edge_factor, a, b, c, seed, int(scramble), wseed,
                                        C.byref(at), C.byref(h)))
@@ -305,10 +320,10 @@ class Graph:
 
 
 def tg_engine_create(graph: Graph, partitions=1, device=0, weighted=None, in_csr=True, rank=0, world=1,
-                     comm=None):
+                     comm=None, strategy=TG_PART_DEGREE, part_seed=4):
     if weighted is None:
         weighted = graph.weighted
-    at = _attr(partitions, device, weighted, in_csr, rank, world, comm)
+    at = _attr(partitions, device, weighted, in_csr, rank, world, comm, strategy, part_seed)
     h = C.c_void_p()
     _check(lib().tg_engine_create(graph.h, C.byref(at), C.byref(h)))
     return h
@@ -340,47 +355,62 @@ def tg_engine_partition_info(h, p: int, P: int) -> dict:
     return d
 
 
-def _out(out, V, dtype):
+def _out(out, V, dtype, device=None):
+    """Output array -> (out, pointer, mem kind).  The library writes V elements
+    of dtype's width, so a wrong width, a short, strided or foreign-device
+    buffer is rejected here instead of being written out of bounds."""
     if out is None:
         out = np.empty(V, dtype)
-    ptr, mem, keep = _arr(out, dtype) if not isinstance(out, np.ndarray) else (
-        out.ctypes.data_as(C.c_void_p), TG_MEM_HOST, out)
-    if isinstance(out, np.ndarray) and (out.dtype != dtype or not out.flags.c_contiguous or len(out) < V):
-        raise ValueError(f"output must be a contiguous {dtype} array of length >= V")
-    return out, ptr, mem
+    itemsize = np.dtype(dtype).itemsize
+    if isinstance(out, np.ndarray):
+        if out.dtype.itemsize != itemsize or out.dtype.kind != np.dtype(dtype).kind \
+                or not out.flags.c_contiguous or out.size < V or not out.flags.writeable:
+            raise ValueError(f"output must be a writeable contiguous {np.dtype(dtype)} array "
+                             f"of length >= V ({V})")
+        return out, out.ctypes.data_as(C.c_void_p), TG_MEM_HOST
+    if hasattr(out, "data_ptr"):  # torch tensor (host or device)
+        if out.element_size() != itemsize or out.numel() < V or not out.is_contiguous():
+            raise ValueError(f"output tensor must be contiguous with {itemsize}-byte elements "
+                             f"and >= V ({V}) elements")
+        if getattr(out, "is_cuda", False):
+            if device is not None and out.device.index != device:
+                raise ValueError(f"output tensor on cuda:{out.device.index}, engine on cuda:{device}")
+            return out, C.c_void_p(out.data_ptr()), TG_MEM_DEVICE
+        return out, C.c_void_p(out.data_ptr()), TG_MEM_HOST
+    raise TypeError("output must be a numpy array or a torch tensor")
 
 
-def tg_bfs(h, V, source, out=None):
-    out, ptr, mem = _out(out, V, np.uint32)
+def tg_bfs(h, V, source, out=None, device=None):
+    out, ptr, mem = _out(out, V, np.uint32, device)
     st = tg_stats()
     _check(lib().tg_bfs(h, source, ptr, mem, C.byref(st)))
     return out, Stats.of(st)
 
 
-def tg_sssp(h, V, source, out=None):
-    out, ptr, mem = _out(out, V, np.uint32)
+def tg_sssp(h, V, source, out=None, device=None):
+    out, ptr, mem = _out(out, V, np.uint32, device)
     st = tg_stats()
     _check(lib().tg_sssp(h, source, ptr, mem, C.byref(st)))
     return out, Stats.of(st)
 
 
-def tg_pagerank(h, V, iterations=5, damping=0.85, out=None):
-    out, ptr, mem = _out(out, V, np.float32)
+def tg_pagerank(h, V, iterations=5, damping=0.85, out=None, device=None):
+    out, ptr, mem = _out(out, V, np.float32, device)
     st = tg_stats()
     _check(lib().tg_pagerank(h, iterations, damping, ptr, mem, C.byref(st)))
     return out, Stats.of(st)
 
 
-def tg_bc(h, V, sources, out=None):
-    out, ptr, mem = _out(out, V, np.float64)
+def tg_bc(h, V, sources, out=None, device=None):
+    out, ptr, mem = _out(out, V, np.float64, device)
     s = np.ascontiguousarray(sources, np.uint64)
     st = tg_stats()
     _check(lib().tg_bc(h, s.ctypes.data_as(C.c_void_p), len(s), ptr, mem, C.byref(st)))
     return out, Stats.of(st)
 
 
-def tg_cc(h, V, out=None):
-    out, ptr, mem = _out(out, V, np.uint32)
+def tg_cc(h, V, out=None, device=None):
+    out, ptr, mem = _out(out, V, np.uint32, device)
     st = tg_stats()
     _check(lib().tg_cc(h, ptr, mem, C.byref(st)))
     return out, Stats.of(st)
@@ -422,6 +452,7 @@ class Engine:
         self.rank = rank
         inf = tg_engine_info(handle)
         self.V, self.E, self.P = inf["V"], inf["E"], inf["num_partitions"]
+        self.device = inf["device"]
         self.info = inf
 
     @classmethod
@@ -451,19 +482,19 @@ class Engine:
         return tg_engine_partition_info(self.h, p, self.P)
 
     def bfs(self, source, out=None):
-        return tg_bfs(self.h, self.V, source, out)
+        return tg_bfs(self.h, self.V, source, out, self.device)
 
     def sssp(self, source, out=None):
-        return tg_sssp(self.h, self.V, source, out)
+        return tg_sssp(self.h, self.V, source, out, self.device)
 
     def pagerank(self, iterations=5, damping=0.85, out=None):
-        return tg_pagerank(self.h, self.V, iterations, damping, out)
+        return tg_pagerank(self.h, self.V, iterations, damping, out, self.device)
 
     def bc(self, sources, out=None):
-        return tg_bc(self.h, self.V, sources, out)
+        return tg_bc(self.h, self.V, sources, out, self.device)
 
     def cc(self, out=None):
-        return tg_cc(self.h, self.V, out)
+        return tg_cc(self.h, self.V, out, self.device)
 
     def set_profiling(self, on=True):
         tg_engine_set_profiling(self.h, on)
@@ -478,3 +509,31 @@ class Engine:
     def set_exchange(self, mode):
         """TG_EXCHANGE_FUSED (default) or TG_EXCHANGE_COPY (tg_engine_set_exchange)."""
         tg_engine_set_exchange(self.h, mode)
+
+
+class HostComm:
+    """tg_hostcomm: the library's shared-memory node-local collective (the
+    multi-process vote); created collectively over a TorchComm."""
+
+    def __init__(self, comm: "TorchComm", rank: int, world: int):
+        self.comm = comm
+        self.h = C.c_void_p()
+        _check(lib().tg_hostcomm_create(C.pointer(comm.struct), rank, world, C.byref(self.h)))
+
+    def allreduce(self, vals, ops):
+        d = np.ascontiguousarray(vals, np.uint64).copy()
+        o = np.ascontiguousarray(ops, np.int32)
+        _check(lib().tg_hostcomm_allreduce_u64(self.h, d.ctypes.data_as(C.c_void_p), len(d),
+                                               o.ctypes.data_as(C.c_void_p)))
+        return d
+
+    def close(self):
+        if self.h:
+            lib().tg_hostcomm_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -63,28 +63,52 @@ def _nccl_dirs() -> tuple[str | None, str | None]:
 
 
 def build_tgraph(force: bool = False) -> str:
+    """Each .cu compiles to build/<name>.o in parallel (a file is recompiled when
+    it or any header is newer than its object), then one nvcc link -> .so."""
+    from concurrent.futures import ThreadPoolExecutor
+
     csrc = os.path.join(ROOT, "paper_1312_3018_b200", "csrc")
     cu = sorted(glob.glob(os.path.join(csrc, "*.cu")))
-    deps = cu + sorted(glob.glob(os.path.join(csrc, "*.cuh"))) + [
+    headers = sorted(glob.glob(os.path.join(csrc, "*.cuh"))) + \
+        sorted(glob.glob(os.path.join(csrc, "*.h"))) + [
         os.path.join(ROOT, "include", "tgraph.h"),
         os.path.join(ROOT, "inputs", "tg_inputs.h"),
     ]
-    if not (force or _stale(TGRAPH_SO, deps)):
+    if not (force or _stale(TGRAPH_SO, cu + headers)):
         return TGRAPH_SO
-    inc, lib = _nccl_dirs()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v", "--expt-relaxed-constexpr",
-           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(ROOT, "inputs"),
-           "-o", TGRAPH_SO, *cu]
-    if inc and os.environ.get("TG_WITH_NCCL"):
-        cmd += ["-DTG_HAVE_NCCL=1", "-I", inc, "-L", lib, "-l:libnccl.so.2",
-                "-Xlinker", "-rpath=" + lib]
-    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    obj_dir = os.path.join(ROOT, "build", "tgraph")
+    os.makedirs(obj_dir, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v", "--expt-relaxed-constexpr",
+             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(ROOT, "inputs")]
+
+    def compile_one(src):
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
+        if force or _stale(obj, [src] + headers):
+            r = subprocess.run([NVCC, *flags, "-c", "-o", obj, src], cwd=ROOT, capture_output=True,
+                               text=True)
+            if r.returncode != 0:
+                return obj, r.stdout + r.stderr, False
+            with open(obj + ".ptxas.log", "w") as f:
+                f.write(r.stderr)
+        return obj, "", True
+
+    with ThreadPoolExecutor(max_workers=min(len(cu), os.cpu_count() or 4)) as ex:
+        res = list(ex.map(compile_one, cu))
+    bad = [(o, log) for o, log, ok in res if not ok]
+    if bad:
+        for o, log in bad:
+            sys.stderr.write(f"{o}:\n{log}\n")
         raise RuntimeError("nvcc failed")
+    objs = [o for o, _, _ in res]
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", TGRAPH_SO, *objs], cwd=ROOT,
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed")
     with open(os.path.join(ROOT, "build_ptxas.log"), "w") as f:
-        f.write(r.stderr)
+        for o in objs:
+            f.write(open(o + ".ptxas.log").read() if os.path.exists(o + ".ptxas.log") else "")
     return TGRAPH_SO
 
 

@@ -65,6 +65,43 @@ def comm_worker(rank, world, port):
     dist.destroy_process_group()
 
 
+def hostcomm_worker(rank, world, port):
+    """The library's shared-memory collective (tg_hostcomm: the multi-process
+    vote) against torch.distributed on the same values: sums mod 2^64, minima
+    with the all-ones sentinel, mixed ops in one call, many epochs in a row
+    (the two value buffers alternate), ranks arriving in skewed order."""
+    import time
+
+    import torch
+
+    import paper_1312_3018_b200 as tg
+
+    dist = _init(rank, world, port)
+    comm = tg.TorchComm()
+    hc = tg.HostComm(comm, rank, world)
+    rng = np.random.default_rng(100 + rank)
+    U64 = (1 << 64) - 1
+    for it in range(300):
+        n = 1 + it % 16
+        vals = rng.integers(0, 1 << 62, n, dtype=np.uint64)
+        if it % 7 == 0:
+            vals[0] = U64
+        ops = np.array([(it + i) % 2 for i in range(n)], np.int32)
+        if it % 50 == rank:            # one rank arrives late
+            time.sleep(0.02)
+        got = hc.allreduce(vals, ops)
+        allv = [torch.zeros(n, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(allv, torch.from_numpy(vals.view(np.int64)))
+        allv = [a.numpy().view(np.uint64) for a in allv]
+        for i in range(n):
+            col = [int(a[i]) for a in allv]
+            want = min(col) if ops[i] == 1 else sum(col) % (1 << 64)
+            assert int(got[i]) == want, (it, i, int(got[i]), want)
+    hc.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def pr_pull(eng):
     """PageRank with ghost-pull communication (collective), then back to push."""
     import paper_1312_3018_b200 as tg

@@ -129,6 +129,34 @@ def test_c1_partition_layout_matches_oracle(tg):
         assert np.isclose(tot_slots / len(src), bd)
 
 
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_random_partitioning_layout_and_parity(tg, P):
+    """TG_PART_RANDOM (Fig. 4's "naive random-based" baseline): the
+    partition layout (|V_p|, |E_p|, local edges, outbox sizes per peer) equals
+    the oracle's random partition + beta, and every algorithm still matches the
+    oracle (results do not depend on the partitioning)."""
+    scale = 12
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    keys = inputs.part_keys(V)
+    part, _ = G.partition_random(P, keys)
+    _, _, slots = oracle.beta(V, src, dst, part, P)
+    for eng in (tg.Engine.from_edges(V, src, dst, w, partitions=P, strategy=tg.TG_PART_RANDOM),
+                tg.Engine.rmat(scale, partitions=P, strategy=tg.TG_PART_RANDOM)):
+        assert eng.info["strategy"] == tg.TG_PART_RANDOM
+        for p in range(P):
+            pi = eng.partition_info(p)
+            assert pi["Vp"] == int((part == p).sum())
+            assert pi["Ep"] == int((part[src] == p).sum())
+            assert pi["Ep_local"] == int(((part[src] == p) & (part[dst] == p)).sum())
+            assert np.array_equal(pi["slots_to"], slots[p]), (P, p)
+        bs = [int(x) for x in inputs.list_sources(src, 3)]
+        check_all(tg, G, eng, bfs_src=bs, sssp_src=bs[:2], pr_T=(5,), bc_src=bs[:2])
+        assert np.array_equal(eng.cc()[0], G.cc())
+        eng.close()
+
+
 # ------------------------------------------------------------ partition invariance
 @pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
 def test_partition_invariance_rmat12(tg, P):

@@ -28,6 +28,11 @@ def test_host_collectives_and_plan_gloo(world):
     mp.spawn(mp_workers.comm_worker, args=(world, _port()), nprocs=world, join=True)
 
 
+@pytest.mark.parametrize("world", [2, 4])
+def test_shared_memory_vote_gloo(world):
+    mp.spawn(mp_workers.hostcomm_worker, args=(world, _port()), nprocs=world, join=True)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("exchange", [0, 1])

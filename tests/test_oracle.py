@@ -392,6 +392,46 @@ def test_partition_balance_and_dense_local_ids():
             assert abs(len(ids) - 1000 / P) <= 1
 
 
+def test_partition_random_definition_and_invariants():
+    """RAND partitioning (Fig. 4's random baseline): the partition depends
+    only on the key draw, not on the edges; sizes equal the serpentine deal's;
+    local ids are dense and follow out-degree desc, id asc inside each part.
+    Checked against a hand-worked 6-vertex case and numpy lexsort."""
+    import inputs
+
+    # hand-worked: keys [5, 1, 5, 0, 9, 2] -> order 3,1,5,0,2,4 -> P=2 serpentine
+    # parts 0,1,1,0,0,1 -> part[3]=0, part[1]=1, part[5]=1, part[0]=0, part[2]=0, part[4]=1
+    src = np.array([0, 0, 0, 4, 4, 2], np.uint32)   # outdeg: 0:3, 4:2, 2:1, others 0
+    dst = np.array([1, 2, 3, 5, 1, 0], np.uint32)
+    G = oracle.Graph(6, src, dst)
+    part, local = G.partition_random(2, np.array([5, 1, 5, 0, 9, 2], np.uint32))
+    assert list(part) == [0, 1, 0, 0, 1, 1]
+    # part 0 = {0 (deg 3), 2 (deg 1), 3 (deg 0)}; part 1 = {4 (deg 2), 1, 5 (deg 0)}
+    assert list(local) == [0, 1, 1, 2, 0, 2]
+
+    rng = np.random.default_rng(17)
+    n = 3000
+    src, dst = random_multigraph(rng, n, 20000)
+    keys = inputs.part_keys(n)
+    G = oracle.Graph(n, src, dst)
+    deg = G.out_degree()
+    G2 = oracle.Graph(n, dst, src)                      # other edges, same keys
+    for P in (1, 2, 3, 8):
+        part, local = G.partition_random(P, keys)
+        assert np.array_equal(G2.partition_random(P, keys)[0], part)
+        pos = np.empty(n, np.int64)
+        pos[np.lexsort((np.arange(n), keys))] = np.arange(n)
+        r, j = pos // P, pos % P
+        assert np.array_equal(part, np.where(r % 2 == 0, j, P - 1 - j))
+        for p in range(P):
+            members = np.flatnonzero(part == p)
+            want = members[np.lexsort((members, -deg[members].astype(np.int64)))]
+            assert np.array_equal(local[want], np.arange(len(members)))
+        sizes = np.bincount(part, minlength=P)
+        dpart, _ = G.partition(P)
+        assert np.array_equal(sizes, np.bincount(dpart, minlength=P))
+
+
 def test_beta_golden_and_invariants():
     g = GOLD["beta_two_edges_one_remote"]
     br, bd, slots = oracle.beta(g["V"], g["src"], g["dst"], g["part"], g["P"])
