@@ -104,10 +104,12 @@ struct BcBwdOp {
 // unvisited v sums sigma over its in-neighbours in F[L]; a non-zero sum puts v
 // in F[L+1].  No atomics: the warp owns its word of F[L+1] and each lane its
 // sigma[v].  Same sigma as the push form (integer-valued fp64 sums are exact).
+// P > 1: the ghost in-CSR; a source u >= Vp is ghost u - Vp whose owner
+// published sigma (0 when not in F[L]) into gsig.
 __global__ void __launch_bounds__(256) k_bc_pull(const uint64_t* in_off, const uint32_t* in_col,
                                                  const uint32_t* F, const uint32_t* visited,
                                                  double* sigma, uint32_t* next, uint64_t Vp,
-                                                 unsigned long long* edges) {
+                                                 unsigned long long* edges, const double* gsig) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t nwords = words_for(Vp);
@@ -123,7 +125,8 @@ __global__ void __launch_bounds__(256) k_bc_pull(const uint64_t* in_off, const u
       cnt += e - b;
       for (uint64_t i = b; i < e; ++i) {
         const uint32_t u = __ldg(in_col + i);
-        if ((__ldg(F + (u >> 5)) >> (u & 31)) & 1u) s += sigma[u];
+        if (gsig && u >= Vp) s += gsig[u - Vp];
+        else if ((__ldg(F + (u >> 5)) >> (u & 31)) & 1u) s += sigma[u];
       }
       if (s > 0.0) sigma[v] = s;
     }
@@ -148,11 +151,26 @@ struct PullSigma {
   double* sigma;
   uint32_t* next;           // F[L+1]
   unsigned long long* edges;
+  const double* gsig;       // P > 1: ghost sources u >= Vp (sigma, 0 if not in F[L])
+  uint32_t Vp;
   __device__ __forceinline__ bool skip(uint64_t v) const {
     return bit_test(visited, (uint32_t)v) || !bit_test(has_in, (uint32_t)v);
   }
+  __device__ __forceinline__ double val(uint32_t u) const {
+    if (gsig && u >= Vp) return gsig[u - Vp];
+    return bit_test(F, u) ? sigma[u] : 0.0;
+  }
   __device__ __forceinline__ double sum(uint64_t i, uint64_t e, uint32_t step) const {
     double s0 = 0.0, s1 = 0.0;
+    if (gsig) {
+      for (; i + step < e; i += 2ull * step) {
+        const uint32_t u0 = __ldg(in_col + i), u1 = __ldg(in_col + i + step);
+        s0 += val(u0);
+        s1 += val(u1);
+      }
+      if (i < e) s0 += val(__ldg(in_col + i));
+      return s0 + s1;
+    }
     for (; i + step < e; i += 2ull * step) {
       const uint32_t u0 = __ldg(in_col + i), u1 = __ldg(in_col + i + step);
       const uint32_t w0 = __ldg(F + (u0 >> 5)), w1 = __ldg(F + (u1 >> 5));
@@ -487,6 +505,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     reserve_levels(*pp, 0);
     degree_classes(eng, *pp);
   }
+  // pull-sigma at P > 1 reads remote in-neighbours through the ghost in-CSR
+  if (eng.P > 1 && eng.has_in && direction_policy(eng).mode != 1) build_pr_ghost(eng);
   // backward pull by out-degree class (TG_BC_BWD_CLASSES=0: reduce-mode walker)
   const bool bwd_classes =
       !(std::getenv("TG_BC_BWD_CLASSES") && std::getenv("TG_BC_BWD_CLASSES")[0] == '0');
@@ -566,6 +586,14 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       const bool pull = dir.bottom_up(eng, lvl_count[L], mf, eng.E - std::min(explored, eng.E),
                                       was_pull, dir.bc_alpha);
       was_pull = pull;
+      if (pull && eng.P > 1) {
+        // sigma of every published source in F[L] (0 otherwise) -> peers' ghosts
+        eng.prof_begin(TG_K_EXCHANGE);
+        for (auto& pp : eng.parts)
+          publish_frontier_sigma(eng, *pp, pp->bcs.level_bm[L].get(), pp->bcs.sigma.get());
+        fused_arrival(eng);
+        eng.prof_end(TG_K_EXCHANGE);
+      }
       for (auto& pp : eng.parts) {
         Part& p = *pp;
         FrontierState& f = p.fs;
@@ -576,19 +604,24 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         // class kernels when the unexplored edges (~ the pull's work) are a
         // large share; otherwise the per-word kernel's cheaper full scan wins
         const bool dense = (eng.E - std::min(explored, eng.E)) * 16 > eng.E;
+        const bool gh = eng.P > 1;  // ghost in-CSR (remote in-neighbours)
         if (pull && pull_classes && dense) {
           // rows by in-degree class on fork/join streams (disjoint rows)
-          PullSigma o{p.in_off.get(), p.in_col.get(), b.level_bm[L].get(), f.visited.get(),
-                      p.in_nz.get(), b.sigma.get(), next, f.counters.get() + 1};
+          PullSigma o{gh ? p.gh.off.get() : p.in_off.get(), gh ? p.gh.col.get() : p.in_col.get(),
+                      b.level_bm[L].get(), f.visited.get(), gh ? p.gh.nz.get() : p.in_nz.get(),
+                      b.sigma.get(), next, f.counters.get() + 1,
+                      gh ? p.gh.sigma.get() : nullptr, (uint32_t)p.Vp};
+          const uint64_t n_cta = gh ? p.gh.n_cta : p.n_cta, n_warp = gh ? p.gh.n_warp : p.n_warp;
           eng.prof_begin(TG_K_BCF_EXPAND);
           eng.fork();
-          if (p.n_cta) {
-            k_bc_pull_cta<<<(unsigned)p.n_cta, 256, 0, eng.side[0]>>>(o, p.pr_cta.get());
+          if (n_cta) {
+            k_bc_pull_cta<<<(unsigned)n_cta, 256, 0, eng.side[0]>>>(
+                o, gh ? p.gh.cta.get() : p.pr_cta.get());
             eng.launches++;
           }
-          if (p.n_warp) {
-            k_bc_pull_warp<<<grid_for(p.n_warp * 32, 256, 148u * 16u), 256, 0, eng.side[1]>>>(
-                o, p.pr_warp.get(), p.n_warp);
+          if (n_warp) {
+            k_bc_pull_warp<<<grid_for(n_warp * 32, 256, 148u * 16u), 256, 0, eng.side[1]>>>(
+                o, gh ? p.gh.warp.get() : p.pr_warp.get(), n_warp);
             eng.launches++;
           }
           k_bc_pull_thread<<<grid_for(p.Vp, 256, 148u * 16u), 256, 0, s>>>(o, p.Vp);
@@ -599,8 +632,9 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         } else if (pull) {
           eng.prof_begin(TG_K_BCF_EXPAND);
           k_bc_pull<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
-              p.in_off.get(), p.in_col.get(), b.level_bm[L].get(), f.visited.get(), b.sigma.get(),
-              next, p.Vp, f.counters.get() + 1);
+              gh ? p.gh.off.get() : p.in_off.get(), gh ? p.gh.col.get() : p.in_col.get(),
+              b.level_bm[L].get(), f.visited.get(), b.sigma.get(), next, p.Vp,
+              f.counters.get() + 1, gh ? p.gh.sigma.get() : nullptr);
           eng.prof_end(TG_K_BCF_EXPAND);
           TG_CK(cudaGetLastError());
           eng.launches++;
@@ -612,7 +646,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         }
       }
       supersteps++;
-      if (eng.P > 1) {
+      if (eng.P > 1 && !pull) {  // a pull step only sets owned vertices: no messages
         eng.prof_begin(TG_K_EXCHANGE);
         if (eng.fused) {
           fused_arrival(eng);

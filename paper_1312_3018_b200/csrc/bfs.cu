@@ -80,11 +80,15 @@ __global__ void k_bfs_scatter(const uint32_t* ibits, const uint32_t* lid, uint64
 // every unvisited vertex scans its in-edges until it finds a parent in the
 // current frontier.  One warp per visited-bitmap word, one lane per vertex; the
 // warp owns its word of `next`, so no atomics.  Same levels as top-down.
+// P > 1: the pull walks the ghost in-CSR (PRGhost): a source u >= Vp is ghost
+// u - Vp, whose frontier bit its owner published into gbits.
+template <bool kGhost>
 __global__ void __launch_bounds__(256) k_bfs_bottom_up(const uint64_t* in_off,
                                                        const uint32_t* in_col, const uint32_t* cur,
                                                        const uint32_t* visited,
                                                        const uint32_t* has_in, uint32_t* next,
-                                                       uint64_t Vp, unsigned long long* edges) {
+                                                       uint64_t Vp, unsigned long long* edges,
+                                                       const uint32_t* gbits) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t nwords = words_for(Vp);
@@ -102,7 +106,14 @@ __global__ void __launch_bounds__(256) k_bfs_bottom_up(const uint64_t* in_off,
       for (uint64_t i = b; i < e; ++i) {
         const uint32_t u = __ldg(in_col + i);
         cnt++;
-        if ((__ldg(cur + (u >> 5)) >> (u & 31)) & 1u) {
+        bool in_f;
+        if (kGhost && u >= Vp) {
+          const uint32_t g = u - (uint32_t)Vp;
+          in_f = (__ldg(gbits + (g >> 5)) >> (g & 31)) & 1u;
+        } else {
+          in_f = (__ldg(cur + (u >> 5)) >> (u & 31)) & 1u;
+        }
+        if (in_f) {
           found = true;
           break;
         }
@@ -133,6 +144,9 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
   uint64_t bm_bytes = 0;  // one pass over every partition's vertex bitmap
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   if (eng.P == 1) eng.l2_window(eng.parts[0]->fs.visited.get(), words_for(eng.parts[0]->Vp) * 4);
+  // bottom-up steps at P > 1 pull over the ghost in-CSR: built once, outside
+  // the timed region (collective across processes)
+  if (eng.P > 1 && eng.has_in && direction_policy(eng).mode != 1) build_pr_ghost(eng);
   time_begin(eng);
   reset_vote(eng);
   for (auto& pp : eng.parts) {
@@ -170,15 +184,28 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
     const bool bottom_up =
         dir.bottom_up(eng, frontier, mf, eng.E - std::min(explored, eng.E), was_bu, dir.alpha);
     was_bu = bottom_up;
+    if (bottom_up && eng.P > 1) {
+      // the frontier bits of every published source -> the peers' ghost bits
+      eng.prof_begin(TG_K_EXCHANGE);
+      for (auto& pp : eng.parts) publish_frontier_bits(eng, *pp, pp->fs.cur.get());
+      fused_arrival(eng);
+      eng.prof_end(TG_K_EXCHANGE);
+    }
     for (auto& pp : eng.parts) {
       Part& p = *pp;
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);  // drains the tile marks even when unused
       if (bottom_up) {
         eng.prof_begin(TG_K_BFS_EXPAND);
-        k_bfs_bottom_up<<<grid_for(words_for(p.Vp) * 32, 256, 148u * 16u), 256, 0, s>>>(
-            p.in_off.get(), p.in_col.get(), f.cur.get(), f.visited.get(), p.in_nz.get(),
-            f.next.get(), p.Vp, f.counters.get() + 1);
+        const unsigned grid = grid_for(words_for(p.Vp) * 32, 256, 148u * 16u);
+        if (eng.P > 1)
+          k_bfs_bottom_up<true><<<grid, 256, 0, s>>>(p.gh.off.get(), p.gh.col.get(), f.cur.get(),
+                                                    f.visited.get(), p.gh.nz.get(), f.next.get(),
+                                                    p.Vp, f.counters.get() + 1, p.gh.bits.get());
+        else
+          k_bfs_bottom_up<false><<<grid, 256, 0, s>>>(p.in_off.get(), p.in_col.get(), f.cur.get(),
+                                                     f.visited.get(), p.in_nz.get(), f.next.get(),
+                                                     p.Vp, f.counters.get() + 1, nullptr);
         eng.prof_end(TG_K_BFS_EXPAND);
         TG_CK(cudaGetLastError());
         eng.launches++;
@@ -190,7 +217,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
     }
     bu_steps += bottom_up;
     supersteps++;
-    if (eng.P > 1) {
+    if (eng.P > 1 && !bottom_up) {  // a bottom-up step only sets owned vertices: no messages
       eng.prof_begin(TG_K_EXCHANGE);
       if (eng.fused) {
         fused_arrival(eng);

@@ -1114,8 +1114,12 @@ void build_pr_ghost(Engine& eng) {
       v.pub_lid = static_cast<const uint32_t*>(open(all[q].h_pub));
     }
   }
-  // size of r's publish list for q = q's ghost segment of r
+  // size of r's publish list for q = q's ghost segment of r (padded to 32
+  // slots: frontier bits are published as whole words)
   auto pubsz = [&](int r, int q) -> uint64_t {
+    return r == q ? 0 : (view[r].pub_off[q + 1] - view[r].pub_off[q] + 31) / 32 * 32;
+  };
+  auto pubn = [&](int r, int q) -> uint64_t {  // unpadded
     return r == q ? 0 : view[r].pub_off[q + 1] - view[r].pub_off[q];
   };
   auto gh_off_of = [&](int q, int r) -> uint64_t {  // q's ghost offset of r
@@ -1162,12 +1166,21 @@ void build_pr_ghost(Engine& eng) {
       if (s1 == s0) continue;
       const uint32_t* lid_by_slot = p.ibox_lid.get() + p.ibox_off[q] - s0;
       k_gh_fill<<<G(s1 - s0), kB, 0, s>>>(Q.in_off, Q.in_col, Q.Vp, s0, s1, lid_by_slot,
-                                          Q.pub_lid + Q.pub_off[p.id], pubsz(q, p.id),
+                                          Q.pub_lid + Q.pub_off[p.id], pubn(q, p.id),
                                           (uint32_t)(Vp + g.gh_off[q]), g.off.get(), g.col.get(),
                                           cnt.get());
       TG_CK(cudaGetLastError());
     }
     sort_rows(g.off.get(), Vp, g.col.get(), nullptr, s);
+    g.nz.alloc(std::max<uint64_t>(words_for(Vp), 1));
+    if (Vp) {
+      k_has_in<<<G(words_for(Vp)), kB, 0, s>>>(g.off.get(), Vp, g.nz.get());
+      TG_CK(cudaGetLastError());
+    }
+    g.bits.alloc(std::max<uint64_t>(words_for(g.G), 1));
+    g.sigma.alloc(std::max<uint64_t>(g.G, 1));
+    TG_CK(cudaMemsetAsync(g.bits.get(), 0, g.bits.bytes(), s));
+    TG_CK(cudaMemsetAsync(g.sigma.get(), 0, g.sigma.bytes(), s));
     // row classes of the ghost in-CSR
     DevBuf<unsigned long long> c2(2);
     TG_CK(cudaMemsetAsync(c2.get(), 0, 16, s));
@@ -1204,23 +1217,34 @@ void build_pr_ghost(Engine& eng) {
   base[1].assign(P, nullptr);
   for (auto& pp : eng.parts)
     for (int b2 = 0; b2 < 2; ++b2) base[b2][pp->id] = pp->pr.contrib[b2].get();
+  std::vector<uint32_t*> gbits(P, nullptr);
+  std::vector<double*> gsig(P, nullptr);
+  for (auto& pp : eng.parts) {
+    gbits[pp->id] = pp->gh.bits.get();
+    gsig[pp->id] = pp->gh.sigma.get();
+  }
   if (eng.multi()) {
     Part& me = *eng.parts[0];
     struct CMeta {
-      cudaIpcMemHandle_t h[2];
+      cudaIpcMemHandle_t h[2], hb, hs;
     } mine{};
     for (int b2 = 0; b2 < 2; ++b2) TG_CK(cudaIpcGetMemHandle(&mine.h[b2], me.pr.contrib[b2].get()));
+    TG_CK(cudaIpcGetMemHandle(&mine.hb, me.gh.bits.get()));
+    TG_CK(cudaIpcGetMemHandle(&mine.hs, me.gh.sigma.get()));
     std::vector<CMeta> all(eng.world);
     TG_REQUIRE(eng.comm.allgather(eng.comm.ctx, &mine, all.data(), sizeof(CMeta)) == 0, TG_ENCCL,
                "tg_comm.allgather failed");
     for (int q = 0; q < eng.world; ++q) {
       if (q == eng.rank) continue;
-      for (int b2 = 0; b2 < 2; ++b2) {
+      auto open = [&](const cudaIpcMemHandle_t& h) {
         void* ptr = nullptr;
-        TG_CK(cudaIpcOpenMemHandle(&ptr, all[q].h[b2], cudaIpcMemLazyEnablePeerAccess));
+        TG_CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
         eng.peers[q].opened.push_back(ptr);  // closed with the engine
-        base[b2][q] = static_cast<float*>(ptr);
-      }
+        return ptr;
+      };
+      for (int b2 = 0; b2 < 2; ++b2) base[b2][q] = static_cast<float*>(open(all[q].h[b2]));
+      gbits[q] = static_cast<uint32_t*>(open(all[q].hb));
+      gsig[q] = static_cast<double*>(open(all[q].hs));
     }
   }
   for (auto& pp : eng.parts) {
@@ -1230,7 +1254,23 @@ void build_pr_ghost(Engine& eng) {
       for (int q = 0; q < P; ++q)
         if (q != pp->id) g.pub_dst[b2][q] = base[b2][q] + view[q].Vp + gh_off_of(q, pp->id);
     }
+    std::vector<uint32_t*> bd(P, nullptr);
+    std::vector<double*> sd(P, nullptr);
+    for (int q = 0; q < P; ++q)
+      if (q != pp->id) {
+        const uint64_t go = gh_off_of(q, pp->id);  // multiple of 32
+        bd[q] = gbits[q] + go / 32;
+        sd[q] = gsig[q] + go;
+      }
+    g.d_pub_off.alloc(P + 1);
+    g.d_bits_dst.alloc(P);
+    g.d_sigma_dst.alloc(P);
+    TG_CK(cudaMemcpy(g.d_pub_off.get(), g.pub_off.data(), (P + 1) * 8, cudaMemcpyHostToDevice));
+    TG_CK(cudaMemcpy(g.d_bits_dst.get(), bd.data(), P * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+    TG_CK(cudaMemcpy(g.d_sigma_dst.get(), sd.data(), P * sizeof(double*), cudaMemcpyHostToDevice));
     g.built = true;
   }
+  TG_CK(cudaStreamSynchronize(s));
+  comm_barrier(eng);  // every rank's ghost buffers are zeroed before anyone publishes
 }
 }  // namespace tg

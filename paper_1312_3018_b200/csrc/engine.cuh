@@ -107,6 +107,16 @@ struct PRGhost {
   // publish destinations per buffer and peer: q's contribution array (local
   // pointer, or CUDA-IPC-mapped across processes) + Vq + q's ghost offset of p
   std::vector<float*> pub_dst[2];
+  // Direction optimization across partitions (SURVEY NEXT-1 at P > 1): the
+  // same publish lists carry frontier bits (bottom-up BFS) and frontier sigma
+  // (pull-sigma BC) into the peers' ghost slots.  Ghost segments are padded to
+  // 32 slots, so a warp publishes whole bitmap words with plain stores.
+  DevBuf<uint32_t> nz;        // bitmap over [0, Vp): ghost-CSR in-degree > 0
+  DevBuf<uint32_t> bits;      // words_for(G): frontier bit of every ghost (receive)
+  DevBuf<double> sigma;       // G: frontier sigma of every ghost, 0 if not in F (receive)
+  DevBuf<uint64_t> d_pub_off; // P + 1 (device copy of pub_off)
+  DevBuf<uint32_t*> d_bits_dst;  // [P] q's bits + q's ghost offset of p / 32
+  DevBuf<double*> d_sigma_dst;   // [P] q's sigma + q's ghost offset of p
 };
 
 struct FrontierState {  // BFS / SSSP / BC-forward (messages arrive in Part::arena_fwd)

@@ -152,6 +152,61 @@ __global__ void k_seed(uint32_t* bm, uint32_t i, uint32_t* vals, uint32_t val) {
   if (vals) vals[i] = val;
 }
 
+// warp per 32 published entries of one peer segment: ballot of the frontier
+// bits -> one word of the peer's ghost bitmap (segments are 32-aligned there)
+__global__ void k_pub_bits(const uint32_t* pub_lid, const uint64_t* pub_off, int P, int me,
+                           const uint32_t* F, uint32_t* const* dst) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    const uint64_t o = pub_off[q], n = pub_off[q + 1] - o;
+    for (uint64_t w = gw; w * 32 < n; w += nwarps) {
+      const uint64_t k = w * 32 + lane;
+      const bool b = k < n && bit_test(F, pub_lid[o + k]);
+      const uint32_t m = __ballot_sync(0xffffffffu, b);
+      if (lane == 0) dst[q][w] = m;
+    }
+  }
+}
+
+__global__ void k_pub_sigma(const uint32_t* pub_lid, const uint64_t* pub_off, int P, int me,
+                            const uint32_t* F, const double* sigma, double* const* dst) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (int q = 0; q < P; ++q) {
+    if (q == me) continue;
+    const uint64_t o = pub_off[q], n = pub_off[q + 1] - o;
+    for (uint64_t k = t; k < n; k += stride) {
+      const uint32_t u = pub_lid[o + k];
+      dst[q][k] = bit_test(F, u) ? sigma[u] : 0.0;
+    }
+  }
+}
+
+void publish_frontier_bits(Engine& eng, Part& p, const uint32_t* F) {
+  const PRGhost& g = p.gh;
+  const uint64_t n = g.pub_off.empty() ? 0 : g.pub_off[eng.P];
+  if (!n) return;
+  k_pub_bits<<<grid_for(n, 256, 148u * 16u), 256, 0, eng.stream>>>(
+      g.pub_lid.get(), g.d_pub_off.get(), eng.P, p.id, F, g.d_bits_dst.get());
+  TG_CK(cudaGetLastError());
+  eng.launches++;
+  eng.comm_bytes += n / 8;
+}
+
+void publish_frontier_sigma(Engine& eng, Part& p, const uint32_t* F, const double* sigma) {
+  const PRGhost& g = p.gh;
+  const uint64_t n = g.pub_off.empty() ? 0 : g.pub_off[eng.P];
+  if (!n) return;
+  k_pub_sigma<<<grid_for(n, 256, 148u * 16u), 256, 0, eng.stream>>>(
+      g.pub_lid.get(), g.d_pub_off.get(), eng.P, p.id, F, sigma, g.d_sigma_dst.get());
+  TG_CK(cudaGetLastError());
+  eng.launches++;
+  eng.comm_bytes += n * 8;
+}
+
 void TileSched::ensure(uint64_t ntiles) {
   const uint64_t nw = words_for(ntiles);
   if (list.n >= std::max<uint64_t>(ntiles, 1) && bm.n >= std::max<uint64_t>(nw, 1)) return;

@@ -249,10 +249,20 @@ __global__ void k_mark_tiles(const uint32_t* bm, uint64_t Vp, const uint64_t* ro
 // set bit i of bm and (optionally) vals[i] = val
 __global__ void k_seed(uint32_t* bm, uint32_t i, uint32_t* vals, uint32_t val);
 
+// the pull directions need the ghost in-CSR when P > 1 (built outside the
+// timed region, collective across processes)
+inline bool pull_ready(const Engine& eng) {
+  if (!eng.has_in) return false;
+  for (auto& pp : eng.parts)
+    if (eng.P > 1 && !pp->gh.built) return false;
+  return true;
+}
+
 // Direction optimization (Beamer et al. 2013, cited at
 // PAPER.md:767): switch top-down -> bottom-up when the frontier's out-edges m_f
 // exceed (edges not yet explored m_u) / alpha, and back when the frontier holds
-// fewer than V/beta vertices.  Single-partition engines with an in-CSR only.
+// fewer than V/beta vertices.  Engines with an in-CSR (P > 1: once the ghost
+// in-CSR is built, pull_ready).
 // Env overrides: TG_DIRECTION=top|bottom|auto, TG_BU_ALPHA (BFS, 14),
 // TG_BC_ALPHA (BC pull-sigma, 2), TG_BU_BETA (24), TG_TRACE=1.
 struct DirectionPolicy {
@@ -270,13 +280,23 @@ struct DirectionPolicy {
   }
   bool bottom_up(const Engine& eng, uint64_t nf, uint64_t mf, uint64_t mu, bool was_bu,
                  double a) const {
-    if (eng.P != 1 || !eng.has_in || mode == 1) return false;
+    if (!pull_ready(eng) || mode == 1) return false;
     if (mode == 2) return true;
     if (was_bu) return (double)nf * beta > (double)eng.V;
     return (double)mf * a > (double)mu;
   }
 };
 DirectionPolicy direction_policy(const Engine& eng);
+
+// Direction optimization across partitions: before a bottom-up BFS / pull-
+// sigma superstep every partition publishes, for each source on its publish
+// lists (PRGhost), its frontier bit (and sigma) into the peers' ghost slots;
+// the pulls then read local sources from F and ghost v = Vp + g from
+// gh.bits / gh.sigma.  One launch per partition covers every peer.  Across
+// processes the stores go to CUDA-IPC-mapped peer memory; the caller runs the
+// arrival barrier before any peer pulls.
+void publish_frontier_bits(Engine& eng, Part& p, const uint32_t* F);
+void publish_frontier_sigma(Engine& eng, Part& p, const uint32_t* F, const double* sigma);
 
 // A CSR with its edge tiles: the out-CSR, or the in-CSR restricted to the
 // local rows [0, Vp).

@@ -113,11 +113,13 @@ def pr_pull(eng):
     return r
 
 
-def engine_worker(rank, world, port, scale, device, exchange=1):
+def engine_worker(rank, world, port, scale, device, exchange=1, direction=None):
     """One partition per process on `device`; boundary messages through
     CUDA-IPC-mapped peer arenas (exchange 1: written by the compute kernels
     into the peers' arenas; 0: outbox + peer copies); rank 0 checks against
-    the oracle."""
+    the oracle.  direction: TG_DIRECTION for BFS / BC (None = auto)."""
+    if direction:
+        os.environ["TG_DIRECTION"] = direction
     import inputs
     import paper_1312_3018_b200 as tg
 

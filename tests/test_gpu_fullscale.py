@@ -1,21 +1,22 @@
-"""Full-size parity in the bench launch configuration (RMAT-28, one partition,
-device-side generation, the bench's first source).  The oracle cannot hold a
-2^32-edge CSR in one thread's time budget, so every output is checked through
-properties that hold at any size, evaluated by oracle code over the edge stream
-regenerated on the host by the shared input generator:
+"""Full-size parity in the bench launch configuration (RMAT-28,
+2^32 edges, one partition, device-side generation, bench.py's sources).
 
-* BFS levels / SSSP distances: exact O(E) certificates (oracle_*_cert_edges):
-  they hold iff the arrays equal the true hop / weighted distances;
-* PageRank: the oracle recomputes round 5 from the GPU's round-4 ranks for a
-  vertex sample (hubs + random), plus the global mass identity;
-* BC (one source): sum_v delta_s(v) = sum_{t reached} (d(s,t) - 1), delta >= 0,
-  zero at the source and at unreached vertices.
-* CC: every edge joins equal labels, label[v] <= v, label[label[v]] ==
-  label[v] (local conditions: they prove labels are constant on components and
-  name a member vertex, not that two components were never merged -- exact
-  union-find parity is at RMAT-22 in test_gpu_cc.py).
+1. Full oracle (oracle/oracle.c on the same regenerated graph, one CSR on the
+   host, the oracle calls running side by side in forked children):
+   BFS from the bench's first 2 sources and SSSP from the first, bit-exact;
+   PageRank T = 5 per vertex within 1e-5 relative (every vertex, every round
+   through the recurrence); BC from the first source per vertex within 1e-4.
+2. Exact O(E) certificates (oracle_*_cert_edges over the regenerated edge
+   stream) for BFS and SSSP from the bench's first K sources (K = 8, or
+   TG_C4_CERT_SOURCES): they hold iff the arrays equal the true hop / weighted
+   distances.
+3. CC: every edge joins equal labels, label[v] <= v, label[label[v]] ==
+   label[v] (local conditions; exact union-find parity is at RMAT-22 in
+   test_gpu_cc.py).
 
-TG_FULL_SCALE=<s> runs the same checks at a smaller scale.
+TG_FULL_SCALE=<s> runs the same checks at a smaller scale.  The full oracle
+needs ~110 GB of host memory at s = 28; it is skipped (with the reason) on a
+host with less.
 """
 import os
 import time
@@ -28,86 +29,126 @@ import oracle
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 INF = 0xFFFFFFFF
+SCALE = int(os.environ.get("TG_FULL_SCALE", "28"))
+K_CERT = int(os.environ.get("TG_C4_CERT_SOURCES", "8"))
+
+
+def host_ram_gb():
+    return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9
 
 
 @pytest.fixture(scope="module")
 def full():
     import paper_1312_3018_b200 as tg
 
-    scale = int(os.environ.get("TG_FULL_SCALE", "28"))
+    scale = SCALE
     V, E = 1 << scale, 16 << scale
     eng = tg.Engine.rmat(scale)                       # bench.py's engine
-    s = int(inputs.rmat_sources(scale, 1)[0])          # bench.py's first source
-    lv, st_bfs = eng.bfs(s)
-    dist, _ = eng.sssp(s)
-    r4, _ = eng.pagerank(4)
+    srcs = [int(s) for s in inputs.rmat_sources(scale, max(K_CERT, 2))]  # bench.py's sources
+    t0 = time.time()
+    lvs, dists, st_bfs = [], [], None
+    for i, s in enumerate(srcs[:K_CERT]):
+        lv, st = eng.bfs(s)
+        st_bfs = st_bfs or st
+        lvs.append(lv.copy())
+        dists.append(eng.sssp(s)[0].copy())
     r5, _ = eng.pagerank(5)
-    bc, _ = eng.bc([s])
+    bc, _ = eng.bc([srcs[0]])
     cc, st_cc = eng.cc()
     eng.close()
+    print(f"GPU runs: {time.time() - t0:.1f} s")
 
     t0 = time.time()
-    bfs_c = oracle.StreamingCertificate(V, s, lv, weighted=False)
-    sssp_c = oracle.StreamingCertificate(V, s, dist, weighted=True)
+    bfs_c = [oracle.StreamingCertificate(V, s, lv, weighted=False) for s, lv in zip(srcs, lvs)]
+    sssp_c = [oracle.StreamingCertificate(V, s, d, weighted=True) for s, d in zip(srcs, dists)]
     outdeg = np.zeros(V, np.uint32)
     indeg = np.zeros(V, np.uint32)
     chunk = 1 << 27
     cc_edges_ok = True
-    for first in range(0, E, chunk):                   # pass 1: certificates + degrees
+    for first in range(0, E, chunk):                   # one pass: certificates + degrees
         src, dst, w = inputs.rmat_edges(scale, weights=True, first=first,
                                         count=min(chunk, E - first))
-        bfs_c.feed(src, dst)
-        sssp_c.feed(src, dst, w)
+        for c in bfs_c:
+            c.feed(src, dst)
+        for c in sssp_c:
+            c.feed(src, dst, w)
         oracle.outdeg_edges(V, src, outdeg)
         oracle.outdeg_edges(V, dst, indeg)
         cc_edges_ok = cc_edges_ok and bool(np.array_equal(cc[src], cc[dst]))
-    rng = np.random.default_rng(2024)
-    sample = np.unique(np.concatenate([np.argsort(indeg)[-256:], rng.integers(0, V, 8192)]))
-    mask = np.zeros((V + 63) // 64, np.uint64)
-    np.bitwise_or.at(mask, sample >> 6, np.uint64(1) << (sample & 63).astype(np.uint64))
-    slot = np.zeros(V, np.uint32)
-    slot[sample] = np.arange(len(sample), dtype=np.uint32)
-    acc = np.zeros(len(sample))
-    for first in range(0, E, chunk):                   # pass 2: PageRank sample recurrence
-        src, dst, _ = inputs.rmat_edges(scale, first=first, count=min(chunk, E - first))
-        oracle.pr_sample_edges(V, src, dst, mask, slot, r4, outdeg, acc)
-    print(f"full-scale host checks: {time.time() - t0:.1f} s")
-    return dict(scale=scale, V=V, E=E, s=s, lv=lv, dist=dist, r4=r4, r5=r5, bc=bc, bfs_c=bfs_c,
-                sssp_c=sssp_c, outdeg=outdeg, indeg=indeg, sample=sample, acc=acc, st_bfs=st_bfs,
-                cc=cc, st_cc=st_cc, cc_edges_ok=cc_edges_ok)
+    print(f"streaming certificates ({K_CERT} BFS + {K_CERT} SSSP sources): {time.time() - t0:.1f} s")
+    return dict(scale=scale, V=V, E=E, srcs=srcs, lvs=lvs, dists=dists, r5=r5, bc=bc,
+                bfs_c=bfs_c, sssp_c=sssp_c, outdeg=outdeg, indeg=indeg, st_bfs=st_bfs, cc=cc,
+                st_cc=st_cc, cc_edges_ok=cc_edges_ok)
 
 
-def test_full_bfs_certificate(full):
-    assert full["lv"][full["s"]] == 0
-    assert full["bfs_c"].holds()
-    reached = full["lv"] != INF
+def test_full_bfs_certificates(full):
+    for s, lv, c in zip(full["srcs"], full["lvs"], full["bfs_c"]):
+        assert lv[s] == 0
+        assert c.holds(), f"BFS certificate fails for source {s}"
+    reached = full["lvs"][0] != INF
     assert full["st_bfs"].traversed_edges == int(full["outdeg"][reached].sum())
 
 
-def test_full_sssp_certificate(full):
-    assert full["sssp_c"].holds()
-    # every vertex BFS reaches SSSP reaches, and vice versa
-    assert np.array_equal(full["lv"] != INF, full["dist"] != INF)
+def test_full_sssp_certificates(full):
+    for s, lv, d, c in zip(full["srcs"], full["lvs"], full["dists"], full["sssp_c"]):
+        assert c.holds(), f"SSSP certificate fails for source {s}"
+        # every vertex BFS reaches SSSP reaches, and vice versa
+        assert np.array_equal(lv != INF, d != INF)
 
 
-def test_full_pagerank_recurrence_and_mass(full):
-    d, V = 0.85, full["V"]
-    pred = (1 - d) / V + d * full["acc"]
-    got = full["r5"][full["sample"]].astype(np.float64)
-    rel = np.abs(got - pred) / pred
-    assert rel.max() <= 1e-5, rel.max()
-    nondangling = full["outdeg"] > 0
-    mass_pred = (1 - d) + d * full["r4"][nondangling].astype(np.float64).sum()
-    assert abs(full["r5"].astype(np.float64).sum() - mass_pred) <= 1e-5 * mass_pred
+def test_full_oracle(full):
+    """The oracle itself on the regenerated RMAT-28 graph: BFS x 2 and SSSP x 1
+    bit-exact, PageRank (5 rounds) within 1e-5 and BC (1 source) within 1e-4
+    relative per vertex (SURVEY 8(d) C4; PAPER.md:332 RMAT28, :545 the
+    5-iteration protocol, :584-600 the BC backward sweep)."""
+    from forkpool import fork_map
 
+    # edge list 12 B/edge + CSR 8 B/edge + 8 B/vertex + the children's state
+    # (~100 B/vertex) + the fixture's result arrays
+    need_gb = (20 * full["E"] + 108 * full["V"] + 8 * K_CERT * full["V"]) / 1e9
+    if host_ram_gb() < need_gb:
+        pytest.skip(f"full oracle needs ~{need_gb:.0f} GB host RAM, box has {host_ram_gb():.0f}")
+    scale, V = full["scale"], full["V"]
+    t0 = time.time()
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    G = oracle.Graph(V, src, dst, w)
+    del src, dst, w
+    t_csr = time.time() - t0
+    s0, s1 = full["srcs"][0], full["srcs"][1]
+    lv0, d0 = full["lvs"][0], full["dists"][0]
+    lv1 = full["lvs"][1] if len(full["lvs"]) > 1 else None
+    r5, bc = full["r5"], full["bc"]
 
-def test_full_bc_dependency_identity(full):
-    lv, bc, s = full["lv"].astype(np.int64), full["bc"], full["s"]
-    reached = (full["lv"] != INF) & (np.arange(full["V"]) != s)
-    expect = float((lv[reached] - 1).sum())
-    assert abs(bc.sum() - expect) <= 1e-6 * max(expect, 1.0)
-    assert (bc >= 0).all() and bc[s] == 0
-    assert (bc[full["lv"] == INF] == 0).all()
+    def bfs_job(s, lv):
+        return ("bfs", s, bool(np.array_equal(lv, G.bfs(s))))
+
+    def sssp_job():
+        return ("sssp", s0, bool(np.array_equal(d0, G.sssp(s0))))
+
+    def pr_job():
+        ref = G.pagerank(5)
+        rel = np.abs(r5.astype(np.float64) - ref) / ref
+        return ("pagerank", 5, float(rel.max()))
+
+    def bc_job():
+        ref = G.bc([s0])
+        tol = 1e-4 * np.abs(ref) + 1e-12 * max(1.0, float(np.abs(ref).max()))
+        return ("bc", s0, int((np.abs(bc - ref) > tol).sum()))
+
+    jobs = [lambda: bfs_job(s0, lv0), sssp_job, pr_job, bc_job]
+    if lv1 is not None:
+        jobs.append(lambda: bfs_job(s1, lv1))
+    t1 = time.time()
+    res = fork_map(jobs)
+    print(f"full oracle RMAT-{scale}: CSR {t_csr:.0f} s, algorithms {time.time() - t1:.0f} s "
+          f"(side by side): {res}")
+    for kind, arg, val in res:
+        if kind in ("bfs", "sssp"):
+            assert val, f"{kind} from {arg} differs from the oracle"
+        elif kind == "pagerank":
+            assert val <= 1e-5, f"PageRank max rel err {val:.3e}"
+        else:
+            assert val == 0, f"BC: {val} vertices outside 1e-4"
 
 
 def test_full_cc_local_certificate(full):

@@ -238,23 +238,30 @@ def test_set_exchange_rejects_unknown_mode(tg):
 
 
 @pytest.mark.parametrize("mode", ["top", "bottom", "auto"])
-def test_direction_modes_same_result(tg, mode, monkeypatch):
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_direction_modes_same_result(tg, mode, P, monkeypatch):
     """Direction-optimizing BFS / pull-sigma BC: top-down,
-    forced bottom-up and the automatic switch all give the oracle's result."""
+    forced bottom-up and the automatic switch all give the oracle's result, on
+    one partition and across P partitions (P > 1: the pulls read remote
+    in-neighbours through ghost frontier bits / sigma published by their
+    owners), in both exchange transports."""
     monkeypatch.setenv("TG_DIRECTION", mode)
     scale = 13
     src, dst, w = inputs.rmat_edges(scale, weights=True)
     V = 1 << scale
     G = oracle.Graph(V, src, dst, w)
-    eng = tg.Engine.from_edges(V, src, dst, w)
+    eng = tg.Engine.from_edges(V, src, dst, w, partitions=P)
     srcs = inputs.list_sources(src, 5)
-    for s in srcs:
-        assert np.array_equal(eng.bfs(int(s))[0], G.bfs(int(s))), (mode, s)
-    assert_bc(eng.bc(srcs[:3])[0], G.bc(srcs[:3]))
+    for x in ((tg.TG_EXCHANGE_FUSED, tg.TG_EXCHANGE_COPY) if P > 1 else (None,)):
+        if x is not None:
+            eng.set_exchange(x)
+        for s in srcs:
+            assert np.array_equal(eng.bfs(int(s))[0], G.bfs(int(s))), (mode, s)
+        assert_bc(eng.bc(srcs[:3])[0], G.bc(srcs[:3]))
     # a path: every level is tiny, bottom-up must still be exact
     n = 500
     p_src = np.arange(n - 1, dtype=np.uint32)
-    Gp, ep = both(tg, n, p_src, p_src + 1)
+    Gp, ep = both(tg, n, p_src, p_src + 1, P=P)
     assert np.array_equal(ep.bfs(0)[0], Gp.bfs(0))
     assert_bc(ep.bc([0, 3])[0], Gp.bc([0, 3]))
 
@@ -432,14 +439,24 @@ def c2(tg):
 
 
 def test_c2_bfs_sssp(c2):
+    """BFS x 64 and SSSP x 64 sources, every one bit-exact
+    against the full oracle (oracle runs in forked children, one per core)."""
+    from forkpool import fork_map
+
     scale, G, eng = c2
-    srcs = inputs.rmat_sources(scale, 8)
+    srcs = [int(s) for s in inputs.rmat_sources(scale, 64)]
+    deg = G.out_degree()
+    lvs, dists = [], []
     for s in srcs:
-        lv, st = eng.bfs(int(s))
-        assert np.array_equal(lv, G.bfs(int(s))), s
-        assert st.traversed_edges == int(G.out_degree()[lv != 0xFFFFFFFF].sum())
-    for s in srcs[:3]:
-        assert np.array_equal(eng.sssp(int(s))[0], G.sssp(int(s))), s
+        lv, st = eng.bfs(s)
+        assert st.traversed_edges == int(deg[lv != 0xFFFFFFFF].sum())
+        lvs.append(lv.copy())
+        dists.append(eng.sssp(s)[0].copy())
+    jobs = [(lambda i=i: bool(np.array_equal(lvs[i], G.bfs(srcs[i])))) for i in range(64)]
+    jobs += [(lambda i=i: bool(np.array_equal(dists[i], G.sssp(srcs[i])))) for i in range(64)]
+    ok = fork_map(jobs)
+    bad = [("bfs" if j < 64 else "sssp", srcs[j % 64]) for j, o in enumerate(ok) if not o]
+    assert not bad, bad
 
 
 def test_c2_pagerank_bc(c2):

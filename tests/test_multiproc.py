@@ -39,3 +39,16 @@ def test_shared_memory_vote_gloo(world):
 def test_ipc_partitions_on_one_gpu(world, exchange):
     mp.spawn(mp_workers.engine_worker, args=(world, _port(), 12, 0, exchange), nprocs=world,
              join=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,scale,direction", [(4, 18, "bottom"), (4, 18, None),
+                                                   (8, 18, None), (8, 14, "top")])
+def test_ipc_partitions_on_one_gpu_wide(world, scale, direction):
+    """4 and 8 processes (one partition each) on one GPU at RMAT-18, fused
+    exchange, direction-optimized BFS / BC across processes (forced bottom-up /
+    pull-sigma, automatic, and top-down only), all five algorithms vs the
+    oracle; the per-superstep vote runs in the library's shared-memory
+    collective."""
+    mp.spawn(mp_workers.engine_worker, args=(world, _port(), scale, 0, 1, direction),
+             nprocs=world, join=True)
