@@ -139,8 +139,33 @@ def ncu_traffic():
 
 
 # ----------------------------------------------------------------- oracle legs
+def host_facts():
+    """nproc + the CPU model (lscpu), for the oracle's timing context."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def pin_one_core():
+    """the oracle is timed single-threaded, pinned to one core."""
+    try:
+        cpu = sorted(os.sched_getaffinity(0))[0]
+        prev = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {cpu})
+        return cpu, prev
+    except (AttributeError, OSError):
+        return None, None
+
+
 def oracle_sample(scale: int, n_src: int = 1, reps_bfs: int = 2):
-    """The CPU oracle, as it stands, on an RMAT sample of the same family.
+    """The CPU oracle, as it stands, on an RMAT sample of the same family
+    (same generator, seeds and source rule), timed pinned to one core.
     Returns (traversed_edges, seconds, description)."""
     import inputs
     import oracle
@@ -150,6 +175,7 @@ def oracle_sample(scale: int, n_src: int = 1, reps_bfs: int = 2):
     deg = G.out_degree()
     srcs = inputs.rmat_sources(scale, max(n_src, reps_bfs))
     total_e, total_s = 0, 0.0
+    cpu, prev = pin_one_core()
     for s in srcs[:reps_bfs]:
         t0 = time.perf_counter()
         lv = G.bfs(int(s))
@@ -170,8 +196,13 @@ def oracle_sample(scale: int, n_src: int = 1, reps_bfs: int = 2):
         G.bc([int(s)])
         total_s += time.perf_counter() - t0
         total_e += 2 * int(deg[lv != 0xFFFFFFFF].sum())
-    desc = (f"oracle/oracle.c single-threaded on RMAT-{scale} (same generator, edge factor 16): "
-            f"BFS x{reps_bfs}, SSSP x{n_src}, PageRank {PR_ITERS} rounds, BC x{n_src}")
+    if prev is not None:
+        os.sched_setaffinity(0, prev)
+    desc = (f"oracle/oracle.c single-threaded, pinned to core {cpu}, on RMAT-{scale} (same "
+            f"generator, seeds and source rule, edge factor 16): BFS x{reps_bfs}, SSSP x{n_src}, "
+            f"PageRank {PR_ITERS} rounds, BC x{n_src}.  Not the RMAT-28 instance itself: its "
+            f"oracle needs ~130 GB of host RAM and ~10 min (tests/test_gpu_fullscale.py "
+            f"test_full_oracle), beyond the bench's few-minute bound")
     return total_e, total_s, desc
 
 
@@ -183,6 +214,7 @@ def run_reference(args):
     import oracle
 
     scale = 20  # bounded sample per step: a few seconds of single-thread oracle work
+    cpu, _ = pin_one_core()
     src, dst, w = inputs.rmat_edges(scale, weights=True)
     G = oracle.Graph(1 << scale, src, dst, w)
     deg = G.out_degree()
@@ -214,14 +246,17 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32+f64",
         "data": "synthetic",
-        # our arm's workload; each step runs a bounded sample of it (RMAT-20)
-        "config": {"workload": f"RMAT-{args.scale} (A,B,C)=(0.57,0.19,0.19) edge factor 16: BFS + "
+        # what this arm actually runs: RMAT-20 per step, a bounded sample of our
+        # arm's RMAT-28 workload (same generator, seeds, source rule and step)
+        "config": {"workload": f"RMAT-{scale} (A,B,C)=(0.57,0.19,0.19) edge factor 16: BFS + "
                                f"SSSP + PageRank x{PR_ITERS} + BC, one source per step",
-                   "scale": args.scale, "vertices": 1 << args.scale, "edges": 16 << args.scale,
-                   "sample": f"RMAT-{scale} per step (same generator, same step), single-thread "
-                             "CPU oracle"},
+                   "scale": scale, "vertices": 1 << scale, "edges": 16 << scale,
+                   "sample_of": f"RMAT-{args.scale} (our arm's workload; its oracle run is "
+                                "minutes per algorithm and ~130 GB of host RAM)",
+                   **host_facts()},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"RMAT-{scale}, one source per step, single thread"},
+                         "sample": f"RMAT-{scale}, one source per step, single thread pinned to "
+                                   f"core {cpu}", **host_facts()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -280,6 +315,8 @@ def main():
               eng.pagerank(PR_ITERS, out=outs[2])[1], eng.bc([s], out=outs[3])[1]]
         return rs
 
+    PHASES = ("supersteps", "relaxations", "compute_ms", "exchange_ms", "vote_ms")
+
     def barrier():
         torch.cuda.synchronize()
         if dist:
@@ -291,6 +328,7 @@ def main():
     # ---- device-resident timed region (value) ----
     eng.set_profiling(True)
     per_alg = {"bfs": [0, 0.0], "sssp": [0, 0.0], "pagerank": [0, 0.0], "bc": [0, 0.0]}
+    split = {k: {f: 0.0 for f in PHASES} for k in per_alg}
     launches = 0
     barrier()
     with ClockSampler(dev) as clk:
@@ -302,6 +340,8 @@ def main():
                 per_alg[name][1] += r.device_ms
                 dev_ms += r.device_ms
                 launches += r.launches
+                for f in PHASES:
+                    split[name][f] += getattr(r, f)
         barrier()
     kstats = eng.kernel_stats()
     eng.set_profiling(False)
@@ -334,10 +374,14 @@ def main():
             t = torch.tensor([sec], device=red_dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             sec = float(t.item())
-        e2e = {"value": tr / sec / 1e9, "unit": UNIT, "h2d_bytes_per_step": 0,
+        e2e = {"value": tr / sec / 1e9, "unit": UNIT,
+               # the step's inputs: the source id of BFS, SSSP and BC (8 B each;
+               # the graph itself is built once and stays resident in HBM)
+               "h2d_bytes_per_step": 3 * 8,
                "d2h_bytes_per_step": V * (4 + 4 + 4 + 8),
-               "note": "step inputs are source ids passed by value; the graph stays resident "
-                       "in HBM; every per-vertex result is copied to pinned host memory"}
+               "note": "per step: 3 source ids host->device (BFS, SSSP, BC; the RMAT-28 graph "
+                       "is resident in HBM), every per-vertex result (levels, distances, ranks, "
+                       "BC scores: 20 B x V) device->pinned host inside the timed region"}
 
     # ---- roofline of the dominant kernel ----
     peak, peak_src = measured_peak()
@@ -346,9 +390,12 @@ def main():
     ks = kstats[dom]
     achieved = ks["algorithmic_bytes"] / (ks["ms"] * 1e-3) / 1e9 if ks["ms"] > 0 else 0.0
     tot_ms = sum(v["ms"] for v in kstats.values())
-    traffic = ncu_traffic().get(dom)
+    traffic = ncu_traffic().get(dom)  # committed ncu --set full capture (per launch)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
+                "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + "
+                                  "dram__bytes_write.sum per launch from the committed ncu "
+                                  "--set full capture (not measured inside this run)",
                 "algorithmic_bytes_per_launch": ks["algorithmic_bytes"] / max(ks["launches"], 1),
                 "avg_launch_ms": ks["ms"] / max(ks["launches"], 1), "peak_source": peak_src,
                 "share_of_kernel_time": ks["ms"] / tot_ms if tot_ms else None}
@@ -372,7 +419,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         e, s, desc = oracle_sample(args.cpu_scale)
         cpu = {"value": e / s / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc,
-               "seconds": s}
+               "seconds": s, **host_facts()}
 
     info = eng.info
     line = {
@@ -384,14 +431,21 @@ def main():
                         f"PageRank x{PR_ITERS} + BC, one source per step",
             "scale": scale, "vertices": V, "edges": E, "partitions_per_gpu": 1,
             "parallelism": "single" if world == 1 else
-            f"1D vertex partition over {world} GPUs (degree-serpentine); exchange: BFS/SSSP/PageRank "
-            "kernels write boundary messages into CUDA-IPC-mapped peer arenas (fused), BC/CC "
-            "peer copies",
+            f"1D vertex partition over {world} GPUs (degree-serpentine); exchange: "
+            + ("fused: the compute kernels of all five algorithms write boundary messages into "
+               "CUDA-IPC-mapped peer arenas (NVLink stores / reductions)"
+               if eng.info["exchange"] == tg.TG_EXCHANGE_FUSED else
+               "copy: outbox segments copied into CUDA-IPC-mapped peer arenas")
+            + "; vote: shared-memory host collective",
             "l2": "inputs larger than L2 (graph %.1f GB >> 126 MB L2)" % (info["device_bytes"] / 1e9),
             "build_s": round(build_s, 2)},
         "per_algorithm_gteps": {k: (v[0] / (v[1] * 1e-3) / 1e9 if v[1] else None)
                                 for k, v in per_alg.items()},
         "per_algorithm_ms_per_step": {k: v[1] / args.steps for k, v in per_alg.items()},
+        # supersteps, relaxations and the compute / exchange / vote
+        # split per algorithm and step (ledger CUDA events; vote = host time)
+        "per_algorithm_phases": {k: {f: v / args.steps for f, v in d.items()}
+                                 for k, d in split.items()},
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": roofline,

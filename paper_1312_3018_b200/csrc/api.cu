@@ -46,7 +46,7 @@ uint64_t Engine::device_bytes() const {
     const Part& p = *pp;
     t += b(p.row_off) + b(p.col) + b(p.w) + b(p.w8) + b(p.global_of) + b(p.tile_vf) + b(p.tile_vl) +
          b(p.obox_rid) + b(p.ibox_lid) + b(p.in_off) + b(p.in_col) + b(p.outdeg) + b(p.in_nz) + b(p.pr_cta) +
-         b(p.pr_warp) + b(p.in_tile_vf) + b(p.in_tile_vl) + b(p.arena_fwd) + b(p.arena_rev) +
+         b(p.pr_warp) + b(p.in_tile_vf) + b(p.in_tile_vl) + b(p.in_all_vf) + b(p.in_all_vl) + b(p.arena_fwd) + b(p.arena_rev) +
          b(p.staging);
   }
   return t;
@@ -77,7 +77,7 @@ void ensure_frontier_state(Engine& eng) {
     f.counters.alloc(8);
     TG_CK(cudaMemset(f.counters.get(), 0, 8 * sizeof(unsigned long long)));
     p.ts.ensure(p.ntiles);
-    if (p.in_ntiles) p.ts_in.ensure(p.in_ntiles);
+    if (p.in_ntiles || p.in_all_ntiles) p.ts_in.ensure(std::max(p.in_ntiles, p.in_all_ntiles));
   }
 }
 

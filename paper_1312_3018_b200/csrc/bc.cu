@@ -356,7 +356,11 @@ struct BcBwdPushOp {
   const uint32_t* FL;
   const double* c;
   double* dsum;
-  __device__ __forceinline__ Aux aux(uint32_t w) const { return c[w]; }
+  // row w < Vp: local w in F[L+1]; row Vp + s (P > 1): outbox slot s, whose
+  // owner published c of its vertex into ghost slot s (0 if not in F[L+1])
+  __device__ __forceinline__ Aux aux(uint32_t w) const {
+    return w < Vp ? c[w] : ghost[(uint64_t)(w - Vp) * gstride];
+  }
   static constexpr bool kSplit = true;
   static constexpr int kUnroll = 2;  // in_col, then the F[L] word, then the add
   struct Pre {
@@ -385,6 +389,9 @@ struct BcBwdPushOp {
     for (uint32_t i = threadIdx.x; i < priv; i += blockDim.x)
       if (s_dsum[i] != 0.0) atomicAdd(&dsum[i], s_dsum[i]);
   }
+  uint32_t Vp;
+  const double* ghost;
+  uint32_t gstride;
   __device__ __forceinline__ void fin(const Aux& cw, const Pre& p, const St& q) const {
     if (!((q.word >> (p.v & 31)) & 1u)) return;
     if (p.v < priv) {
@@ -395,6 +402,22 @@ struct BcBwdPushOp {
     }
   }
 };
+
+// P > 1 backward push: active rows of the whole in-CSR [0, Vp + S) = F[L+1]
+// for the local rows, ghost c != 0 for the outbox rows (thread per row, one
+// ballot per word)
+__global__ void k_bc_ext(const uint32_t* F, uint64_t Vp, const double* ghost, uint32_t gstride,
+                         uint64_t R, uint32_t* ext) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t n = (R + 31) / 32 * 32;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += stride) {
+    bool b = false;
+    if (r < Vp) b = bit_test(F, (uint32_t)r);
+    else if (r < R) b = ghost[(r - Vp) * gstride] != 0.0;
+    const uint32_t m = __ballot_sync(0xffffffffu, b);
+    if ((threadIdx.x & 31) == 0) ext[r >> 5] = m;
+  }
+}
 
 __global__ void k_bc_seed(uint32_t* bm, uint32_t i, double* sigma) {
   bm[i >> 5] |= 1u << (i & 31);
@@ -739,15 +762,35 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         // direction per level: pull over the out-edges of F[L] (cost ~ their
         // count) or push c[w] over the in-edges of F[L+1] (fp64 atomics, ~2x
         // per edge) -- whichever touches fewer edges
-        const bool push = eng.P == 1 && dir.mode != 1 && eng.parts[0]->in_ntiles &&
+        // (P > 1: over every in-CSR row -- the outbox rows carry the edges into
+        // remote successors, whose c the owners just published into the ghosts)
+        const bool push = dir.mode != 1 && pull_ready(eng) &&
+                          (eng.P == 1 ? eng.parts[0]->in_ntiles > 0 : true) &&
                           (dir.mode == 2 || 2 * lvl_in[L + 1] < lvl_out[L]);
         for (auto& pp : eng.parts) {
           Part& p = *pp;
-          if (push) {
+          if (push && eng.P > 1) {
+            if (!p.in_all_ntiles) continue;
+            const uint64_t R = p.Vp + p.S;
+            if (p.bcs.ext.n < words_for(R)) p.bcs.ext.alloc(words_for(R));
+            const double* ghost = reinterpret_cast<const double*>(p.arena_rev.get());
+            const double* gh = eng.fused ? ghost + (L & 1) : ghost;
+            const uint32_t gs = eng.fused ? 2u : 1u;
+            k_bc_ext<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(p.bcs.level_bm[L + 1].get(), p.Vp,
+                                                                 gh, gs, R, p.bcs.ext.get());
+            TG_CK(cudaGetLastError());
+            eng.launches++;
+            launch_mark_tiles(eng, in_all_tiles(p), R, p.bcs.ext.get(), p.ts_in);
+            launch_compact(eng, p.ts_in);
+            BcBwdPushOp op{p.in_col.get(), p.bcs.level_bm[L].get(), p.bcs.c.get(), p.bcs.dsum.get(),
+                           (uint32_t)std::min<uint64_t>(bc_priv, p.Vp), (uint32_t)p.Vp, gh, gs};
+            launch_expand_on(eng, in_all_tiles(p), p.ts_in, p.bcs.ext.get(), op, TG_K_BCB_EXPAND,
+                             p.fs.counters.get() + 1);
+          } else if (push) {
             launch_mark_tiles(eng, in_tiles(p), p.Vp, p.bcs.level_bm[L + 1].get(), p.ts_in);
             launch_compact(eng, p.ts_in);
             BcBwdPushOp op{p.in_col.get(), p.bcs.level_bm[L].get(), p.bcs.c.get(), p.bcs.dsum.get(),
-                           (uint32_t)std::min<uint64_t>(bc_priv, p.Vp)};
+                           (uint32_t)std::min<uint64_t>(bc_priv, p.Vp), (uint32_t)p.Vp, nullptr, 1u};
             launch_expand_on(eng, in_tiles(p), p.ts_in, p.bcs.level_bm[L + 1].get(), op,
                              TG_K_BCB_EXPAND, p.fs.counters.get() + 1);
           } else if (bwd_classes && lvl_out[L] * 16 > eng.E) {

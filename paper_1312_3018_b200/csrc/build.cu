@@ -642,6 +642,14 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
                                              pt.in_tile_vf.get(), pt.in_tile_vl.get());
       TG_CK(cudaGetLastError());
     }
+    if (P > 1 && pt.Ep && R) {
+      pt.in_all_ntiles = (pt.Ep + kTile - 1) / kTile;
+      pt.in_all_vf.alloc(pt.in_all_ntiles);
+      pt.in_all_vl.alloc(pt.in_all_ntiles);
+      k_tiles<<<G(pt.in_all_ntiles), kB, 0, s>>>(pt.in_off.get(), R, pt.Ep, pt.in_all_ntiles,
+                                                 pt.in_all_vf.get(), pt.in_all_vl.get());
+      TG_CK(cudaGetLastError());
+    }
     pt.outdeg.alloc(std::max<uint64_t>(Vp, 1));
     k_outdeg_local<<<G(Vp), kB, 0, s>>>(pt.row_off.get(), Vp, pt.outdeg.get());
     TG_CK(cudaGetLastError());

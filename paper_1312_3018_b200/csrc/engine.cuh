@@ -133,6 +133,7 @@ struct BCState {
   DevBuf<double> obox_sigma;              // forward partial sigma sums (send)
   DevBuf<double> ibox_pack;               // backward pull: owner-packed c (send)
   std::vector<DevBuf<uint32_t>> level_bm; // frontier bitmap per level
+  DevBuf<uint32_t> ext;                   // P > 1 backward push: rows [0, Vp + S) active
   // out-degree class bounds of the local ids (ids are in out-degree order):
   // [0, n_big) >= 2048, [n_big, n_mid) >= 32; computed once (backward pull)
   bool classes = false;
@@ -165,6 +166,10 @@ struct Part {
   uint64_t in_E_local = 0;          // in-edges of the local rows [0, Vp)
   uint64_t in_ntiles = 0;           // edge tiles of the in-CSR local rows
   DevBuf<uint32_t> in_tile_vf, in_tile_vl;
+  // P > 1: edge tiles over every in-CSR row [0, Vp + S) (local rows + outbox
+  // rows), for the BC backward push across partitions
+  uint64_t in_all_ntiles = 0;
+  DevBuf<uint32_t> in_all_vf, in_all_vl;
   DevBuf<uint32_t> pr_cta, pr_warp; // in-CSR rows with in-degree >= 2048 / in [32, 2048)
   uint64_t n_cta = 0, n_warp = 0;
   std::vector<uint64_t> seg_real;  // real (unpadded) outbox slots per peer

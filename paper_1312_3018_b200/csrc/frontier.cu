@@ -274,7 +274,9 @@ void launch_advance(Engine& eng, Part& p, TileSched& ts, uint32_t* next, uint32_
   eng.prof_begin(TG_K_ADVANCE);
   k_advance<<<blocks, 256, 0, eng.stream>>>(next, cur_old, visited, vals, level_val, p.Vp,
                                             p.row_off.get(), ts.bm.get(), count, degsum,
-                                            p.in_off.get(), p.has_in ? indegsum : nullptr,
+                                            // P > 1: the ghost in-CSR counts remote in-edges too
+                                            p.gh.built ? p.gh.off.get() : p.in_off.get(),
+                                            p.has_in ? indegsum : nullptr,
                                             minvals, minvals ? minout : nullptr);
   eng.prof_end(TG_K_ADVANCE);
   // next read + cur_old clear + visited RMW, one pass each

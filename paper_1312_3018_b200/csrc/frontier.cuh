@@ -312,6 +312,10 @@ inline CsrTiles out_tiles(const Part& p) {
 inline CsrTiles in_tiles(const Part& p) {
   return {p.in_off.get(), p.in_tile_vf.get(), p.in_tile_vl.get(), p.in_ntiles, p.in_E_local};
 }
+// every in-CSR row [0, Vp + S): local rows, then the outbox rows (P > 1)
+inline CsrTiles in_all_tiles(const Part& p) {
+  return {p.in_off.get(), p.in_all_vf.get(), p.in_all_vl.get(), p.in_all_ntiles, p.Ep};
+}
 
 template <class Op>
 void launch_expand_on(Engine& eng, const CsrTiles& c, TileSched& ts, const uint32_t* frontier,

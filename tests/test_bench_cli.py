@@ -1,6 +1,6 @@
 """bench.py's driver contract on CPU: the reference arm (the CPU oracle on a
 bounded sample) prints one JSON line with the keys the driver reads, on our
-arm's metric / unit / config workload."""
+arm's metric / unit, its config naming the sample it actually runs."""
 import json
 import os
 import subprocess
@@ -21,8 +21,11 @@ def test_reference_arm_json_line():
               "higher_is_better", "scaling", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "GTEPS"
-    assert d["config"]["scale"] == 28 and "RMAT-28" in d["config"]["workload"]
+    # the config names what this arm runs (a bounded RMAT-20 sample of RMAT-28)
+    assert d["config"]["scale"] == 20 and "RMAT-20" in d["config"]["workload"]
+    assert "RMAT-28" in d["config"]["sample_of"]
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
+    assert d["cpu_baseline"]["nproc"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0
 
 
