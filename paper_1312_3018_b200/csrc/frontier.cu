@@ -230,6 +230,15 @@ DirectionPolicy direction_policy(const Engine&) {
   return d;
 }
 
+bool stage_rowoff() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("TG_STAGE_ROWOFF");
+    on = e && e[0] == '1';
+  }
+  return on != 0;
+}
+
 static int g_num_sms = 0;
 unsigned expand_grid() {
   if (!g_num_sms) {

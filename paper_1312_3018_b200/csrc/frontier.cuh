@@ -98,7 +98,47 @@ struct is_split<Op, std::void_t<decltype(Op::kSplit)>> {
 //   void edge(const Aux&, uint64_t e) const;                   (!kReduce)
 //   double edge_val(uint64_t e) const;                         (kReduce)
 //   void vertex_done(uint32_t v, double sum, bool whole_row) const;  (kReduce)
-template <class Op, int U, int MB = 0>  // MB 0: no min-blocks bound (ptxas default, <= 64 regs here)
+// Row-offset staging (north star: "shared-memory or TMA staging of row
+// offsets"; kStage = 1): while a warp walks tile k, one lane has already
+// issued a bulk async copy (cp.async.bulk, the TMA engine's 1-D form,
+// completing on a per-warp mbarrier) of tile k+1's row offsets
+// row_off[vf..vl+1] into a shared-memory double buffer, so the window loop
+// reads its offsets from shared memory instead of waiting on global loads.
+// Tiles spanning more than kStageRows rows fall back to global reads.
+constexpr int kStageRows = 128;
+struct StageSlot {
+  uint64_t base;  // first staged row (even: 16-byte aligned source)
+  bool on;
+};
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// lane 0: arm the barrier with the byte count, then the bulk copy completes it
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <class Op, int U, int MB = 0, int kStage = 0>  // MB 0: no min-blocks bound
 __global__ void __launch_bounds__(kExpandThreads, MB) k_warp_expand(TileArgs a, Op op) {
   using Aux = typename Op::Aux;
   const uint32_t lane = threadIdx.x & 31;
@@ -107,11 +147,60 @@ __global__ void __launch_bounds__(kExpandThreads, MB) k_warp_expand(TileArgs a, 
   const unsigned long long ntl = *a.tile_count;
   unsigned long long edges = 0;
   if constexpr (has_block_hooks<Op>::value) op.block_begin();
-  for (uint64_t it = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; it < ntl; it += nwarps) {
+  __shared__ __align__(16) uint64_t s_ro[kStage ? kExpandThreads / 32 : 1][2][kStageRows + 2];
+  __shared__ __align__(8) uint64_t s_bar[kStage ? kExpandThreads / 32 : 1][2];
+  const uint32_t wib = kStage ? threadIdx.x >> 5 : 0;
+  // two staging slots (scalars, not arrays: no local-memory indexing)
+  StageSlot sl0{0, false}, sl1{0, false};
+  uint32_t ph0 = 0, ph1 = 0;
+  int buf = 0;
+  // stage tile list entry `it` into buffer b (all lanes agree on the slot)
+  auto stage = [&](uint64_t it, int b) {
+    StageSlot st{0, false};
+    if (it < ntl) {
+      const uint32_t t = a.tile_list[it];
+      const uint32_t vf = a.tile_vf[t], vl = a.tile_vl[t];
+      const uint64_t base = vf & ~1u;
+      const uint64_t n = ((uint64_t)vl + 2 - base + 1) & ~1ull;  // even count: 16-byte multiple
+      if (n <= (uint64_t)kStageRows + 2) {
+        st = {base, true};
+        __syncwarp();  // every lane is done reading this buffer (previous tile)
+        if (lane == 0)
+          bulk_load(&s_ro[wib][b][0], a.row_off + base, (uint32_t)(n * 8), &s_bar[wib][b]);
+      }
+    }
+    if (b) sl1 = st;
+    else sl0 = st;
+  };
+  const uint64_t it0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if constexpr (kStage != 0) {
+    if (lane == 0) {
+      mbar_init(&s_bar[wib][0]);
+      mbar_init(&s_bar[wib][1]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    stage(it0, 0);
+  }
+  for (uint64_t it = it0; it < ntl; it += nwarps) {
     const uint32_t t = a.tile_list[it];
     const uint32_t vf = a.tile_vf[t], vl = a.tile_vl[t];
     const uint64_t e_lo = (uint64_t)t * kTile;
     const uint64_t e_hi = min(e_lo + (uint64_t)kTile, a.Ep);
+    const uint64_t* ro = a.row_off;  // row offsets: global, or the staged window
+    int64_t ro_shift = 0;
+    if constexpr (kStage != 0) {
+      stage(it + nwarps, buf ^ 1);  // the next tile's offsets, in flight during this one
+      const StageSlot cs = buf ? sl1 : sl0;
+      if (cs.on) {
+        mbar_wait(&s_bar[wib][buf], buf ? ph1 : ph0);
+        if (buf) ph1 ^= 1u;
+        else ph0 ^= 1u;
+        ro = &s_ro[wib][buf][0];
+        ro_shift = (int64_t)cs.base;
+      }
+      buf ^= 1;
+    }
     for (uint32_t wv = vf & ~31u; wv <= vl; wv += 32) {
       const uint32_t x = a.frontier[wv >> 5];
       const uint32_t v = wv + lane;
@@ -129,14 +218,14 @@ __global__ void __launch_bounds__(kExpandThreads, MB) k_warp_expand(TileArgs a, 
             op.defer(v);
             aux = Aux{};
           } else {
-            const uint64_t rb = a.row_off[v], re = a.row_off[v + 1];
+            const uint64_t rb = ro[v - ro_shift], re = ro[v + 1 - ro_shift];
             b = rb > e_lo ? rb : e_lo;
             const uint64_t en = re < e_hi ? re : e_hi;
             len = (uint32_t)(en - b);
             whole = (b == rb) && (en == re);
           }
         } else {
-          const uint64_t rb = a.row_off[v], re = a.row_off[v + 1];
+          const uint64_t rb = ro[v - ro_shift], re = ro[v + 1 - ro_shift];
           b = rb > e_lo ? rb : e_lo;
           const uint64_t en = re < e_hi ? re : e_hi;
           len = (uint32_t)(en - b);
@@ -225,6 +314,9 @@ __global__ void __launch_bounds__(kExpandThreads, MB) k_warp_expand(TileArgs a, 
       }
       edges += T;
     }
+  }
+  if constexpr (kStage != 0) {  // drain a copy still in flight (issued past the last tile)
+    if (buf ? sl1.on : sl0.on) mbar_wait(&s_bar[wib][buf], buf ? ph1 : ph0);
   }
   if (a.edges && lane == 0 && edges) atomicAdd(a.edges, edges);
   if constexpr (has_block_hooks<Op>::value) op.block_end();
@@ -340,23 +432,30 @@ void launch_expand(Engine& eng, Part& p, TileSched& ts, const uint32_t* frontier
   launch_expand_on(eng, out_tiles(p), ts, frontier, op, kid, edges);
 }
 
-template <class Op, int U, int MB = 0>
-void launch_walker(Engine& eng, const TileArgs& a, const Op& op) {
+template <class Op, int U, int MB = 0, int S = 0>
+void launch_walker_s(Engine& eng, const TileArgs& a, const Op& op) {
   // persistent grid = exactly the resident CTAs (static tile striding assumes residency)
   static int per_sm = 0;
   static size_t per_sm_smem = ~(size_t)0;
   const size_t smem = smem_of(op);
   if (!per_sm || smem != per_sm_smem) {
     if (smem > 48 * 1024)
-      TG_CK(cudaFuncSetAttribute(k_warp_expand<Op, U, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    TG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_warp_expand<Op, U, MB>,
+      TG_CK(cudaFuncSetAttribute(k_warp_expand<Op, U, MB, S>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_warp_expand<Op, U, MB, S>,
                                                         kExpandThreads, smem));
     if (per_sm < 1) per_sm = 1;
     per_sm_smem = smem;
   }
-  k_warp_expand<Op, U, MB><<<expand_grid() / 8u * (unsigned)per_sm, kExpandThreads, smem, eng.stream>>>(
-      a, op);
+  k_warp_expand<Op, U, MB, S><<<expand_grid() / 8u * (unsigned)per_sm, kExpandThreads, smem,
+                                eng.stream>>>(a, op);
+}
+// TG_STAGE_ROWOFF=1: the row-offset staging variant (kStage = 1)
+bool stage_rowoff();
+template <class Op, int U, int MB = 0>
+void launch_walker(Engine& eng, const TileArgs& a, const Op& op) {
+  if (stage_rowoff()) launch_walker_s<Op, U, MB, 1>(eng, a, op);
+  else launch_walker_s<Op, U, MB, 0>(eng, a, op);
 }
 
 template <class Op>
