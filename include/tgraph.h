@@ -202,6 +202,9 @@ typedef struct {
   int strategy;              /* TG_PART_DEGREE / TG_PART_RANDOM                */
   int exchange;              /* current TG_EXCHANGE_* transport                */
   int pr_comm;               /* current TG_PR_* PageRank communication         */
+  int peer_probe;            /* multi-process: 1 if the setup self-test of peer atomics and
+                                stores through the CUDA-IPC mappings ran and passed (the
+                                fused transport is only kept when it passes)         */
 } tg_info;
 int tg_engine_info(const tg_engine* eng, tg_info* info);
 

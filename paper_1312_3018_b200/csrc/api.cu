@@ -730,6 +730,7 @@ int tg_engine_info(const tg_engine* e, tg_info* info) {
     info->strategy = eng->strategy;
     info->exchange = eng->fused ? TG_EXCHANGE_FUSED : TG_EXCHANGE_COPY;
     info->pr_comm = eng->pr_comm;
+    info->peer_probe = eng->peer_probe_passed ? 1 : 0;
   });
 }
 

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <cstring>
 
 #include "engine.cuh"
 #include "tg_inputs.h"
@@ -480,24 +481,24 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
     k_collect_keys<<<G(eng.E), kB, 0, s>>>(g, eng.E, eng.rank_of.get(), P, p, keys.get(),
                                            cnt.get() + 2);
     TG_CK(cudaGetLastError());
-    TG_REQUIRE(nremote < (1ull << 31), TG_ECAPACITY, "too many boundary edges in a partition");
+    // 64-bit item counts throughout (CUB 2.8): no 2^31 cap on boundary edges
     size_t tmp = 0;
-    TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.get(), keys2.get(), (int)nremote, 0,
+    TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.get(), keys2.get(), (int64_t)nremote, 0,
                                          64, s));
     {
       DevBuf<uint8_t> t(tmp ? tmp : 1);
-      TG_CK(cub::DeviceRadixSort::SortKeys(t.get(), tmp, keys.get(), keys2.get(), (int)nremote, 0,
+      TG_CK(cub::DeviceRadixSort::SortKeys(t.get(), tmp, keys.get(), keys2.get(), (int64_t)nremote, 0,
                                            64, s));
     }
     // unique into keys (reuse buffer)
     DevBuf<unsigned long long> nsel(1);
     tmp = 0;
     TG_CK(cub::DeviceSelect::Unique(nullptr, tmp, keys2.get(), keys.get(), nsel.get(),
-                                    (int)nremote, s));
+                                    (int64_t)nremote, s));
     {
       DevBuf<uint8_t> t(tmp ? tmp : 1);
       TG_CK(cub::DeviceSelect::Unique(t.get(), tmp, keys2.get(), keys.get(), nsel.get(),
-                                      (int)nremote, s));
+                                      (int64_t)nremote, s));
     }
     pt.S_real = d2h(nsel.get(), s);
     ukeys.alloc(pt.S_real);
@@ -516,6 +517,8 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
     }
   }
   pt.S = pt.obox_off[P];
+  // an out-CSR entry is kRemote | slot: slots must stay below 2^31
+  TG_REQUIRE(pt.S < (1ull << 31), TG_ECAPACITY, "more than 2^31 outbox slots in a partition");
   TG_CK(cudaMemcpyAsync(d_ustart.get(), ustart.data(), (P + 1) * 8, cudaMemcpyHostToDevice, s));
   TG_CK(cudaMemcpyAsync(d_poff.get(), pt.obox_off.data(), (P + 1) * 8, cudaMemcpyHostToDevice, s));
   pt.obox_rid.alloc(std::max<uint64_t>(pt.S, 1));
@@ -697,23 +700,22 @@ void build_inbox(Engine& eng, Part& pt, const EdgeGen& g) {
   uint64_t nu = 0;
   std::vector<uint64_t> ustart(P + 1, 0);
   if (n) {
-    TG_REQUIRE(n < (1ull << 31), TG_ECAPACITY, "too many boundary in-edges in a partition");
     DevBuf<unsigned long long> keys(n), keys2(n);
     TG_CK(cudaMemsetAsync(cnt.get(), 0, 8, s));
     k_in_keys<<<G(eng.E), kB, 0, s>>>(g, eng.E, eng.rank_of.get(), P, pt.id, keys.get(), cnt.get());
     TG_CK(cudaGetLastError());
     size_t tmp = 0;
-    TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.get(), keys2.get(), (int)n, 0, 64, s));
+    TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.get(), keys2.get(), (int64_t)n, 0, 64, s));
     {
       DevBuf<uint8_t> t(tmp ? tmp : 1);
-      TG_CK(cub::DeviceRadixSort::SortKeys(t.get(), tmp, keys.get(), keys2.get(), (int)n, 0, 64, s));
+      TG_CK(cub::DeviceRadixSort::SortKeys(t.get(), tmp, keys.get(), keys2.get(), (int64_t)n, 0, 64, s));
     }
     DevBuf<unsigned long long> nsel(1);
     tmp = 0;
-    TG_CK(cub::DeviceSelect::Unique(nullptr, tmp, keys2.get(), keys.get(), nsel.get(), (int)n, s));
+    TG_CK(cub::DeviceSelect::Unique(nullptr, tmp, keys2.get(), keys.get(), nsel.get(), (int64_t)n, s));
     {
       DevBuf<uint8_t> t(tmp ? tmp : 1);
-      TG_CK(cub::DeviceSelect::Unique(t.get(), tmp, keys2.get(), keys.get(), nsel.get(), (int)n, s));
+      TG_CK(cub::DeviceSelect::Unique(t.get(), tmp, keys2.get(), keys.get(), nsel.get(), (int64_t)n, s));
     }
     nu = d2h(nsel.get(), s);
     ukeys.alloc(nu);
@@ -744,6 +746,23 @@ void build_inbox(Engine& eng, Part& pt, const EdgeGen& g) {
     TG_CK(cudaGetLastError());
     TG_CK(cudaStreamSynchronize(s));
   }
+}
+
+// Fused-exchange self-test across processes: every rank adds / ORs / mins /
+// fp64-adds into each peer's probe words (its staging buffer) and stores its
+// rank into a per-sender word, through the same CUDA-IPC mappings the compute
+// kernels use; after a barrier each rank checks what landed in its own words.
+// The native-atomics attribute says peer atomics are supported; this proves
+// they (and plain peer stores) arrive, before the fused transport is trusted.
+__global__ void k_peer_probe(uint8_t* const* peer_stage, int world, int me) {
+  const int q = threadIdx.x;
+  if (q >= world || q == me) return;
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(peer_stage[q]);
+  atomicAdd(&w[0], 1ull);
+  atomicOr(reinterpret_cast<unsigned int*>(&w[1]), 1u << (me & 31));
+  atomicMin(reinterpret_cast<unsigned int*>(&w[2]), (unsigned)me);
+  atomicAdd(reinterpret_cast<double*>(&w[3]), 0.5);
+  w[4 + me] = 1000ull + (unsigned long long)me;
 }
 
 // What every partition needs to know about every other: arena / staging /
@@ -879,6 +898,44 @@ void map_remote_peers(Engine& eng) {
   }
   TG_REQUIRE(eng.comm.allreduce_u64(eng.comm.ctx, &ok, 1, 1) == 0, TG_ENCCL,
              "tg_comm.allreduce_u64 failed");
+  // self-test of peer atomics + stores through the IPC mappings (staging is
+  // >= 8 B per vertex; the probe needs 4 + world words, so only when every
+  // rank has that many vertices -- otherwise the attribute alone decides)
+  uint64_t room = me.Vp >= (uint64_t)(4 + eng.world) ? 1 : 0;
+  comm_allreduce(eng, &room, 1, 1);
+  if (ok && room && !(std::getenv("TG_PEER_PROBE") && std::getenv("TG_PEER_PROBE")[0] == '0')) {
+    cudaStream_t s = eng.stream;
+    std::vector<unsigned long long> init(4 + eng.world, 0);
+    init[2] = 0xFFFFFFFFull;
+    TG_CK(cudaMemcpy(me.staging.get(), init.data(), init.size() * 8, cudaMemcpyHostToDevice));
+    comm_barrier(eng);
+    std::vector<uint8_t*> st(eng.world, nullptr);
+    for (int q = 0; q < eng.world; ++q) st[q] = eng.peers[q].staging;
+    DevBuf<uint8_t*> d_st(eng.world);
+    TG_CK(cudaMemcpy(d_st.get(), st.data(), eng.world * sizeof(uint8_t*), cudaMemcpyHostToDevice));
+    k_peer_probe<<<1, 64, 0, s>>>(d_st.get(), eng.world, eng.rank);
+    TG_CK(cudaGetLastError());
+    TG_CK(cudaStreamSynchronize(s));
+    comm_barrier(eng);
+    std::vector<unsigned long long> got(4 + eng.world);
+    TG_CK(cudaMemcpy(got.data(), me.staging.get(), got.size() * 8, cudaMemcpyDeviceToHost));
+    uint32_t want_or = 0;
+    unsigned want_min = 0xFFFFFFFFu;
+    for (int q = 0; q < eng.world; ++q)
+      if (q != eng.rank) {
+        want_or |= 1u << (q & 31);
+        want_min = std::min<unsigned>(want_min, (unsigned)q);
+      }
+    double fsum;
+    std::memcpy(&fsum, &got[3], 8);
+    bool good = got[0] == (unsigned long long)(eng.world - 1) && (uint32_t)got[1] == want_or &&
+                (uint32_t)got[2] == want_min && fsum == 0.5 * (eng.world - 1);
+    for (int q = 0; q < eng.world; ++q)
+      if (q != eng.rank) good = good && got[4 + q] == 1000ull + (unsigned long long)q;
+    ok = good ? 1 : 0;
+    comm_allreduce(eng, &ok, 1, 1);
+    eng.peer_probe_passed = ok != 0;
+  }
   eng.peer_atomics = ok != 0;
   if (!eng.peer_atomics) eng.fused = false;
 }
@@ -1048,20 +1105,19 @@ void build_pr_ghost(Engine& eng) {
       const uint64_t e1 = d2h(p.in_off.get() + p.Vp + p.obox_off[q + 1], s);
       const uint64_t n = e1 - e0;
       if (!n) continue;
-      TG_REQUIRE(n < (1ull << 31), TG_ECAPACITY, "publish list too large");
       DevBuf<uint32_t> sorted(n);
       seg[q].alloc(n);
       size_t tmp = 0;
-      TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, p.in_col.get() + e0, sorted.get(), (int)n, 0,
+      TG_CK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, p.in_col.get() + e0, sorted.get(), (int64_t)n, 0,
                                            32, s));
       DevBuf<uint8_t> t1(tmp ? tmp : 1);
-      TG_CK(cub::DeviceRadixSort::SortKeys(t1.get(), tmp, p.in_col.get() + e0, sorted.get(), (int)n,
+      TG_CK(cub::DeviceRadixSort::SortKeys(t1.get(), tmp, p.in_col.get() + e0, sorted.get(), (int64_t)n,
                                            0, 32, s));
       DevBuf<unsigned long long> nsel(1);
       tmp = 0;
-      TG_CK(cub::DeviceSelect::Unique(nullptr, tmp, sorted.get(), seg[q].get(), nsel.get(), (int)n, s));
+      TG_CK(cub::DeviceSelect::Unique(nullptr, tmp, sorted.get(), seg[q].get(), nsel.get(), (int64_t)n, s));
       DevBuf<uint8_t> t2(tmp ? tmp : 1);
-      TG_CK(cub::DeviceSelect::Unique(t2.get(), tmp, sorted.get(), seg[q].get(), nsel.get(), (int)n, s));
+      TG_CK(cub::DeviceSelect::Unique(t2.get(), tmp, sorted.get(), seg[q].get(), nsel.get(), (int64_t)n, s));
       cnt[q] = d2h(nsel.get(), s);
     }
     for (int q = 0; q < P; ++q) g.pub_off[q + 1] = g.pub_off[q] + cnt[q];

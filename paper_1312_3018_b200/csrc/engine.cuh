@@ -229,6 +229,7 @@ struct Engine {
   // the outbox + copy communication phase instead
   bool fused = true;
   bool peer_atomics = true;  // every peer GPU supports native atomics on its memory
+  bool peer_probe_passed = false;  // the setup self-test of peer atomics / stores ran and passed
   int pr_comm = 0;           // TG_PR_PUSH (partial sums) or TG_PR_PULL (ghost contributions)
   std::vector<PeerView> peers;  // indexed by partition id (all P)
   uint64_t V = 0, E = 0;

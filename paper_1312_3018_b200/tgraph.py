@@ -95,7 +95,7 @@ class tg_info(C.Structure):
     _fields_ = [("V", C.c_uint64), ("E", C.c_uint64), ("num_partitions", C.c_int),
                 ("weighted", C.c_int), ("has_in_csr", C.c_int), ("device_bytes", C.c_uint64),
                 ("build_ms", C.c_uint64), ("device", C.c_int), ("strategy", C.c_int),
-                ("exchange", C.c_int), ("pr_comm", C.c_int)]
+                ("exchange", C.c_int), ("pr_comm", C.c_int), ("peer_probe", C.c_int)]
 
 
 class tg_part_info(C.Structure):

@@ -120,6 +120,8 @@ def engine_worker(rank, world, port, scale, device, exchange=1, direction=None):
     the oracle.  direction: TG_DIRECTION for BFS / BC (None = auto)."""
     if direction:
         os.environ["TG_DIRECTION"] = direction
+    if device < 0:  # one GPU per rank
+        device = rank
     import inputs
     import paper_1312_3018_b200 as tg
 
@@ -132,6 +134,8 @@ def engine_worker(rank, world, port, scale, device, exchange=1, direction=None):
     srcs = [int(x) for x in inputs.list_sources(src, 4)]
     results = []
     for eng in (eng_e, eng_g):
+        # the fused transport was kept only after the peer self-test passed
+        assert eng.info["peer_probe"] == 1 and eng.info["exchange"] == tg.TG_EXCHANGE_FUSED
         eng.set_exchange(exchange)
         pi = eng.partition_info(rank)
         assert pi["Vp"] == tg.tg_partition_size(V, rank, world)
