@@ -122,6 +122,7 @@ struct PRGhost {
 struct FrontierState {  // BFS / SSSP / BC-forward (messages arrive in Part::arena_fwd)
   DevBuf<uint32_t> cur, next, visited;            // bitmaps over local ids
   DevBuf<uint32_t> vals;                          // BFS level or SSSP dist (u32, Vp)
+  DevBuf<uint32_t> prev;                          // SSSP dense steps: dist before the step
   DevBuf<uint32_t> obox_mark, obox_new;           // bitmaps over outbox slots
   DevBuf<uint32_t> obox_u32;                      // SSSP / CC min-combined values
   DevBuf<uint32_t> ibox_u32;                      // CC: owner-packed labels (reverse send)

@@ -39,17 +39,37 @@ __device__ __forceinline__ double warp_sum(double x) {
 // Sources are in out-degree order, so ids below `hot` are the hubs that most
 // in-edges gather from: they are loaded evict_last; the cold tail and the
 // streamed in_col are evict_first, so they do not push the hub lines out of L2.
+// L1 placement (kL1, TG_PR_L1 A/B): 0 = L1 default for everything (L2 hints
+// only); 1 = the streamed in_col bypasses L1 (L1::no_allocate); 2 = 1 + cold
+// gathers (c >= hot) bypass L1 too, so L1 keeps hub contributions; 3 = 2 +
+// the hottest sources (c < l1hot) are L1::evict_last.
+template <int kL1>
 __device__ __forceinline__ float gather_one(const float* __restrict__ contrib, uint32_t c,
-                                            uint32_t hot, uint64_t keep, uint64_t stream) {
-  // (L1::evict_last / L1::no_allocate variants measured slower: 20.8 vs 20.35 ms)
-  return ld_f32_hint(contrib + c, c < hot ? keep : stream);
+                                            uint32_t hot, uint64_t keep, uint64_t stream,
+                                            uint32_t l1hot) {
+  if constexpr (kL1 >= 2) {
+    if (c >= hot) return ld_f32_cold(contrib + c, stream);
+    if constexpr (kL1 >= 3) {
+      if (c < l1hot) return ld_f32_hot(contrib + c, keep);
+    }
+    return ld_f32_hint(contrib + c, keep);
+  } else {
+    return ld_f32_hint(contrib + c, c < hot ? keep : stream);
+  }
 }
 
+template <int kL1>
 __device__ __forceinline__ double gather_sum(const uint32_t* __restrict__ in_col,
                                              const float* __restrict__ contrib, uint64_t i,
-                                             uint64_t e, uint32_t step, uint32_t hot) {
+                                             uint64_t e, uint32_t step, uint32_t hot,
+                                             uint32_t l1hot) {
   const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
-  auto col = [&](uint64_t j) { return ld_u32_hint(in_col + j, stream); };
+  auto col = [&](uint64_t j) {
+    if constexpr (kL1 >= 1) return ld_u32_stream(in_col + j, stream);
+    else return ld_u32_hint(in_col + j, stream);
+  };
+  auto gather_one = [&](const float* __restrict__ cb, uint32_t c, uint32_t h, uint64_t k,
+                        uint64_t st) { return tg::gather_one<kL1>(cb, c, h, k, st, l1hot); };
   double s0 = 0.0, s1 = 0.0;
   for (; i + 3ull * step < e; i += 4ull * step) {
     const uint32_t c0 = col(i), c1 = col(i + step);
@@ -77,6 +97,7 @@ struct PullOut {
   float* contrib_next;     // fused
   const uint32_t* outdeg;  // fused
   uint32_t hot;            // sources [0, hot) are gathered evict_last
+  uint32_t l1hot;          // kL1 3: sources [0, l1hot) L1::evict_last
   RemoteOut rout;          // remote: outbox sums go straight into the owner's inbox ...
   bool remote;
   int parity;              // ... double-buffered by round parity (arena slot = 2 x f64)
@@ -102,6 +123,7 @@ struct PullOut {
 };
 
 // one CTA per listed row (in-degree >= kPrCta)
+template <int kL1>
 __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off,
                                                           const uint32_t* in_col,
                                                           const float* contrib,
@@ -109,7 +131,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off
   __shared__ double s_part[kCtaThreads / 32];
   const uint64_t r = rows[blockIdx.x];
   const uint64_t b = in_off[r], e = in_off[r + 1];
-  double sum = gather_sum(in_col, contrib, b + threadIdx.x, e, kCtaThreads, o.hot);
+  double sum = gather_sum<kL1>(in_col, contrib, b + threadIdx.x, e, kCtaThreads, o.hot, o.l1hot);
   sum = warp_sum(sum);
   if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = sum;
   __syncthreads();
@@ -121,6 +143,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off
 }
 
 // one warp per listed row (32 <= in-degree < kPrCta)
+template <int kL1>
 __global__ void __launch_bounds__(256) k_pull_warp(const uint64_t* in_off, const uint32_t* in_col,
                                                    const float* contrib, const uint32_t* rows,
                                                    uint64_t n, PullOut o) {
@@ -129,13 +152,14 @@ __global__ void __launch_bounds__(256) k_pull_warp(const uint64_t* in_off, const
   for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps) {
     const uint64_t r = rows[k];
     const uint64_t b = in_off[r], e = in_off[r + 1];
-    double sum = gather_sum(in_col, contrib, b + lane, e, 32, o.hot);
+    double sum = gather_sum<kL1>(in_col, contrib, b + lane, e, 32, o.hot, o.l1hot);
     sum = warp_sum(sum);
     if (lane == 0) o.put(r, sum);
   }
 }
 
 // one thread per row of [r0, r1) with in-degree < 32 (incl. 0); others skipped
+template <int kL1>
 __global__ void __launch_bounds__(256) k_pull_thread(const uint64_t* in_off, const uint32_t* in_col,
                                                      const float* contrib, uint64_t r0, uint64_t r1,
                                                      PullOut o) {
@@ -143,7 +167,7 @@ __global__ void __launch_bounds__(256) k_pull_thread(const uint64_t* in_off, con
   for (uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < r1; r += stride) {
     const uint64_t b = in_off[r], e = in_off[r + 1];
     if (e - b >= 32) continue;
-    o.put(r, gather_sum(in_col, contrib, b, e, 1, o.hot));
+    o.put(r, gather_sum<kL1>(in_col, contrib, b, e, 1, o.hot, o.l1hot));
   }
 }
 
@@ -228,8 +252,9 @@ void publish(Engine& eng, int buf) {
   fused_arrival(eng);  // processes: published values land before any pull reads them
 }
 
-void launch_pull(Engine& eng, const PullCsr& c, const float* contrib, const PullOut& o,
-                 bool concurrent) {
+template <int kL1>
+void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const PullOut& o,
+                    bool concurrent) {
   cudaStream_t s = eng.stream, s_cta = s, s_warp = s;
   if (concurrent) {
     eng.fork();
@@ -238,20 +263,30 @@ void launch_pull(Engine& eng, const PullCsr& c, const float* contrib, const Pull
   }
   const uint64_t R = c.R;
   if (c.n_cta) {
-    k_pull_cta<<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o);
+    k_pull_cta<kL1><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o);
     eng.launches++;
   }
   if (c.n_warp) {
-    k_pull_warp<<<grid_for(c.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(c.off, c.col, contrib,
-                                                                            c.warp, c.n_warp, o);
+    k_pull_warp<kL1><<<grid_for(c.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(
+        c.off, c.col, contrib, c.warp, c.n_warp, o);
     eng.launches++;
   }
   if (R) {
-    k_pull_thread<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
+    k_pull_thread<kL1><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
     eng.launches++;
   }
   if (concurrent) eng.join();
   TG_CK(cudaGetLastError());
+}
+
+void launch_pull(Engine& eng, const PullCsr& c, const float* contrib, const PullOut& o,
+                 bool concurrent, int l1) {
+  switch (l1) {
+    case 1: launch_pull_l1<1>(eng, c, contrib, o, concurrent); break;
+    case 2: launch_pull_l1<2>(eng, c, contrib, o, concurrent); break;
+    case 3: launch_pull_l1<3>(eng, c, contrib, o, concurrent); break;
+    default: launch_pull_l1<0>(eng, c, contrib, o, concurrent);
+  }
 }
 
 void* send_obox(Part& p) { return p.pr.obox.get(); }
@@ -293,6 +328,11 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   // in profiles/r01_pr_hot_sweep.txt: 0 -> 28.2, 16M -> 20.35, all -> 21.0 ms)
   uint32_t hot = 16u << 20;
   if (const char* h = std::getenv("TG_PR_HOT")) hot = (uint32_t)std::strtoul(h, nullptr, 10);
+  // L1 placement variant (gather_one) and its L1-hot prefix (TG_PR_L1, TG_PR_L1HOT)
+  int l1 = 0;
+  if (const char* v = std::getenv("TG_PR_L1")) l1 = std::atoi(v);
+  uint32_t l1hot = 32768;
+  if (const char* v = std::getenv("TG_PR_L1HOT")) l1hot = (uint32_t)std::strtoul(v, nullptr, 10);
   // row classes on fork/join streams (TG_PR_CONCURRENT=0: one stream)
   const bool concurrent =
       !(std::getenv("TG_PR_CONCURRENT") && std::getenv("TG_PR_CONCURRENT")[0] == '0');
@@ -313,9 +353,9 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       PRState& r = p.pr;
       // P == 1 and ghost-pull: every in-edge is in the row, finalize in the pull
       PullOut o{eng.P == 1 || ghost, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
-                r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, p.rout(), eng.fused, it & 1};
+                r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, l1hot, p.rout(), eng.fused, it & 1};
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
-      launch_pull(eng, ghost ? ghost_csr(p) : push_csr(p), r.contrib[cur].get(), o, concurrent);
+      launch_pull(eng, ghost ? ghost_csr(p) : push_csr(p), r.contrib[cur].get(), o, concurrent, l1);
     }
     eng.prof_end(TG_K_PR_PULL);
     if (ghost) {  // communication: contributions of boundary sources -> peers' ghosts

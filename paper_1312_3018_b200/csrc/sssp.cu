@@ -46,6 +46,10 @@ struct SsspOp {
   bool fused;        // as RED.MIN straight into the owner's inbox slot
   uint32_t thresh;   // relax rows with dist < thresh now, defer the others ...
   uint32_t hub_end;  // ... but only rows v < hub_end (the high-degree prefix)
+  // dense superstep: the next frontier is derived afterwards from the distances
+  // that dropped (k_mark_dropped), so a relaxation issues one reduction (the
+  // RED.MIN) instead of two -- the L2 request rate is what bounds this walk
+  bool mark;
   __device__ __forceinline__ Aux aux(uint32_t v) const { return dist[v]; }
   __device__ __forceinline__ bool keep(uint32_t v, const Aux& dv) const {
     return v >= hub_end || dv < thresh;
@@ -85,10 +89,22 @@ struct SsspOp {
       // so t is active next superstep.  Both updates are fire-and-forget
       // reductions (RED.MIN / RED.OR): no round trip on the critical path.
       atomicMin(&dist[t], nd);
-      atomicOr(&next[t >> 5], 1u << (t & 31));
+      if (mark) atomicOr(&next[t >> 5], 1u << (t & 31));
     }
   }
 };
+
+// dense superstep epilogue: next |= {v : dist[v] < prev[v]} (one ballot per word)
+__global__ void k_mark_dropped(const uint32_t* __restrict__ dist, const uint32_t* __restrict__ prev,
+                               uint64_t Vp, uint32_t* next) {
+  const uint64_t n = (Vp + 31) / 32 * 32;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+    const bool d = v < Vp && __ldcs(dist + v) < __ldcs(prev + v);
+    const uint32_t m = __ballot_sync(0xffffffffu, d);
+    if ((threadIdx.x & 31) == 0 && m) next[v >> 5] |= m;
+  }
+}
 
 __global__ void k_sssp_scatter(const uint32_t* msg, const uint32_t* lid, uint64_t I, uint32_t* dist,
                                uint32_t* next) {
@@ -157,6 +173,13 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   // delta 1 / hub_deg 128 relaxes 1.5x fewer edges than plain Bellman-Ford.
   const uint32_t delta = env_u32("TG_SSSP_DELTA", 1);
   const uint32_t hub_deg = env_u32("TG_SSSP_HUB_DEG", 128);
+  // dense supersteps (more than V / dense_div active vertices) mark the next
+  // frontier by comparing distances afterwards instead of RED.OR per
+  // improvement (TG_SSSP_DENSE_DIV, 0 = never)
+  const uint32_t dense_div = env_u32("TG_SSSP_DENSE_DIV", 64);
+  if (dense_div)
+    for (auto& pp : eng.parts)
+      if (pp->fs.prev.n < std::max<uint64_t>(pp->Vp, 1)) pp->fs.prev.alloc(std::max<uint64_t>(pp->Vp, 1));
   std::vector<uint32_t> hubs(eng.parts.size(), 0);
   if (delta)
     for (size_t i = 0; i < eng.parts.size(); ++i) hubs[i] = hub_end(eng, *eng.parts[i], hub_deg);
@@ -191,20 +214,31 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get() + 5, 0xFF, 8, s));
     const uint64_t th = delta ? mind + delta : (uint64_t)kInf;
     const uint32_t thresh = th >= (uint64_t)kInf ? kInf : (uint32_t)th;
+    const bool dense = dense_div && frontier * dense_div > eng.V;
     for (size_t i = 0; i < eng.parts.size(); ++i) {
       Part& p = *eng.parts[i];
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
+      if (dense && p.Vp)
+        TG_CK(cudaMemcpyAsync(f.prev.get(), f.vals.get(), p.Vp * 4, cudaMemcpyDeviceToDevice, s));
       if (p.w8.get()) {
         SsspOp<uint8_t> op{p.col.get(), p.w8.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
                            f.counters.get() + 4, p.rout(), eng.fused, thresh,
-                           hub_deg ? hubs[i] : kInf};
+                           hub_deg ? hubs[i] : kInf, !dense};
         launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
       } else {
         SsspOp<uint32_t> op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
                             f.counters.get() + 4, p.rout(), eng.fused, thresh,
-                            hub_deg ? hubs[i] : kInf};
+                            hub_deg ? hubs[i] : kInf, !dense};
         launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
+      }
+      if (dense && p.Vp) {
+        eng.prof_begin(TG_K_SSSP_EXPAND);
+        k_mark_dropped<<<grid_for(p.Vp, 256, 148u * 16u), 256, 0, s>>>(f.vals.get(), f.prev.get(),
+                                                                      p.Vp, f.next.get());
+        eng.prof_end(TG_K_SSSP_EXPAND);
+        TG_CK(cudaGetLastError());
+        eng.launches++;
       }
     }
     supersteps++;
