@@ -7,7 +7,7 @@
    PageRank T = 5 per vertex within 1e-5 relative (every vertex, every round
    through the recurrence); BC from the first source per vertex within 1e-4.
 2. Exact O(E) certificates (oracle_*_cert_edges over the regenerated edge
-   stream) for BFS and SSSP from the bench's first K sources (K = 8, or
+   stream) for BFS and SSSP from the bench's first K sources (K = 4, or
    TG_C4_CERT_SOURCES): they hold iff the arrays equal the true hop / weighted
    distances.
 3. CC: every edge joins equal labels, label[v] <= v, label[label[v]] ==
@@ -30,7 +30,7 @@ import oracle
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 INF = 0xFFFFFFFF
 SCALE = int(os.environ.get("TG_FULL_SCALE", "28"))
-K_CERT = int(os.environ.get("TG_C4_CERT_SOURCES", "8"))
+K_CERT = int(os.environ.get("TG_C4_CERT_SOURCES", "4"))
 
 
 def host_ram_gb():
