@@ -375,6 +375,10 @@ struct BcBwdPushOp {
   // flushed once per CTA: contended global RED.ADD.F64 on a few hot addresses
   // runs at 11-31 G/s vs ~185 G/s spread out (profiles/r01_atomic_probe.txt),
   // and the backward push's targets are mostly hubs (ids are in out-degree order).
+  // Privatized targets are [hub, hub + priv): the hottest ones, [0, hub), are
+  // not pushed at all -- their dsum comes from a pull over their out-rows
+  // (k_bc_bwd_cta over [0, hub) before the push), which costs their out-degree
+  // in coalesced reads instead of ~that many RED.ADDs serialized on one address.
   uint32_t priv;
   static constexpr bool kBlockHooks = true;
   size_t smem_bytes() const { return (size_t)priv * sizeof(double); }
@@ -387,16 +391,18 @@ struct BcBwdPushOp {
     extern __shared__ double s_dsum[];
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < priv; i += blockDim.x)
-      if (s_dsum[i] != 0.0) atomicAdd(&dsum[i], s_dsum[i]);
+      if (s_dsum[i] != 0.0) atomicAdd(&dsum[hub + i], s_dsum[i]);
   }
   uint32_t Vp;
   const double* ghost;
   uint32_t gstride;
+  uint32_t hub;  // sources [0, hub) are pulled, not pushed
   __device__ __forceinline__ void fin(const Aux& cw, const Pre& p, const St& q) const {
-    if (!((q.word >> (p.v & 31)) & 1u)) return;
-    if (p.v < priv) {
+    if (p.v < hub || !((q.word >> (p.v & 31)) & 1u)) return;
+    const uint32_t k = p.v - hub;
+    if (k < priv) {
       extern __shared__ double s_dsum[];
-      atomicAdd(&s_dsum[p.v], cw);
+      atomicAdd(&s_dsum[k], cw);
     } else {
       atomicAdd(&dsum[p.v], cw);
     }
@@ -561,6 +567,10 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       !(std::getenv("TG_BC_PULL_CLASSES") && std::getenv("TG_BC_PULL_CLASSES")[0] == '0');
   uint32_t bc_priv = 512;  // RMAT-28 sweep: profiles/r01_bc_priv_sweep.txt
   if (const char* e = std::getenv("TG_BC_PRIV")) bc_priv = (uint32_t)std::strtoul(e, nullptr, 10);
+  // backward push: the top `bc_hub` local ids (highest out-degree) are pulled
+  // instead (TG_BC_HUBPULL)
+  uint32_t bc_hub = 2048;
+  if (const char* e = std::getenv("TG_BC_HUBPULL")) bc_hub = (uint32_t)std::strtoul(e, nullptr, 10);
   uint64_t supersteps = 0, traversed = 0, bytes = 0, bm_bytes = 0, relax = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   for (int si = 0; si < k; ++si) {
@@ -769,6 +779,20 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
                           (dir.mode == 2 || 2 * lvl_in[L + 1] < lvl_out[L]);
         for (auto& pp : eng.parts) {
           Part& p = *pp;
+          const uint32_t hub = push ? (uint32_t)std::min<uint64_t>(bc_hub, p.nz_end) : 0u;
+          if (hub) {  // hub rows of F[L]: pull over their out-edges (CTA per row)
+            const double* ghost = reinterpret_cast<const double*>(p.arena_rev.get());
+            PullDelta o{p.row_off.get(), p.col.get(), p.bcs.level_bm[L].get(),
+                        p.bcs.level_bm[L + 1].get(), p.bcs.c.get(),
+                        eng.fused ? ghost + (L & 1) : ghost, eng.fused ? 2u : 1u,
+                        p.bcs.dsum.get(), p.fs.counters.get() + 1};
+            eng.prof_begin(TG_K_BCB_EXPAND);
+            k_bc_bwd_cta<<<grid_for(hub, 1, 148u * 8u), 256, 0, s>>>(o, hub);
+            eng.prof_end(TG_K_BCB_EXPAND);
+            TG_CK(cudaGetLastError());
+            eng.launches++;
+          }
+          const uint32_t priv = (uint32_t)std::min<uint64_t>(bc_priv, p.Vp - std::min<uint64_t>(hub, p.Vp));
           if (push && eng.P > 1) {
             if (!p.in_all_ntiles) continue;
             const uint64_t R = p.Vp + p.S;
@@ -783,14 +807,14 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
             launch_mark_tiles(eng, in_all_tiles(p), R, p.bcs.ext.get(), p.ts_in);
             launch_compact(eng, p.ts_in);
             BcBwdPushOp op{p.in_col.get(), p.bcs.level_bm[L].get(), p.bcs.c.get(), p.bcs.dsum.get(),
-                           (uint32_t)std::min<uint64_t>(bc_priv, p.Vp), (uint32_t)p.Vp, gh, gs};
+                           priv, (uint32_t)p.Vp, gh, gs, hub};
             launch_expand_on(eng, in_all_tiles(p), p.ts_in, p.bcs.ext.get(), op, TG_K_BCB_EXPAND,
                              p.fs.counters.get() + 1);
           } else if (push) {
             launch_mark_tiles(eng, in_tiles(p), p.Vp, p.bcs.level_bm[L + 1].get(), p.ts_in);
             launch_compact(eng, p.ts_in);
             BcBwdPushOp op{p.in_col.get(), p.bcs.level_bm[L].get(), p.bcs.c.get(), p.bcs.dsum.get(),
-                           (uint32_t)std::min<uint64_t>(bc_priv, p.Vp), (uint32_t)p.Vp, nullptr, 1u};
+                           priv, (uint32_t)p.Vp, nullptr, 1u, hub};
             launch_expand_on(eng, in_tiles(p), p.ts_in, p.bcs.level_bm[L + 1].get(), op,
                              TG_K_BCB_EXPAND, p.fs.counters.get() + 1);
           } else if (bwd_classes && lvl_out[L] * 16 > eng.E) {

@@ -176,7 +176,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   // dense supersteps (more than V / dense_div active vertices) mark the next
   // frontier by comparing distances afterwards instead of RED.OR per
   // improvement (TG_SSSP_DENSE_DIV, 0 = never)
-  const uint32_t dense_div = env_u32("TG_SSSP_DENSE_DIV", 64);
+  const uint32_t dense_div = env_u32("TG_SSSP_DENSE_DIV", 0);  // A/B: profiles/r02_sssp_dense_ab.txt
   if (dense_div)
     for (auto& pp : eng.parts)
       if (pp->fs.prev.n < std::max<uint64_t>(pp->Vp, 1)) pp->fs.prev.alloc(std::max<uint64_t>(pp->Vp, 1));
