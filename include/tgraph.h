@@ -336,6 +336,19 @@ int tg_engine_set_exchange(tg_engine* eng, int mode);
  * TG_EINVAL for NULL or an unknown mode. */
 enum { TG_PR_PUSH = 0, TG_PR_PULL = 1 };
 int tg_engine_set_pagerank_comm(tg_engine* eng, int mode);
+
+/* Asynchronous result collection into HOST memory (single-process engines;
+ * the collection step of P:902-913, outside the paper's timed scope).  With
+ * on = 1, an algorithm call that writes a host output array returns once its
+ * results are gathered on the device: the device->host copy proceeds on a
+ * copy stream, overlapping the caller's next algorithm call, and the host
+ * array is complete only after tg_engine_sync.  Device outputs, stats and
+ * errors are unaffected.  The caller must not free or read a host output
+ * before tg_engine_sync.  on = 0 (default): outputs are complete on return.
+ * TG_EINVAL for NULL; ignored (stays synchronous) on multi-process engines. */
+int tg_engine_set_async_collect(tg_engine* eng, int on);
+/* Wait for every pending result copy (and the engine's stream). */
+int tg_engine_sync(tg_engine* eng);
 int tg_engine_kernel_stat(const tg_engine* eng, int kernel_id, tg_kernel_stat* out);
 const char* tg_kernel_name(int kernel_id);
 

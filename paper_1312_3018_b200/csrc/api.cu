@@ -31,6 +31,11 @@ Engine::~Engine() {
     if (join_ev[i]) cudaEventDestroy(join_ev[i]);
   }
   if (fork_ev) cudaEventDestroy(fork_ev);
+  if (copy_stream) cudaStreamSynchronize(copy_stream);
+  for (int i = 0; i < 2; ++i)
+    if (stage_free[i]) cudaEventDestroy(stage_free[i]);
+  if (chunk_ev) cudaEventDestroy(chunk_ev);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
   if (prof_open) cudaEventDestroy(prof_open);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -41,7 +46,7 @@ static uint64_t b(const DevBuf<T>& d) {
 }
 
 uint64_t Engine::device_bytes() const {
-  uint64_t t = b(rank_of);
+  uint64_t t = b(rank_of) + b(scratch) + b(stage2[0]) + b(stage2[1]);
   for (auto& pp : parts) {
     const Part& p = *pp;
     t += b(p.row_off) + b(p.col) + b(p.w) + b(p.w8) + b(p.global_of) + b(p.tile_vf) + b(p.tile_vl) +
@@ -461,6 +466,32 @@ void collect(Engine& eng, ValsOf vals, size_t elem, void* out, int mem) {
     PartVals pv{};
     pv.P = eng.P;
     for (auto& pp : eng.parts) pv.v[pp->id] = vals(*pp);
+    if (mem == TG_MEM_HOST && eng.async_collect) {
+      // gather chunks into a staging buffer on the engine stream; copy_stream
+      // moves each chunk to the host as soon as it is gathered and keeps going
+      // while the caller's next algorithm runs (tg_engine_sync completes it)
+      if (!eng.copy_stream) {
+        TG_CK(cudaStreamCreateWithFlags(&eng.copy_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) TG_CK(cudaEventCreateWithFlags(&eng.stage_free[i], cudaEventDisableTiming));
+        TG_CK(cudaEventCreateWithFlags(&eng.chunk_ev, cudaEventDisableTiming));
+      }
+      const int k = eng.stage_next;
+      eng.stage_next ^= 1;
+      if (eng.stage2[k].bytes() < eng.V * elem) eng.stage2[k].alloc(eng.V * 8);
+      uint8_t* st = eng.stage2[k].get();
+      TG_CK(cudaStreamWaitEvent(s, eng.stage_free[k], 0));  // its previous copy is done
+      const uint64_t chunk = 1ull << 25;
+      for (uint64_t g0 = 0; g0 < eng.V; g0 += chunk) {
+        const uint64_t g1 = std::min<uint64_t>(eng.V, g0 + chunk);
+        gather_global(eng, pv, elem, g0, g1, st, s);
+        TG_CK(cudaEventRecord(eng.chunk_ev, s));
+        TG_CK(cudaStreamWaitEvent(eng.copy_stream, eng.chunk_ev, 0));
+        TG_CK(cudaMemcpyAsync(static_cast<uint8_t*>(out) + g0 * elem, st + g0 * elem,
+                              (g1 - g0) * elem, cudaMemcpyDeviceToHost, eng.copy_stream));
+      }
+      TG_CK(cudaEventRecord(eng.stage_free[k], eng.copy_stream));
+      return;
+    }
     if (mem == TG_MEM_HOST && mode == 2) {
       // chunked: gather chunk k on the engine stream, copy it to the host on a
       // side stream while chunk k+1 is gathered
@@ -816,6 +847,26 @@ int tg_engine_set_exchange(tg_engine* e, int mode) {
     TG_REQUIRE(mode == TG_EXCHANGE_COPY || eng.peer_atomics, TG_EINVAL,
                "tg_engine_set_exchange: FUSED needs native peer atomics between the ranks' GPUs");
     eng.fused = mode == TG_EXCHANGE_FUSED;
+  });
+}
+
+int tg_engine_set_async_collect(tg_engine* e, int on) {
+  return guard([&] {
+    TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");
+    Engine& eng = *reinterpret_cast<Engine*>(e);
+    TG_CK(cudaSetDevice(eng.device));
+    if (eng.copy_stream) TG_CK(cudaStreamSynchronize(eng.copy_stream));
+    eng.async_collect = on != 0 && !eng.multi();
+  });
+}
+
+int tg_engine_sync(tg_engine* e) {
+  return guard([&] {
+    TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");
+    Engine& eng = *reinterpret_cast<Engine*>(e);
+    TG_CK(cudaSetDevice(eng.device));
+    if (eng.copy_stream) TG_CK(cudaStreamSynchronize(eng.copy_stream));
+    TG_CK(cudaStreamSynchronize(eng.stream));
   });
 }
 

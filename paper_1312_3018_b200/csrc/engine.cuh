@@ -245,6 +245,17 @@ struct Engine {
   void join();   // the main stream waits for the side streams' work
   DevBuf<uint32_t> rank_of;  // global id -> degree-order position
   DevBuf<uint8_t> scratch;   // device staging of host-bound results (V x 8 max)
+  // Asynchronous host collection (tg_engine_set_async_collect): results bound
+  // for host memory are gathered into one of two device staging buffers on
+  // the engine stream, then copied to the host on copy_stream while the next
+  // algorithm already computes; tg_engine_sync waits for the copies.  A
+  // staging buffer is reused only after its previous copy finished (event).
+  bool async_collect = false;
+  cudaStream_t copy_stream = nullptr;
+  DevBuf<uint8_t> stage2[2];
+  cudaEvent_t stage_free[2] = {nullptr, nullptr};
+  cudaEvent_t chunk_ev = nullptr;
+  int stage_next = 0;
   std::vector<std::unique_ptr<Part>> parts;
   uint64_t build_ms = 0;
   uint64_t launches = 0;     // kernels launched by the current run

@@ -171,6 +171,75 @@ __global__ void __launch_bounds__(256) k_pull_thread(const uint64_t* in_off, con
   }
 }
 
+// rows with in-degree < 32, a warp per 32 consecutive rows (TG_PR_SEG=1): the
+// warp walks the rows' concatenated in-edges 32 at a time (in_col reads
+// coalesced, where a thread per row makes 32 lanes read 32 separate rows) and
+// sums each row's contributions with a segmented shuffle scan (fp64), the
+// row's lane collecting its segment's partial at the end of every 32-edge chunk.
+// Rows of in-degree >= 32 are left to the CTA / warp classes.
+__global__ void __launch_bounds__(256) k_pull_seg(const uint64_t* in_off, const uint32_t* in_col,
+                                                  const float* contrib, uint64_t R, PullOut o) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lowm = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
+  for (uint64_t r0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32; r0 < R;
+       r0 += nwarps * 32) {
+    const uint64_t r = r0 + lane;
+    uint64_t b = 0, e = 0;
+    if (r < R) {
+      b = in_off[r];
+      e = in_off[r + 1];
+    }
+    const bool mine = r < R && e - b < 32;
+    const uint32_t len = mine ? (uint32_t)(e - b) : 0u;
+    uint32_t incl = len;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, k);
+      if (lane >= (uint32_t)k) incl += y;
+    }
+    const uint32_t T = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - len;
+    const uint64_t basev = b - excl;  // in_col index of flattened position i of my row = basev + i
+    const uint32_t lmask = __ballot_sync(0xffffffffu, len > 0);
+    const uint32_t owner_of = __fns(lmask, 0, (int)lane + 1);  // lane of non-empty row #lane
+    double acc = 0.0;
+    uint32_t s0 = 0;
+    for (uint32_t c0 = 0; c0 < T; c0 += 32) {
+      const uint32_t flag = (len > 0 && excl > c0 && excl < c0 + 32) ? (1u << (excl - c0)) : 0u;
+      const uint32_t starts = __reduce_or_sync(0xffffffffu, flag);
+      const uint32_t s = s0 + __popc(starts & lowm);
+      const uint32_t idx = c0 + lane;
+      const uint32_t ow = __shfl_sync(0xffffffffu, owner_of, s & 31);
+      const uint64_t bs = __shfl_sync(0xffffffffu, basev, ow & 31);
+      double val = 0.0;
+      if (idx < T) {
+        const uint32_t c = ld_u32_hint(in_col + bs + idx, stream);
+        val = (double)ld_f32_hint(contrib + c, c < o.hot ? keep : stream);
+      }
+#pragma unroll
+      for (int k = 1; k < 32; k <<= 1) {
+        const double vo = __shfl_up_sync(0xffffffffu, val, k);
+        const uint32_t so = __shfl_up_sync(0xffffffffu, s, k);
+        if (lane >= (uint32_t)k && so == s) val += vo;
+      }
+      int tail = -1;
+      if (len > 0) {
+        const uint32_t st = excl > c0 ? excl : c0;
+        const uint32_t en = (excl + len) < (c0 + 32) ? (excl + len) : (c0 + 32);
+        if (st < en) tail = (int)(en - 1 - c0);
+      }
+      const double got = __shfl_sync(0xffffffffu, val, tail < 0 ? 0 : tail);
+      if (tail >= 0) acc += got;
+      const uint32_t sl = __shfl_sync(0xffffffffu, s, 31);
+      const uint32_t nb = __reduce_or_sync(0xffffffffu, (len > 0 && excl == c0 + 32) ? 1u : 0u);
+      s0 = sl + nb;
+    }
+    if (mine) o.put(r, acc);
+  }
+}
+
 __global__ void k_pr_init(const uint32_t* outdeg, uint64_t Vp, double r0, float* contrib, float* rank) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride) {
@@ -272,7 +341,11 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
     eng.launches++;
   }
   if (R) {
-    k_pull_thread<kL1><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
+    const char* seg = std::getenv("TG_PR_SEG");
+    if (seg && seg[0] == '1')
+      k_pull_seg<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, R, o);
+    else
+      k_pull_thread<kL1><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
     eng.launches++;
   }
   if (concurrent) eng.join();

@@ -178,11 +178,13 @@ def lib():
         L.tg_graph_free.restype = None
         L.tg_engine_create.argtypes = [p, C.POINTER(tg_attr), C.POINTER(p)]
         L.tg_rmat_edges.argtypes = [i32, i32, dbl, dbl, dbl, u64, i32, u64, u64, u64, p, p, p, i32]
+        L.tg_engine_set_async_collect.argtypes = [p, i32]
+        L.tg_engine_sync.argtypes = [p]
         L.tg_hostcomm_create.argtypes = [C.POINTER(tg_comm), i32, i32, C.POINTER(p)]
         L.tg_hostcomm_allreduce_u64.argtypes = [p, p, i32, p]
         L.tg_hostcomm_free.argtypes = [p]
         L.tg_hostcomm_free.restype = None
-        for f in ("tg_hostcomm_create", "tg_hostcomm_allreduce_u64", "tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
+        for f in ("tg_engine_set_async_collect", "tg_engine_sync", "tg_hostcomm_create", "tg_hostcomm_allreduce_u64", "tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
                   "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc",
                   "tg_cc", "tg_engine_set_profiling", "tg_engine_set_exchange", "tg_engine_set_pagerank_comm", "tg_engine_kernel_stat", "tg_graph_from_edges",
                   "tg_graph_load_edge_list", "tg_graph_info", "tg_graph_edges", "tg_engine_create",
@@ -505,6 +507,14 @@ class Engine:
     def set_pagerank_comm(self, mode):
         """TG_PR_PUSH (default) or TG_PR_PULL (tg_engine_set_pagerank_comm)."""
         tg_engine_set_pagerank_comm(self.h, mode)
+
+    def set_async_collect(self, on=True):
+        """tg_engine_set_async_collect: host outputs complete only after sync()."""
+        _check(lib().tg_engine_set_async_collect(self.h, int(on)))
+
+    def sync(self):
+        """tg_engine_sync: wait for pending result copies."""
+        _check(lib().tg_engine_sync(self.h))
 
     def set_exchange(self, mode):
         """TG_EXCHANGE_FUSED (default) or TG_EXCHANGE_COPY (tg_engine_set_exchange)."""

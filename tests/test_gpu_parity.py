@@ -237,6 +237,24 @@ def test_set_exchange_rejects_unknown_mode(tg):
     assert e.value.code == tgraph.TG_EINVAL
 
 
+@pytest.mark.parametrize("variant", [("TG_PR_SEG", "1"), ("TG_PR_L1", "2"), ("TG_PR_L1", "3"),
+                                     ("TG_SSSP_DENSE_DIV", "64"), ("TG_BC_HUBPULL", "0"),
+                                     ("TG_BC_HUBPULL", "64"), ("TG_STAGE_ROWOFF", "1")])
+@pytest.mark.parametrize("P", [1, 3])
+def test_kernel_variants_same_result(tg, variant, P, monkeypatch):
+    """The A/B kernel variants behind run-time switches
+    give the oracle's results too: they only change how the same sums / minima
+    are formed."""
+    monkeypatch.setenv(*variant)
+    scale = 13
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    eng = tg.Engine.from_edges(V, src, dst, w, partitions=P)
+    srcs = inputs.list_sources(src, 3)
+    check_all(tg, G, eng, bfs_src=srcs, sssp_src=srcs[:2], pr_T=(5,), bc_src=srcs[:2])
+
+
 @pytest.mark.parametrize("mode", ["top", "bottom", "auto"])
 @pytest.mark.parametrize("P", [1, 2, 3, 8])
 def test_direction_modes_same_result(tg, mode, P, monkeypatch):
@@ -515,3 +533,35 @@ def test_sssp_wide_weights_and_overflow(tg, P):
     with pytest.raises(tgraph.TGraphError) as e:
         eng2.sssp(0)
     assert e.value.code == tgraph.TG_EINTERNAL
+
+
+def test_async_host_collection(tg):
+    """tg_engine_set_async_collect: host outputs of consecutive calls (copied
+    on the library's copy stream while the next algorithm runs, two staging
+    buffers in rotation) are all exact once tg_engine_sync returns; off again,
+    outputs are complete on return."""
+    scale = 14
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    eng = tg.Engine.from_edges(V, src, dst, w)
+    srcs = [int(x) for x in inputs.list_sources(src, 3)]
+    eng.set_async_collect(True)
+    outs = []
+    for s in srcs:
+        lv, ds = np.empty(V, np.uint32), np.empty(V, np.uint32)
+        b, pr = np.empty(V), np.empty(V, np.float32)
+        eng.bc([s], out=b)
+        eng.bfs(s, out=lv)
+        eng.pagerank(5, out=pr)
+        eng.sssp(s, out=ds)
+        outs.append((s, lv, ds, pr, b))
+    eng.sync()
+    ref_pr = G.pagerank(5)
+    for s, lv, ds, pr, b in outs:
+        assert np.array_equal(lv, G.bfs(s)) and np.array_equal(ds, G.sssp(s))
+        assert_pr(pr, ref_pr)
+        assert_bc(b, G.bc([s]))
+    eng.set_async_collect(False)
+    assert np.array_equal(eng.bfs(srcs[0])[0], G.bfs(srcs[0]))
+    eng.close()
