@@ -569,7 +569,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
   if (const char* e = std::getenv("TG_BC_PRIV")) bc_priv = (uint32_t)std::strtoul(e, nullptr, 10);
   // backward push: the top `bc_hub` local ids (highest out-degree) are pulled
   // instead (TG_BC_HUBPULL)
-  uint32_t bc_hub = 2048;
+  uint32_t bc_hub = 0;  // A/B: profiles/r02_bc_hubpull_ab.txt (a CTA per hub row serializes 2M-edge rows)
   if (const char* e = std::getenv("TG_BC_HUBPULL")) bc_hub = (uint32_t)std::strtoul(e, nullptr, 10);
   uint64_t supersteps = 0, traversed = 0, bytes = 0, bm_bytes = 0, relax = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;

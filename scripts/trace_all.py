@@ -1,5 +1,6 @@
 """Per-superstep trace (TG_TRACE=1: counts + synchronized lap ms) of BFS, SSSP
-and BC from one source, plus the kernel ledger of each, at a given scale."""
+and BC from one source, plus the kernel ledger of each, at a given scale.
+usage: trace_all.py SCALE [algs] [P]"""
 import os
 import sys
 
@@ -9,7 +10,8 @@ import paper_1312_3018_b200 as tg  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 28
 algs = sys.argv[2].split(",") if len(sys.argv) > 2 else ["bfs", "sssp", "bc"]
-eng = tg.Engine.rmat(scale)
+P = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+eng = tg.Engine.rmat(scale, partitions=P)
 s = int(inputs.rmat_sources(scale, 1)[0])
 run = {"bfs": lambda: eng.bfs(s), "sssp": lambda: eng.sssp(s), "bc": lambda: eng.bc([s]),
        "pagerank": lambda: eng.pagerank(5)}
