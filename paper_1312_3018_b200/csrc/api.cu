@@ -419,7 +419,10 @@ void gather_global(Engine& eng, const PartVals& pv, size_t elem, uint64_t g0, ui
 }
 
 uint64_t reached(Engine& eng, bool bitmap, uint64_t* nreached) {
-  DevBuf<unsigned long long> acc(2);
+  // persistent accumulator: a per-call cudaMalloc / cudaFree would synchronize
+  // the whole device (including result copies in flight on copy_stream)
+  if (!eng.reach_acc.n) eng.reach_acc.alloc(2);
+  DevBuf<unsigned long long>& acc = eng.reach_acc;
   TG_CK(cudaMemsetAsync(acc.get(), 0, 16, eng.stream));
   for (auto& pp : eng.parts) {
     Part& p = *pp;

@@ -250,6 +250,7 @@ struct Engine {
   // the engine stream, then copied to the host on copy_stream while the next
   // algorithm already computes; tg_engine_sync waits for the copies.  A
   // staging buffer is reused only after its previous copy finished (event).
+  DevBuf<unsigned long long> reach_acc;  // reached-vertex statistics (api.cu reached)
   bool async_collect = false;
   cudaStream_t copy_stream = nullptr;
   DevBuf<uint8_t> stage2[2];
