@@ -99,6 +99,50 @@ struct CcRevOp {  // in-CSR local rows: v active, entries = local sources u
   }
 };
 
+// Referencing side of the reverse exchange as a walker over the outbox rows of
+// the in-CSR (rows Vp + s, tiles over every in-CSR row): a slot whose owner
+// published a label (ghost != INF) is an active row with Aux = that label, and
+// lowers the row's local sources.  Replaces a warp per slot, which left 31
+// lanes idle on the typical 1-2-entry outbox row and visited every slot.
+struct CcGhostOp {
+  using Aux = uint32_t;
+  static constexpr bool kReduce = false, kFilter = false;
+  const uint32_t* in_col;
+  uint32_t* label;
+  uint32_t* next;
+  const uint32_t* ghost;  // [S] published labels (INF = none)
+  uint32_t Vp;
+  __device__ __forceinline__ Aux aux(uint32_t r) const { return r >= Vp ? ghost[r - Vp] : kInf; }
+  static constexpr bool kSplit = true;
+  static constexpr int kUnroll = 4;
+  struct Pre {
+    uint32_t u;
+  };
+  struct St {
+    uint32_t cur;
+  };
+  __device__ __forceinline__ Pre pre(uint64_t e) const { return {__ldcs(in_col + e)}; }
+  __device__ __forceinline__ St st(const Pre& p) const { return {label[p.u]}; }
+  __device__ __forceinline__ void fin(const Aux& l, const Pre& p, const St& q) const {
+    if (l < q.cur) {
+      atomicMin(&label[p.u], l);
+      atomicOr(&next[p.u >> 5], 1u << (p.u & 31));
+    }
+  }
+};
+
+// active rows of the whole in-CSR [0, Vp + S) for CcGhostOp: outbox rows
+// whose ghost holds a label (thread per row, one ballot per word)
+__global__ void k_cc_ext(const uint32_t* ghost, uint64_t Vp, uint64_t R, uint32_t* ext) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t n = (R + 31) / 32 * 32;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < n; r += stride) {
+    const bool b = r >= Vp && r < R && ghost[r - Vp] != kInf;
+    const uint32_t m = __ballot_sync(0xffffffffu, b);
+    if ((threadIdx.x & 31) == 0) ext[r >> 5] = m;
+  }
+}
+
 // labels = global ids; every vertex active (next = all ones over [0, Vp))
 __global__ void k_cc_init(const uint32_t* global_of, uint64_t Vp, uint32_t* label, uint32_t* next) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -185,6 +229,8 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
   const bool trace = direction_policy(eng).trace;
   uint64_t bm_bytes = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
+  // TG_CC_GHOST_WARP=1: the round-1 warp-per-slot ghost pass (A/B)
+  const bool ghost_warp = std::getenv("TG_CC_GHOST_WARP") && std::getenv("TG_CC_GHOST_WARP")[0] == '1';
   time_begin(eng);
   for (auto& pp : eng.parts) {
     Part& p = *pp;
@@ -252,7 +298,27 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
               f.vals.get(), f.next.get());
           eng.launches++;
         }
-        if (p.S) {
+        TG_CK(cudaGetLastError());
+      }
+      eng.prof_end(TG_K_EXCHANGE);
+      // reverse direction, referencing side: published labels lower the local
+      // sources of the outbox rows (compute on the received ghosts)
+      for (auto& pp : eng.parts) {
+        Part& p = *pp;
+        FrontierState& f = p.fs;
+        if (p.S && p.in_all_ntiles && !ghost_warp) {
+          const uint64_t R = p.Vp + p.S;
+          if (p.bcs.ext.n < words_for(R)) p.bcs.ext.alloc(words_for(R));
+          const uint32_t* gh = reinterpret_cast<const uint32_t*>(p.arena_rev.get());
+          k_cc_ext<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(gh, p.Vp, R, p.bcs.ext.get());
+          TG_CK(cudaGetLastError());
+          eng.launches++;
+          launch_mark_tiles(eng, in_all_tiles(p), R, p.bcs.ext.get(), p.ts_in);
+          launch_compact(eng, p.ts_in);
+          CcGhostOp gop{p.in_col.get(), f.vals.get(), f.next.get(), gh, (uint32_t)p.Vp};
+          launch_expand_on(eng, in_all_tiles(p), p.ts_in, p.bcs.ext.get(), gop, TG_K_CC_EXPAND,
+                           f.counters.get() + 1);
+        } else if (p.S) {
           k_cc_ghost<<<grid_for(p.S * 32, 256, 148u * 16u), 256, 0, s>>>(
               reinterpret_cast<const uint32_t*>(p.arena_rev.get()), p.S, p.Vp, p.in_off.get(),
               p.in_col.get(), f.vals.get(), f.next.get(), f.counters.get() + 1);
@@ -260,7 +326,6 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
         }
         TG_CK(cudaGetLastError());
       }
-      eng.prof_end(TG_K_EXCHANGE);
     }
     for (auto& pp : eng.parts) {
       Part& p = *pp;

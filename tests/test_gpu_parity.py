@@ -239,7 +239,8 @@ def test_set_exchange_rejects_unknown_mode(tg):
 
 @pytest.mark.parametrize("variant", [("TG_PR_SEG", "1"), ("TG_PR_L1", "2"), ("TG_PR_L1", "3"),
                                      ("TG_SSSP_DENSE_DIV", "64"), ("TG_BC_HUBPULL", "0"),
-                                     ("TG_BC_HUBPULL", "64"), ("TG_STAGE_ROWOFF", "1")])
+                                     ("TG_BC_HUBPULL", "64"), ("TG_STAGE_ROWOFF", "1"),
+                                     ("TG_CC_GHOST_WARP", "1"), ("TG_CC_GHOST_WARP", "0")])
 @pytest.mark.parametrize("P", [1, 3])
 def test_kernel_variants_same_result(tg, variant, P, monkeypatch):
     """The A/B kernel variants behind run-time switches
@@ -253,6 +254,7 @@ def test_kernel_variants_same_result(tg, variant, P, monkeypatch):
     eng = tg.Engine.from_edges(V, src, dst, w, partitions=P)
     srcs = inputs.list_sources(src, 3)
     check_all(tg, G, eng, bfs_src=srcs, sssp_src=srcs[:2], pr_T=(5,), bc_src=srcs[:2])
+    assert np.array_equal(eng.cc()[0], G.cc())
 
 
 @pytest.mark.parametrize("mode", ["top", "bottom", "auto"])
