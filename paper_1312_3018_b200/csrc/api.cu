@@ -65,6 +65,11 @@ void Engine::locate(uint64_t g, int* p, uint32_t* l) const {
 }
 
 void ensure_frontier_state(Engine& eng) {
+  if (!eng.ctr_all.n) {
+    eng.ctr_all.alloc(8 * std::max<size_t>(eng.parts.size(), 1));
+    TG_CK(cudaMemset(eng.ctr_all.get(), 0, eng.ctr_all.bytes()));
+    for (size_t i = 0; i < eng.parts.size(); ++i) eng.parts[i]->fs.counters = {eng.ctr_all.get() + 8 * i, 8};
+  }
   for (auto& pp : eng.parts) {
     Part& p = *pp;
     FrontierState& f = p.fs;
@@ -79,8 +84,6 @@ void ensure_frontier_state(Engine& eng) {
     f.obox_new.alloc(sw);
     f.obox_u32.alloc(std::max<uint64_t>(p.S, 1));
     (void)iw;
-    f.counters.alloc(8);
-    TG_CK(cudaMemset(f.counters.get(), 0, 8 * sizeof(unsigned long long)));
     p.ts.ensure(p.ntiles);
     if (p.in_ntiles || p.in_all_ntiles) p.ts_in.ensure(std::max(p.in_ntiles, p.in_all_ntiles));
   }
@@ -190,8 +193,7 @@ void fused_reset(Engine& eng, int byte, size_t elem) {
 
 unsigned long long read_counts(Engine& eng, int idx) {
   const int P = (int)eng.parts.size();
-  for (int i = 0; i < P; ++i)
-    TG_CK(cudaMemcpyAsync(eng.h_counts + i, eng.parts[i]->fs.counters.get() + idx, 8,
+  TG_CK(cudaMemcpy2DAsync(eng.h_counts, 8, eng.ctr_all.get() + idx, 64, 8, P,
                           cudaMemcpyDeviceToHost, eng.stream));
   TG_CK(cudaStreamSynchronize(eng.stream));
   uint64_t t = 0;
@@ -206,9 +208,8 @@ Vote read_vote(Engine& eng) {
   // (counter read + cross-process reduction)
   TG_CK(cudaStreamSynchronize(eng.stream));
   const auto t0 = std::chrono::steady_clock::now();
-  for (int i = 0; i < P; ++i)
-    TG_CK(cudaMemcpyAsync(eng.h_counts + 6 * i, eng.parts[i]->fs.counters.get(), 48,
-                          cudaMemcpyDeviceToHost, eng.stream));
+  TG_CK(cudaMemcpy2DAsync(eng.h_counts, 48, eng.ctr_all.get(), 64, 48, P, cudaMemcpyDeviceToHost,
+                          eng.stream));
   TG_CK(cudaStreamSynchronize(eng.stream));
   Vote v;
   v.minval = ~0ull;
@@ -234,7 +235,7 @@ Vote read_vote(Engine& eng) {
 }
 
 void reset_vote(Engine& eng) {
-  for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get(), 0, 32, eng.stream));
+  TG_CK(cudaMemset2DAsync(eng.ctr_all.get(), 64, 0, 32, eng.parts.size(), eng.stream));
 }
 
 void time_begin(Engine& eng) { TG_CK(cudaEventRecord(eng.ev0, eng.stream)); }

@@ -126,7 +126,13 @@ struct FrontierState {  // BFS / SSSP / BC-forward (messages arrive in Part::are
   DevBuf<uint32_t> obox_mark, obox_new;           // bitmaps over outbox slots
   DevBuf<uint32_t> obox_u32;                      // SSSP / CC min-combined values
   DevBuf<uint32_t> ibox_u32;                      // CC: owner-packed labels (reverse send)
-  DevBuf<unsigned long long> counters;            // see Vote
+  // see Vote: 8 counters per partition, a view into Engine::ctr_all (all
+  // partitions contiguous, 64 B apart: one strided memset / copy per vote)
+  struct {
+    unsigned long long* p = nullptr;
+    size_t n = 0;
+    unsigned long long* get() const { return p; }
+  } counters;
 };
 
 struct BCState {
@@ -251,6 +257,7 @@ struct Engine {
   // algorithm already computes; tg_engine_sync waits for the copies.  A
   // staging buffer is reused only after its previous copy finished (event).
   DevBuf<unsigned long long> reach_acc;  // reached-vertex statistics (api.cu reached)
+  DevBuf<unsigned long long> ctr_all;    // vote counters of every hosted partition (8 each)
   bool async_collect = false;
   cudaStream_t copy_stream = nullptr;
   DevBuf<uint8_t> stage2[2];

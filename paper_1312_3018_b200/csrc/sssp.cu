@@ -211,7 +211,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   uint64_t mind = 0;  // smallest tentative distance among the active vertices
   for (;;) {
     reset_vote(eng);
-    for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get() + 5, 0xFF, 8, s));
+    TG_CK(cudaMemset2DAsync(eng.ctr_all.get() + 5, 64, 0xFF, 8, eng.parts.size(), s));
     const uint64_t th = delta ? mind + delta : (uint64_t)kInf;
     const uint32_t thresh = th >= (uint64_t)kInf ? kInf : (uint32_t)th;
     const bool dense = dense_div && frontier * dense_div > eng.V;

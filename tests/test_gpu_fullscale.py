@@ -5,7 +5,8 @@
    host, the oracle calls running side by side in forked children):
    BFS from the bench's first 2 sources and SSSP from the first, bit-exact;
    PageRank T = 5 per vertex within 1e-5 relative (every vertex, every round
-   through the recurrence); BC from the first source per vertex within 1e-4.
+   through the recurrence); BC from the first source per vertex within 1e-4;
+   connected components (union-find) label for label.
 2. Exact O(E) certificates (oracle_*_cert_edges over the regenerated edge
    stream) for BFS and SSSP from the bench's first K sources (K = 4, or
    TG_C4_CERT_SOURCES): they hold iff the arrays equal the true hop / weighted
@@ -135,7 +136,12 @@ def test_full_oracle(full):
         tol = 1e-4 * np.abs(ref) + 1e-12 * max(1.0, float(np.abs(ref).max()))
         return ("bc", s0, int((np.abs(bc - ref) > tol).sum()))
 
-    jobs = [lambda: bfs_job(s0, lv0), sssp_job, pr_job, bc_job]
+    cc = full["cc"]
+
+    def cc_job():  # union-find over the oracle's CSR (NEXT-3 row, reading A29)
+        return ("cc", 0, bool(np.array_equal(cc, G.cc())))
+
+    jobs = [lambda: bfs_job(s0, lv0), sssp_job, pr_job, bc_job, cc_job]
     if lv1 is not None:
         jobs.append(lambda: bfs_job(s1, lv1))
     t1 = time.time()
@@ -143,7 +149,7 @@ def test_full_oracle(full):
     print(f"full oracle RMAT-{scale}: CSR {t_csr:.0f} s, algorithms {time.time() - t1:.0f} s "
           f"(side by side): {res}")
     for kind, arg, val in res:
-        if kind in ("bfs", "sssp"):
+        if kind in ("bfs", "sssp", "cc"):
             assert val, f"{kind} from {arg} differs from the oracle"
         elif kind == "pagerank":
             assert val <= 1e-5, f"PageRank max rel err {val:.3e}"
