@@ -837,6 +837,9 @@ void setup_peers(Engine& eng) {
     TG_CK(cudaMemcpy(p.rin_delta.get(), idelta.data(), eng.P * sizeof(int64_t), cudaMemcpyHostToDevice));
   }
   if (const char* f = std::getenv("TG_FUSED_EXCHANGE")) eng.fused = f[0] != '0' && eng.peer_atomics;
+  // the tables above were copied from pageable host memory on the legacy
+  // stream: make sure they landed before any engine-stream kernel reads them
+  TG_CK(cudaDeviceSynchronize());
 }
 
 void map_remote_peers(Engine& eng) {
@@ -904,10 +907,14 @@ void map_remote_peers(Engine& eng) {
   uint64_t room = me.Vp >= (uint64_t)(4 + eng.world) ? 1 : 0;
   comm_allreduce(eng, &room, 1, 1);
   if (ok && room && !(std::getenv("TG_PEER_PROBE") && std::getenv("TG_PEER_PROBE")[0] == '0')) {
-    cudaStream_t s = eng.stream;
     std::vector<unsigned long long> init(4 + eng.world, 0);
     init[2] = 0xFFFFFFFFull;
-    TG_CK(cudaMemcpy(me.staging.get(), init.data(), init.size() * 8, cudaMemcpyHostToDevice));
+    // stream-ordered and drained before the barrier: a plain cudaMemcpy from
+    // pageable memory may still be in flight when it returns, and would then
+    // overwrite a peer's early probe writes
+    cudaStream_t s = eng.stream;
+    TG_CK(cudaMemcpyAsync(me.staging.get(), init.data(), init.size() * 8, cudaMemcpyHostToDevice, s));
+    TG_CK(cudaStreamSynchronize(s));
     comm_barrier(eng);
     std::vector<uint8_t*> st(eng.world, nullptr);
     for (int q = 0; q < eng.world; ++q) st[q] = eng.peers[q].staging;
