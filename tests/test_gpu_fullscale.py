@@ -6,7 +6,8 @@
    BFS from the bench's first 2 sources and SSSP from the first, bit-exact;
    PageRank T = 5 per vertex within 1e-5 relative (every vertex, every round
    through the recurrence); BC from the first source per vertex within 1e-4;
-   connected components (union-find) label for label.
+   with TG_C4_CC=1 also connected components (union-find) label for label
+   (opt-in: one thread over 2^32 random finds does not fit the suite budget).
 2. Exact O(E) certificates (oracle_*_cert_edges over the regenerated edge
    stream) for BFS and SSSP from the bench's first K sources (K = 4, or
    TG_C4_CERT_SOURCES): they hold iff the arrays equal the true hop / weighted
@@ -141,7 +142,9 @@ def test_full_oracle(full):
     def cc_job():  # union-find over the oracle's CSR (NEXT-3 row, reading A29)
         return ("cc", 0, bool(np.array_equal(cc, G.cc())))
 
-    jobs = [lambda: bfs_job(s0, lv0), sssp_job, pr_job, bc_job, cc_job]
+    jobs = [lambda: bfs_job(s0, lv0), sssp_job, pr_job, bc_job]
+    if os.environ.get("TG_C4_CC") == "1":  # single-threaded union-find over 2^32 edges: opt-in
+        jobs.append(cc_job)
     if lv1 is not None:
         jobs.append(lambda: bfs_job(s1, lv1))
     t1 = time.time()
