@@ -57,10 +57,30 @@ uint64_t Engine::device_bytes() const {
   return t;
 }
 
+namespace {
+__global__ void k_to_host(const unsigned long long* src, int n, int stride, int off,
+                          unsigned long long* dst) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[(size_t)i * stride + off];
+}
+__global__ void k_to_host_u32(const uint32_t* src, unsigned long long* dst) { dst[0] = src[0]; }
+}  // namespace
+
+const volatile unsigned long long* to_host(Engine& eng, const unsigned long long* src, int n,
+                                           int stride, int off) {
+  k_to_host<<<1, 64, 0, eng.stream>>>(src, n, stride, off, eng.d_counts);
+  TG_CK(cudaGetLastError());
+  TG_CK(cudaStreamSynchronize(eng.stream));
+  return eng.h_counts;
+}
+
 void Engine::locate(uint64_t g, int* p, uint32_t* l) const {
   TG_REQUIRE(g < V, TG_EINVAL, "source vertex " + std::to_string(g) + " >= V");
-  uint32_t i = 0;
-  TG_CK(cudaMemcpy(&i, rank_of.get() + g, 4, cudaMemcpyDeviceToHost));
+  // the position is read through the mapped scratch (a kernel store), not a
+  // DMA copy that could queue behind an asynchronous result copy
+  k_to_host_u32<<<1, 1, 0, stream>>>(rank_of.get() + g, d_counts);
+  TG_CK(cudaGetLastError());
+  TG_CK(cudaStreamSynchronize(stream));
+  const uint32_t i = (uint32_t)((const volatile unsigned long long*)h_counts)[0];
   deal(i, P, p, l);
 }
 
@@ -193,11 +213,9 @@ void fused_reset(Engine& eng, int byte, size_t elem) {
 
 unsigned long long read_counts(Engine& eng, int idx) {
   const int P = (int)eng.parts.size();
-  TG_CK(cudaMemcpy2DAsync(eng.h_counts, 8, eng.ctr_all.get() + idx, 64, 8, P,
-                          cudaMemcpyDeviceToHost, eng.stream));
-  TG_CK(cudaStreamSynchronize(eng.stream));
+  const volatile unsigned long long* h = to_host(eng, eng.ctr_all.get(), P, 8, idx);
   uint64_t t = 0;
-  for (int i = 0; i < P; ++i) t += eng.h_counts[i];
+  for (int i = 0; i < P; ++i) t += h[i];
   comm_allreduce(eng, &t, 1, 0);
   return t;
 }
@@ -208,17 +226,18 @@ Vote read_vote(Engine& eng) {
   // (counter read + cross-process reduction)
   TG_CK(cudaStreamSynchronize(eng.stream));
   const auto t0 = std::chrono::steady_clock::now();
-  TG_CK(cudaMemcpy2DAsync(eng.h_counts, 48, eng.ctr_all.get(), 64, 48, P, cudaMemcpyDeviceToHost,
-                          eng.stream));
-  TG_CK(cudaStreamSynchronize(eng.stream));
+  // the partitions' counters land in mapped host memory by a kernel store
+  // (the paper's host-resident vote flag)
+  const volatile unsigned long long* h = to_host(eng, eng.ctr_all.get(), 8 * P);
   Vote v;
   v.minval = ~0ull;
   for (int i = 0; i < P; ++i) {
-    v.count += eng.h_counts[6 * i];
-    v.edges += eng.h_counts[6 * i + 1];
-    v.degsum += eng.h_counts[6 * i + 2];
-    v.indegsum += eng.h_counts[6 * i + 3];
-    v.minval = std::min<unsigned long long>(v.minval, eng.h_counts[6 * i + 5]);
+    v.count += h[8 * i];
+    v.edges += h[8 * i + 1];
+    v.degsum += h[8 * i + 2];
+    v.indegsum += h[8 * i + 3];
+    const unsigned long long mn = h[8 * i + 5];
+    v.minval = std::min<unsigned long long>(v.minval, mn);
   }
   if (eng.multi()) {  // the global vote: sums + the minimum, one reduction
     uint64_t x[5] = {v.count, v.edges, v.degsum, v.indegsum, v.minval};
@@ -436,9 +455,8 @@ uint64_t reached(Engine& eng, bool bitmap, uint64_t* nreached) {
                                                                  p.Vp, acc.get());
   }
   TG_CK(cudaGetLastError());
-  uint64_t h[2];
-  TG_CK(cudaMemcpyAsync(h, acc.get(), 16, cudaMemcpyDeviceToHost, eng.stream));
-  TG_CK(cudaStreamSynchronize(eng.stream));
+  const volatile unsigned long long* hv = to_host(eng, acc.get(), 2);
+  uint64_t h[2] = {hv[0], hv[1]};
   comm_allreduce(eng, h, 2, 0);
   if (nreached) *nreached = h[1];
   return h[0];
@@ -606,7 +624,9 @@ static void init_engine(Engine& eng, const tg_attr* attr) {
   TG_CK(cudaStreamCreateWithFlags(&eng.stream, cudaStreamNonBlocking));
   TG_CK(cudaEventCreate(&eng.ev0));
   TG_CK(cudaEventCreate(&eng.ev1));
-  TG_CK(cudaMallocHost(&eng.h_counts, sizeof(unsigned long long) * TG_MAX_PARTITIONS * 8));
+  TG_CK(cudaHostAlloc(&eng.h_counts, sizeof(unsigned long long) * TG_MAX_PARTITIONS * 8,
+                      cudaHostAllocMapped | cudaHostAllocPortable));
+  TG_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&eng.d_counts), eng.h_counts, 0));
   // L2 set-aside for persisting accesses: measured slower on RMAT-28 (the
   // set-aside starves the rest of the working set), so opt-in only
   // (TG_L2_WINDOW=1).

@@ -268,7 +268,11 @@ struct Engine {
   uint64_t build_ms = 0;
   uint64_t launches = 0;     // kernels launched by the current run
   uint64_t comm_bytes = 0;   // message bytes exchanged by the current run
-  unsigned long long* h_counts = nullptr;  // pinned host scratch (TG_MAX_PARTITIONS * 4)
+  unsigned long long* h_counts = nullptr;  // pinned, MAPPED host scratch (TG_MAX_PARTITIONS * 8)
+  unsigned long long* d_counts = nullptr;  // its device alias: small results (votes, source
+                                           // placement, statistics) are written there by a
+                                           // kernel, not read back with a DMA copy, so they never
+                                           // queue behind a result copy on the copy engines
   // kernel ledger (tg_engine_set_profiling)
   bool prof = false;
   tg_kernel_stat kstat[TG_K_COUNT] = {};
@@ -347,6 +351,10 @@ void collect(Engine& eng, ValsOf vals, size_t elem, void* out, int mem);
 void comm_allreduce(Engine& eng, uint64_t* data, int n, int op);  // op 0 sum, 1 min
 void comm_barrier(Engine& eng);
 void ensure_frontier_state(Engine& eng);
+// copy n u64 words (src[i * stride + off]) into the mapped host scratch with a
+// kernel on the engine stream, wait for the stream, return the host view
+const volatile unsigned long long* to_host(Engine& eng, const unsigned long long* src, int n,
+                                           int stride = 1, int off = 0);
 // read the per-partition counters[idx] (one sync) and return their sum
 unsigned long long read_counts(Engine& eng, int idx);
 // counters layout: [0] new-frontier count (advance), [1] edges processed by the
