@@ -96,7 +96,11 @@ void tg_hostcomm_free(tg_hostcomm* h);
  *       device exercises the full outbox/inbox machinery in one process.
  *   device: CUDA device ordinal.
  *   weighted: 1 to keep per-edge SSSP weights (required by tg_sssp).
- *   build_in_csr: 1 to build the in-edge CSR used by tg_pagerank (pull).
+ *   build_in_csr: 1 to build the in-edge CSR used by tg_pagerank (pull);
+ *       2 = in-CSR only: the out-CSR is released after the build, so only
+ *       tg_pagerank runs (the others return TG_EINVAL) -- for a graph whose
+ *       two CSRs do not fit one device (RMAT-30 PageRank on one B200);
+ *       single-process engines only.
  *   rank, world: multi-process engine (world > 1): this process hosts
  *       partition `rank` of `world` (num_partitions must be 1); every process
  *       makes the same calls in the same order (SPMD), results are written on

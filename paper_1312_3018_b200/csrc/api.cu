@@ -620,7 +620,12 @@ static void init_engine(Engine& eng, const tg_attr* attr) {
   TG_CK(cudaSetDevice(eng.device));
   eng.P = world > 1 ? world : attr->num_partitions;
   eng.weighted = attr->weighted != 0;
+  TG_REQUIRE(attr->build_in_csr >= 0 && attr->build_in_csr <= 2, TG_EINVAL,
+             "tg_attr.build_in_csr must be 0, 1 or 2");
   eng.has_in = attr->build_in_csr != 0;
+  eng.in_only = attr->build_in_csr == 2;
+  TG_REQUIRE(!eng.in_only || attr->world <= 1, TG_EINVAL,
+             "build_in_csr = 2 (in-CSR only) is single-process");
   TG_CK(cudaStreamCreateWithFlags(&eng.stream, cudaStreamNonBlocking));
   TG_CK(cudaEventCreate(&eng.ev0));
   TG_CK(cudaEventCreate(&eng.ev1));
@@ -831,15 +836,24 @@ int tg_engine_partition_info(const tg_engine* e, int p, tg_part_info* info, uint
 // NULL outputs are rejected inside run_* except on non-root ranks of a
 // multi-process engine (results are written on rank 0 only).
 int tg_bfs(tg_engine* e, uint64_t source, uint32_t* levels, int mem, tg_stats* user_st) {
-  TG_RUN({ run_bfs(eng, source, levels, mem, st); });
+  TG_RUN({
+    TG_REQUIRE(!eng.in_only, TG_EINVAL, "engine holds the in-CSR only (build_in_csr = 2): PageRank only");
+    run_bfs(eng, source, levels, mem, st);
+  });
 }
 
 int tg_sssp(tg_engine* e, uint64_t source, uint32_t* dist, int mem, tg_stats* user_st) {
-  TG_RUN({ run_sssp(eng, source, dist, mem, st); });
+  TG_RUN({
+    TG_REQUIRE(!eng.in_only, TG_EINVAL, "engine holds the in-CSR only (build_in_csr = 2): PageRank only");
+    run_sssp(eng, source, dist, mem, st);
+  });
 }
 
 int tg_cc(tg_engine* e, uint32_t* labels, int mem, tg_stats* user_st) {
-  TG_RUN({ run_cc(eng, labels, mem, st); });
+  TG_RUN({
+    TG_REQUIRE(!eng.in_only, TG_EINVAL, "engine holds the in-CSR only (build_in_csr = 2): PageRank only");
+    run_cc(eng, labels, mem, st);
+  });
 }
 
 int tg_pagerank(tg_engine* e, int iterations, double damping, float* rank, int mem,
@@ -848,7 +862,10 @@ int tg_pagerank(tg_engine* e, int iterations, double damping, float* rank, int m
 }
 
 int tg_bc(tg_engine* e, const uint64_t* sources, int k, double* bc, int mem, tg_stats* user_st) {
-  TG_RUN({ run_bc(eng, sources, k, bc, mem, st); });
+  TG_RUN({
+    TG_REQUIRE(!eng.in_only, TG_EINVAL, "engine holds the in-CSR only (build_in_csr = 2): PageRank only");
+    run_bc(eng, sources, k, bc, mem, st);
+  });
 }
 
 int tg_engine_set_profiling(tg_engine* e, int on) {

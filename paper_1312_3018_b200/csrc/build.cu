@@ -1085,6 +1085,17 @@ void build_engine(Engine& eng, const EdgeInput& in) {
     pt->staging.alloc(std::max<uint64_t>(pt->Vp, 1) * 8);
   }
   TG_CK(cudaStreamSynchronize(s));
+  if (eng.in_only)  // PageRank-only engine: its pull needs the in-CSR and outdeg only
+    for (auto& pt : eng.parts) {
+      pt->col.release();
+      pt->w.release();
+      pt->w8.release();
+      pt->tile_vf.release();
+      pt->tile_vl.release();
+      pt->in_all_vf.release();
+      pt->in_all_vl.release();
+      pt->ntiles = pt->in_all_ntiles = 0;
+    }
   setup_peers(eng);
   eng.build_ms = (uint64_t)std::chrono::duration_cast<std::chrono::milliseconds>(
                      std::chrono::steady_clock::now() - t0)

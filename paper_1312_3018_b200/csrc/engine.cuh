@@ -241,6 +241,9 @@ struct Engine {
   std::vector<PeerView> peers;  // indexed by partition id (all P)
   uint64_t V = 0, E = 0;
   bool weighted = false, has_in = false;
+  // tg_attr.build_in_csr == 2: the out-CSR is released after the build (only
+  // the pull PageRank runs; graphs whose two CSRs do not fit one GPU, C5)
+  bool in_only = false;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // fork/join side streams (independent kernels of one phase run concurrently,

@@ -193,3 +193,47 @@ def test_rmat30_bfs_certificate_one_gpu():
     assert cert.holds()
     print(f"RMAT-30 BFS: {st.device_ms:.1f} ms, supersteps {st.supersteps}, "
           f"{st.traversed_edges / st.device_ms / 1e6:.1f} GTEPS")
+
+
+@pytest.mark.skipif(os.environ.get("TG_RMAT30") != "1",
+                    reason="RMAT-30 PageRank (2^34 edges, ~20 min of host checks): TG_RMAT30=1")
+def test_rmat30_pagerank_one_gpu():
+    """BASELINE configs[4]'s PageRank on ONE B200: an in-CSR-only engine
+    (build_in_csr = 2: the out-CSR is released after the build) runs 5 rounds;
+    the oracle recomputes round 5 from the GPU's round-4 ranks on a vertex
+    sample (the 256 highest in-degrees + 8192 random vertices) over the
+    regenerated 2^34-edge stream (1e-5 relative), plus the mass identity."""
+    import paper_1312_3018_b200 as tg
+
+    scale = 30
+    V, E = 1 << scale, 16 << scale
+    eng = tg.Engine.rmat(scale, weighted=False, in_csr=2)
+    r4, _ = eng.pagerank(4)
+    r4 = r4.copy()
+    r5, st = eng.pagerank(5)
+    eng.close()
+    outdeg = np.zeros(V, np.uint32)
+    indeg = np.zeros(V, np.uint32)
+    chunk = 1 << 28
+    for first in range(0, E, chunk):
+        src, dst, _ = inputs.rmat_edges(scale, first=first, count=min(chunk, E - first))
+        oracle.outdeg_edges(V, src, outdeg)
+        oracle.outdeg_edges(V, dst, indeg)
+    rng = np.random.default_rng(2024)
+    sample = np.unique(np.concatenate([np.argsort(indeg)[-256:], rng.integers(0, V, 8192)]))
+    mask = np.zeros((V + 63) // 64, np.uint64)
+    np.bitwise_or.at(mask, sample >> 6, np.uint64(1) << (sample & 63).astype(np.uint64))
+    slot = np.zeros(V, np.uint32)
+    slot[sample] = np.arange(len(sample), dtype=np.uint32)
+    acc = np.zeros(len(sample))
+    for first in range(0, E, chunk):
+        src, dst, _ = inputs.rmat_edges(scale, first=first, count=min(chunk, E - first))
+        oracle.pr_sample_edges(V, src, dst, mask, slot, r4, outdeg, acc)
+    d = 0.85
+    pred = (1 - d) / V + d * acc
+    rel = np.abs(r5[sample].astype(np.float64) - pred) / pred
+    assert rel.max() <= 1e-5, rel.max()
+    mass_pred = (1 - d) + d * r4[outdeg > 0].astype(np.float64).sum()
+    assert abs(r5.astype(np.float64).sum() - mass_pred) <= 1e-5 * mass_pred
+    print(f"RMAT-30 PageRank: {st.device_ms / 5:.1f} ms per round, "
+          f"{E * 5 / st.device_ms / 1e6:.1f} G edges/s, sample max rel err {rel.max():.2e}")

@@ -567,3 +567,22 @@ def test_async_host_collection(tg):
     eng.set_async_collect(False)
     assert np.array_equal(eng.bfs(srcs[0])[0], G.bfs(srcs[0]))
     eng.close()
+
+
+def test_in_csr_only_engine(tg):
+    """build_in_csr = 2 (the out-CSR released after the build): PageRank matches
+    the oracle at P = 1; the frontier algorithms refuse with TG_EINVAL."""
+    scale = 12
+    src, dst, _ = inputs.rmat_edges(scale)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst)
+    eng = tg.Engine.from_edges(V, src, dst, in_csr=2)
+    assert_pr(eng.pagerank(5)[0], G.pagerank(5))
+    for call in (lambda: eng.bfs(0), lambda: eng.sssp(0), lambda: eng.bc([0]), lambda: eng.cc()):
+        with pytest.raises(tg.TGraphError) as e:
+            call()
+        assert e.value.code == tg.tgraph.TG_EINVAL
+    full = tg.Engine.from_edges(V, src, dst)
+    assert eng.info["device_bytes"] < full.info["device_bytes"]
+    eng.close()
+    full.close()
