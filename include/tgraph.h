@@ -341,6 +341,16 @@ int tg_engine_set_exchange(tg_engine* eng, int mode);
 enum { TG_PR_PUSH = 0, TG_PR_PULL = 1 };
 int tg_engine_set_pagerank_comm(tg_engine* eng, int mode);
 
+/* The SM -> die map of a two-die GPU (B200: each die's half of the L2 caches
+ * the lines its own SMs read), measured once per device by a pointer-chase
+ * latency probe (dies.cu) and cached.  PageRank's die split (pagerank.cu)
+ * uses it to give each die's SMs their own half of the gathered sources.
+ * die_of (host, cap entries, may be NULL) receives die 0 / 1 per SM id;
+ * *nsm the SM count; *ok = 1 if two clear latency clusters were found (0: a
+ * one-die part or an unclear probe -> no die split).  TG_EINVAL for a bad
+ * device or NULL nsm / ok. */
+int tg_device_die_map(int device, uint8_t* die_of, int cap, int* nsm, int* ok);
+
 /* Asynchronous result collection into HOST memory (single-process engines;
  * the collection step of P:902-913, outside the paper's timed scope).  With
  * on = 1, an algorithm call that writes a host output array returns once its

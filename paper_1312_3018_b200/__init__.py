@@ -33,6 +33,7 @@ from .tgraph import (  # noqa: F401
     tg_engine_partition_info,
     tg_engine_set_exchange,
     tg_engine_set_pagerank_comm,
+    tg_device_die_map,
     tg_pagerank,
     tg_rmat_edges,
     tg_sssp,

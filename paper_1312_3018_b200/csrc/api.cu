@@ -911,6 +911,20 @@ int tg_engine_sync(tg_engine* e) {
   });
 }
 
+int tg_device_die_map(int device, uint8_t* die_of, int cap, int* nsm, int* ok) {
+  return guard([&] {
+    TG_REQUIRE(nsm != nullptr && ok != nullptr, TG_EINVAL, "tg_device_die_map: NULL output");
+    int nd = 0;
+    TG_CK(cudaGetDeviceCount(&nd));
+    TG_REQUIRE(device >= 0 && device < nd, TG_EINVAL, "tg_device_die_map: bad device");
+    const DieMap& m = die_map(device);
+    *nsm = m.nsm;
+    *ok = m.ok ? 1 : 0;
+    if (die_of)
+      for (int i = 0; i < cap && i < (int)m.h_die_of.size(); ++i) die_of[i] = m.h_die_of[i];
+  });
+}
+
 int tg_engine_set_pagerank_comm(tg_engine* e, int mode) {
   return guard([&] {
     TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");

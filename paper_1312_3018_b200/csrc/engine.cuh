@@ -81,11 +81,68 @@ struct RemoteOut {
   }
 };
 
+// PageRank hub split (pagerank.cu, TG_PR_HUB): the in-edges of the CTA- and
+// warp-class rows whose source is one of the K hubs (local ids [0, K): the
+// out-degree order puts them first) are summed by a separate pass from a
+// shared-memory replica of contrib[0, K) -- an LDS instead of a random L2
+// request -- and the class pulls start each of those rows after its hub prefix.
+struct PRHub {
+  uint32_t K = 0;
+  const uint32_t* built_for = nullptr;  // the in-CSR column array it was built from
+  uint64_t n_list = 0;                  // CTA-class rows, then warp-class rows
+  uint64_t ntask = 0, H = 0;            // tasks (<= kHubChunk hub entries each), entries
+  DevBuf<uint32_t> hlen;                // [n_list] hub-prefix length of each list row
+  DevBuf<uint16_t> col;                 // [H] hub source ids, list-row order
+  DevBuf<uint64_t> t_off;               // [ntask] first entry of the task in col
+  DevBuf<uint32_t> t_len, t_k;          // [ntask] entries, list row
+  DevBuf<double> hsum;                  // [n_list] hub part of each list row's sum
+};
+
+// The two dies of a B200 each cache in their half of the L2 the lines their own
+// SMs read (profiles/r02_die_probe.txt: a 128 MB gather region runs at 118 G
+// loads/s when every SM reads all of it, 282 G/s when each die's SMs read only
+// their own 64 MB half).  DieMap is the SM -> die map measured at run time
+// (dies.cu): pointer-chase latency from every SM to lines the reference SM just
+// pulled into its L2.
+struct DieMap {
+  bool ok = false;            // two clear latency clusters were found
+  int nsm = 0, n[2] = {0, 0};
+  double lat_near = 0, lat_far = 0;  // cycles per chased line
+  DevBuf<uint8_t> die_of;     // [nsm] die of each SM id (device)
+  std::vector<uint8_t> h_die_of;
+};
+const DieMap& die_map(int device);  // measured once per device, cached
+
+// PageRank die split (pagerank.cu): the in-edges of every row are split by the
+// die that gathers their source -- source u belongs to die d(u), a hash of its
+// 128-byte line weighted by the dies' SM counts -- into two CSRs.  The SMs of
+// die d pull only over CSR d, so each die's L2 caches only its half of the hot
+// contributions; a finalize pass adds the two partial sums of every row.
+struct PRSplit {
+  bool built = false, on = false;
+  const uint32_t* built_for = nullptr;  // in-CSR column array it was built from
+  uint32_t thresh = 0;                  // d(u) = hash(u >> 5) >= thresh
+  uint64_t R = 0;
+  DevBuf<uint64_t> off[2];              // [R + 1]
+  DevBuf<uint32_t> col[2];              // sources of die d, each row ascending
+  DevBuf<uint32_t> wrow[2];             // rows with 32 <= half-degree < kSplitChunk
+  uint64_t n_w[2] = {0, 0};
+  DevBuf<uint32_t> c_row[2], c_k[2], c_len[2];  // chunks of the rows >= kSplitChunk
+  DevBuf<uint64_t> c_start[2];
+  DevBuf<uint32_t> c_list[2];           // those rows (k -> row)
+  uint64_t n_c[2] = {0, 0}, n_ck[2] = {0, 0};  // chunks, chunked rows
+  DevBuf<double> cacc[2];               // [n_ck] chunked-row sums (atomics)
+  DevBuf<float> psum[2];                // [R] partial sum of every row per die
+  DevBuf<unsigned long long> qnext;     // [2] task queues' next index
+};
+
 struct PRState {  // PageRank (local-id order)
   DevBuf<float> contrib[2];
   DevBuf<float> rank;
   DevBuf<double> acc;
   DevBuf<double> obox;  // partial sums per outbox slot (send)
+  PRHub hub;
+  PRSplit split;
 };
 
 // Ghost-pull PageRank (TOTEM_COMM_PULL):

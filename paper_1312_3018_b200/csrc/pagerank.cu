@@ -19,6 +19,8 @@
 // No vote: a fixed number of rounds.
 #include <cstdlib>
 
+#include <cub/cub.cuh>
+
 #include "frontier.cuh"
 
 namespace tg {
@@ -43,11 +45,29 @@ __device__ __forceinline__ double warp_sum(double x) {
 // only); 1 = the streamed in_col bypasses L1 (L1::no_allocate); 2 = 1 + cold
 // gathers (c >= hot) bypass L1 too, so L1 keeps hub contributions; 3 = 2 +
 // the hottest sources (c < l1hot) are L1::evict_last.
-template <int kL1>
+// Shared-memory replica of the hub prefix contrib[0, k) (TG_PR_REP A/B): a
+// gather of a source below k is an LDS instead of an L2 request.
+struct Rep {
+  const float* s;
+  uint32_t k;
+};
+
+// kL1 == 9: TIMING PROBE ONLY (wrong results): gathers of sources in
+// [c_xlo, c_xhi) are skipped, to measure what a source range costs
+// (TG_PR_L1=9, TG_PR_XLO / TG_PR_XHI; scripts/sweep_pr.py).
+__constant__ uint32_t c_xlo, c_xhi;
+
+template <int kL1, bool kRep = false>
 __device__ __forceinline__ float gather_one(const float* __restrict__ contrib, uint32_t c,
                                             uint32_t hot, uint64_t keep, uint64_t stream,
-                                            uint32_t l1hot) {
-  if constexpr (kL1 >= 2) {
+                                            uint32_t l1hot, Rep rep = {nullptr, 0}) {
+  if constexpr (kRep) {
+    if (c < rep.k) return rep.s[c];
+  }
+  if constexpr (kL1 == 9) {
+    if (c >= c_xlo && c < c_xhi) return 0.0f;
+    return ld_f32_hint(contrib + c, c < hot ? keep : stream);
+  } else if constexpr (kL1 >= 2) {
     if (c >= hot) return ld_f32_cold(contrib + c, stream);
     if constexpr (kL1 >= 3) {
       if (c < l1hot) return ld_f32_hot(contrib + c, keep);
@@ -58,18 +78,18 @@ __device__ __forceinline__ float gather_one(const float* __restrict__ contrib, u
   }
 }
 
-template <int kL1>
+template <int kL1, bool kRep = false>
 __device__ __forceinline__ double gather_sum(const uint32_t* __restrict__ in_col,
                                              const float* __restrict__ contrib, uint64_t i,
                                              uint64_t e, uint32_t step, uint32_t hot,
-                                             uint32_t l1hot) {
+                                             uint32_t l1hot, Rep rep = {nullptr, 0}) {
   const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
   auto col = [&](uint64_t j) {
     if constexpr (kL1 >= 1) return ld_u32_stream(in_col + j, stream);
     else return ld_u32_hint(in_col + j, stream);
   };
   auto gather_one = [&](const float* __restrict__ cb, uint32_t c, uint32_t h, uint64_t k,
-                        uint64_t st) { return tg::gather_one<kL1>(cb, c, h, k, st, l1hot); };
+                        uint64_t st) { return tg::gather_one<kL1, kRep>(cb, c, h, k, st, l1hot, rep); };
   double s0 = 0.0, s1 = 0.0;
   for (; i + 3ull * step < e; i += 4ull * step) {
     const uint32_t c0 = col(i), c1 = col(i + step);
@@ -98,6 +118,7 @@ struct PullOut {
   const uint32_t* outdeg;  // fused
   uint32_t hot;            // sources [0, hot) are gathered evict_last
   uint32_t l1hot;          // kL1 3: sources [0, l1hot) L1::evict_last
+  int npol;                // next contributions of rows < hot: 0 evict_last, 1 normal, 2 evict_first
   RemoteOut rout;          // remote: outbox sums go straight into the owner's inbox ...
   bool remote;
   int parity;              // ... double-buffered by round parity (arena slot = 2 x f64)
@@ -109,8 +130,9 @@ struct PullOut {
         st_f32_hint(rank + r, (float)rk, stream);
         const uint32_t od = outdeg[r];
         // next round's contributions: hubs stay evict_last like their gathers
-        st_f32_hint(contrib_next + r, od ? (float)(rk / (double)od) : 0.0f,
-                    r < hot ? l2_evict_last() : stream);
+        const float cn = od ? (float)(rk / (double)od) : 0.0f;
+        if (npol == 1 && r < hot) contrib_next[r] = cn;
+        else st_f32_hint(contrib_next + r, cn, (npol == 0 && r < hot) ? l2_evict_last() : stream);
       } else {
         acc[r] = sum;
       }
@@ -123,14 +145,18 @@ struct PullOut {
 };
 
 // one CTA per listed row (in-degree >= kPrCta)
+// Hub split (PRHub): hlen / hsum non-null -> the row's first hlen[k] in-edges
+// (sources < K) were summed by k_pull_hub into hsum[k]; start after them.
 template <int kL1>
 __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off,
                                                           const uint32_t* in_col,
                                                           const float* contrib,
-                                                          const uint32_t* rows, PullOut o) {
+                                                          const uint32_t* rows, PullOut o,
+                                                          const uint32_t* hlen,
+                                                          const double* hsum) {
   __shared__ double s_part[kCtaThreads / 32];
   const uint64_t r = rows[blockIdx.x];
-  const uint64_t b = in_off[r], e = in_off[r + 1];
+  const uint64_t b = in_off[r] + (hlen ? hlen[blockIdx.x] : 0u), e = in_off[r + 1];
   double sum = gather_sum<kL1>(in_col, contrib, b + threadIdx.x, e, kCtaThreads, o.hot, o.l1hot);
   sum = warp_sum(sum);
   if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = sum;
@@ -138,36 +164,52 @@ __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off
   if (threadIdx.x < 32) {
     double v = threadIdx.x < kCtaThreads / 32 ? s_part[threadIdx.x] : 0.0;
     v = warp_sum(v);
-    if (threadIdx.x == 0) o.put(r, v);
+    if (threadIdx.x == 0) o.put(r, v + (hsum ? hsum[blockIdx.x] : 0.0));
   }
 }
 
 // one warp per listed row (32 <= in-degree < kPrCta)
-template <int kL1>
-__global__ void __launch_bounds__(256) k_pull_warp(const uint64_t* in_off, const uint32_t* in_col,
+// kRep: 1024-thread CTAs holding the shared-memory replica of contrib[0, rep_k)
+template <bool kRep>
+__device__ __forceinline__ Rep load_rep(const float* contrib, uint32_t k) {
+  if constexpr (kRep) {
+    extern __shared__ float s_rep[];
+    for (uint32_t i = threadIdx.x; i < k; i += blockDim.x) s_rep[i] = contrib[i];
+    __syncthreads();
+    return {s_rep, k};
+  } else {
+    return {nullptr, 0};
+  }
+}
+
+template <int kL1, bool kRep = false>
+__global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_warp(const uint64_t* in_off, const uint32_t* in_col,
                                                    const float* contrib, const uint32_t* rows,
-                                                   uint64_t n, PullOut o) {
+                                                   uint64_t n, PullOut o, uint32_t rep_k,
+                                                   const uint32_t* hlen, const double* hsum) {
+  const Rep rep = load_rep<kRep>(contrib, rep_k);
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps) {
     const uint64_t r = rows[k];
-    const uint64_t b = in_off[r], e = in_off[r + 1];
-    double sum = gather_sum<kL1>(in_col, contrib, b + lane, e, 32, o.hot, o.l1hot);
+    const uint64_t b = in_off[r] + (hlen ? hlen[k] : 0u), e = in_off[r + 1];
+    double sum = gather_sum<kL1, kRep>(in_col, contrib, b + lane, e, 32, o.hot, o.l1hot, rep);
     sum = warp_sum(sum);
-    if (lane == 0) o.put(r, sum);
+    if (lane == 0) o.put(r, sum + (hsum ? hsum[k] : 0.0));
   }
 }
 
 // one thread per row of [r0, r1) with in-degree < 32 (incl. 0); others skipped
-template <int kL1>
-__global__ void __launch_bounds__(256) k_pull_thread(const uint64_t* in_off, const uint32_t* in_col,
+template <int kL1, bool kRep = false>
+__global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_thread(const uint64_t* in_off, const uint32_t* in_col,
                                                      const float* contrib, uint64_t r0, uint64_t r1,
-                                                     PullOut o) {
+                                                     PullOut o, uint32_t rep_k = 0) {
+  const Rep rep = load_rep<kRep>(contrib, rep_k);
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < r1; r += stride) {
     const uint64_t b = in_off[r], e = in_off[r + 1];
     if (e - b >= 32) continue;
-    o.put(r, gather_sum<kL1>(in_col, contrib, b, e, 1, o.hot, o.l1hot));
+    o.put(r, gather_sum<kL1, kRep>(in_col, contrib, b, e, 1, o.hot, o.l1hot, rep));
   }
 }
 
@@ -240,6 +282,119 @@ __global__ void __launch_bounds__(256) k_pull_seg(const uint64_t* in_off, const 
   }
 }
 
+// ---------------------------------------------------------------- hub split
+constexpr uint32_t kHubThreads = 1024;
+constexpr uint32_t kHubChunk = 4096;  // hub entries per task (CTA-class rows split)
+
+// The hub pass: one 1024-thread CTA per SM holds contrib[0, K) in shared
+// memory (rep[K] = 0 pads); a warp takes 32 tasks at a time (coalesced task
+// reads), and sums them four at a time: 4 independent coalesced u16 column
+// loads, 4 LDS gathers, then the rest of any task longer than 32, a warp sum
+// per task, and one fp64 atomicAdd per task into its row's hub sum (a CTA-class
+// row is several tasks).
+__global__ void __launch_bounds__(kHubThreads, 1)
+    k_pull_hub(const uint64_t* __restrict__ t_off, const uint32_t* __restrict__ t_len,
+               const uint32_t* __restrict__ t_k, uint64_t ntask,
+               const uint16_t* __restrict__ hcol, const float* __restrict__ contrib, uint32_t K,
+               double* hsum) {
+  extern __shared__ float rep[];
+  for (uint32_t i = threadIdx.x; i < K; i += blockDim.x) rep[i] = contrib[i];
+  if (threadIdx.x == 0) rep[K] = 0.0f;
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t stream = l2_evict_first();
+  for (uint64_t base = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32; base < ntask;
+       base += nwarps * 32) {
+    const uint64_t my = base + lane;
+    uint64_t o = 0;
+    uint32_t n = 0, k = 0;
+    if (my < ntask) {
+      o = t_off[my];
+      n = t_len[my];
+      k = t_k[my];
+    }
+    double mine = 0.0;
+    const uint32_t cnt = ntask - base < 32 ? (uint32_t)(ntask - base) : 32u;
+    for (uint32_t j = 0; j < cnt; j += 4) {
+      uint64_t oj[4];
+      uint32_t nj[4], ej[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        oj[t] = __shfl_sync(kFull, o, (j + t) & 31);
+        nj[t] = __shfl_sync(kFull, n, (j + t) & 31);
+        if (j + t >= cnt) nj[t] = 0;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        ej[t] = lane < nj[t] ? (uint32_t)ld_u16_hint(hcol + oj[t] + lane, stream) : K;
+      double sj[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sj[t] = (double)rep[ej[t]];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        for (uint32_t i = lane + 32; i < nj[t]; i += 32)
+          sj[t] += (double)rep[ld_u16_hint(hcol + oj[t] + i, stream)];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const double v = warp_sum(sj[t]);
+        if (lane == j + t) mine = v;
+      }
+    }
+    if (my < ntask) atomicAdd(&hsum[k], mine);
+  }
+}
+
+// list row k (CTA-class rows, then warp-class rows) -> hub-prefix length (the
+// row is ascending, so it is the lower bound of K), entries, tasks
+__global__ void k_hub_len(const uint64_t* off, const uint32_t* col, const uint32_t* cta,
+                          uint64_t n_cta, const uint32_t* warp, uint64_t n_list, uint32_t K,
+                          uint32_t* hlen, uint64_t* h64, uint64_t* tcnt) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n_list; k += stride) {
+    const uint64_t r = k < n_cta ? cta[k] : warp[k - n_cta];
+    uint64_t lo = off[r], hi = off[r + 1];
+    const uint64_t b = lo;
+    while (lo < hi) {
+      const uint64_t m = (lo + hi) >> 1;
+      if (col[m] < K) lo = m + 1;
+      else hi = m;
+    }
+    const uint64_t h = lo - b;
+    hlen[k] = (uint32_t)h;
+    h64[k] = h;
+    tcnt[k] = (h + kHubChunk - 1) / kHubChunk;
+  }
+}
+
+// a warp per list row: copy its hub prefix (u16) and write its tasks
+__global__ void k_hub_fill(const uint64_t* off, const uint32_t* col, const uint32_t* cta,
+                           uint64_t n_cta, const uint32_t* warp, uint64_t n_list,
+                           const uint64_t* hoff, const uint64_t* toff, uint16_t* hcol,
+                           uint64_t* t_off, uint32_t* t_len, uint32_t* t_k) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; k < n_list;
+       k += nwarps) {
+    const uint64_t r = k < n_cta ? cta[k] : warp[k - n_cta];
+    const uint64_t b = off[r], h0 = hoff[k], h = hoff[k + 1] - h0;
+    for (uint64_t i = lane; i < h; i += 32) hcol[h0 + i] = (uint16_t)col[b + i];
+    const uint64_t t0 = toff[k], nt = toff[k + 1] - t0;
+    for (uint64_t j = lane; j < nt; j += 32) {
+      t_off[t0 + j] = h0 + j * kHubChunk;
+      t_len[t0 + j] = (uint32_t)(h - j * kHubChunk < kHubChunk ? h - j * kHubChunk : kHubChunk);
+      t_k[t0 + j] = (uint32_t)k;
+    }
+  }
+}
+
+void scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s) {
+  size_t tmp = 0;
+  TG_CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, (int64_t)n, s));
+  DevBuf<uint8_t> t(tmp ? tmp : 1);
+  TG_CK(cub::DeviceScan::ExclusiveSum(t.get(), tmp, in, out, (int64_t)n, s));
+}
+
 __global__ void k_pr_init(const uint32_t* outdeg, uint64_t Vp, double r0, float* contrib, float* rank) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride) {
@@ -294,6 +449,44 @@ PullCsr ghost_csr(const Part& p) {
   return {g.off.get(), g.col.get(), g.cta.get(), g.n_cta, g.warp.get(), g.n_warp, p.Vp};
 }
 
+// Hub split layout for the in-CSR `c` (outside the timed region; rebuilt when
+// the layout or K changes).  K = 0 or no class rows: disabled.
+void build_pr_hub(PRHub& h, const PullCsr& c, uint64_t Vp, uint32_t K, cudaStream_t s) {
+  K = (uint32_t)std::min<uint64_t>(K, Vp);
+  if (h.built_for == c.col && h.K == K) return;
+  h = PRHub{};
+  h.K = K;
+  h.built_for = c.col;
+  h.n_list = c.n_cta + c.n_warp;
+  if (!K || !h.n_list) return;
+  const uint64_t n = h.n_list;
+  h.hlen.alloc(n);
+  DevBuf<uint64_t> h64(n + 1), tc(n + 1), hoff(n + 1), toff(n + 1);
+  TG_CK(cudaMemsetAsync(h64.get() + n, 0, 8, s));
+  TG_CK(cudaMemsetAsync(tc.get() + n, 0, 8, s));
+  k_hub_len<<<grid_for(n, 256), 256, 0, s>>>(c.off, c.col, c.cta, c.n_cta, c.warp, n, K,
+                                             h.hlen.get(), h64.get(), tc.get());
+  scan_u64(h64.get(), hoff.get(), n + 1, s);
+  scan_u64(tc.get(), toff.get(), n + 1, s);
+  uint64_t tot[2];
+  TG_CK(cudaMemcpyAsync(&tot[0], hoff.get() + n, 8, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaMemcpyAsync(&tot[1], toff.get() + n, 8, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+  h.H = tot[0];
+  h.ntask = tot[1];
+  TG_REQUIRE(h.ntask < (1ull << 32), TG_ECAPACITY, "pagerank hub split: too many tasks");
+  h.col.alloc(std::max<uint64_t>(h.H, 1));
+  h.t_off.alloc(std::max<uint64_t>(h.ntask, 1));
+  h.t_len.alloc(std::max<uint64_t>(h.ntask, 1));
+  h.t_k.alloc(std::max<uint64_t>(h.ntask, 1));
+  h.hsum.alloc(n);
+  k_hub_fill<<<grid_for(n * 32, 256), 256, 0, s>>>(c.off, c.col, c.cta, c.n_cta, c.warp, n,
+                                                   hoff.get(), toff.get(), h.col.get(),
+                                                   h.t_off.get(), h.t_len.get(), h.t_k.get());
+  TG_CK(cudaGetLastError());
+  TG_CK(cudaStreamSynchronize(s));
+}
+
 // ghost-pull: p's published contributions -> q's ghost slots (Vq + gh_off[p] + k)
 __global__ void k_publish(const uint32_t* lid, uint64_t n, const float* src, float* dst) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -323,8 +516,22 @@ void publish(Engine& eng, int buf) {
 
 template <int kL1>
 void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const PullOut& o,
-                    bool concurrent) {
+                    bool concurrent, PRHub* hub) {
   cudaStream_t s = eng.stream, s_cta = s, s_warp = s;
+  // hub pass first: the class pulls of the CTA / warp rows add its sums
+  const uint32_t* hl = nullptr;
+  const double* hs = nullptr;
+  if (hub && hub->K && hub->ntask) {
+    const size_t smem = ((size_t)hub->K + 1) * sizeof(float);
+    TG_CK(cudaFuncSetAttribute(k_pull_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    TG_CK(cudaMemsetAsync(hub->hsum.get(), 0, hub->n_list * sizeof(double), s));
+    k_pull_hub<<<148, kHubThreads, smem, s>>>(hub->t_off.get(), hub->t_len.get(), hub->t_k.get(),
+                                              hub->ntask, hub->col.get(), contrib, hub->K,
+                                              hub->hsum.get());
+    eng.launches++;
+    hl = hub->hlen.get();
+    hs = hub->hsum.get();
+  }
   if (concurrent) {
     eng.fork();
     s_cta = eng.side[0];
@@ -332,18 +539,42 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
   }
   const uint64_t R = c.R;
   if (c.n_cta) {
-    k_pull_cta<kL1><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o);
+    k_pull_cta<kL1><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o,
+                                                                  hl, hs);
     eng.launches++;
   }
+  // TG_PR_REP=k (A/B): warp / thread classes (TG_PR_REP_CLASSES bits 2 / 4) in
+  // 1024-thread CTAs, TG_PR_REP_CTAS per SM, each with a shared-memory replica
+  // of contrib[0, k)
+  uint32_t rep_k = 0, rep_cls = 6, rep_ctas = 2;
+  if (const char* v = std::getenv("TG_PR_REP")) rep_k = (uint32_t)std::strtoul(v, nullptr, 10);
+  if (const char* v = std::getenv("TG_PR_REP_CLASSES")) rep_cls = (uint32_t)std::atoi(v);
+  if (const char* v = std::getenv("TG_PR_REP_CTAS")) rep_ctas = (uint32_t)std::atoi(v);
+  const size_t rep_bytes = (size_t)rep_k * sizeof(float);
+  if (rep_k) {
+    TG_CK(cudaFuncSetAttribute(k_pull_warp<kL1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)rep_bytes));
+    TG_CK(cudaFuncSetAttribute(k_pull_thread<kL1, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rep_bytes));
+  }
   if (c.n_warp) {
-    k_pull_warp<kL1><<<grid_for(c.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(
-        c.off, c.col, contrib, c.warp, c.n_warp, o);
+    if (rep_k && (rep_cls & 2))
+      k_pull_warp<kL1, true><<<148u * rep_ctas, 1024, rep_bytes, s_warp>>>(
+          c.off, c.col, contrib, c.warp, c.n_warp, o, rep_k, hl ? hl + c.n_cta : nullptr,
+          hs ? hs + c.n_cta : nullptr);
+    else
+      k_pull_warp<kL1><<<grid_for(c.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(
+          c.off, c.col, contrib, c.warp, c.n_warp, o, 0u, hl ? hl + c.n_cta : nullptr,
+          hs ? hs + c.n_cta : nullptr);
     eng.launches++;
   }
   if (R) {
     const char* seg = std::getenv("TG_PR_SEG");
     if (seg && seg[0] == '1')
       k_pull_seg<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, R, o);
+    else if (rep_k && (rep_cls & 4))
+      k_pull_thread<kL1, true><<<148u * rep_ctas, 1024, rep_bytes, s>>>(c.off, c.col, contrib, 0, R,
+                                                                       o, rep_k);
     else
       k_pull_thread<kL1><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
     eng.launches++;
@@ -353,13 +584,287 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
 }
 
 void launch_pull(Engine& eng, const PullCsr& c, const float* contrib, const PullOut& o,
-                 bool concurrent, int l1) {
+                 bool concurrent, int l1, PRHub* hub) {
   switch (l1) {
-    case 1: launch_pull_l1<1>(eng, c, contrib, o, concurrent); break;
-    case 2: launch_pull_l1<2>(eng, c, contrib, o, concurrent); break;
-    case 3: launch_pull_l1<3>(eng, c, contrib, o, concurrent); break;
-    default: launch_pull_l1<0>(eng, c, contrib, o, concurrent);
+    case 1: launch_pull_l1<1>(eng, c, contrib, o, concurrent, hub); break;
+    case 2: launch_pull_l1<2>(eng, c, contrib, o, concurrent, hub); break;
+    case 3: launch_pull_l1<3>(eng, c, contrib, o, concurrent, hub); break;
+    case 9: {
+      uint32_t lo = 0, hi = 0;
+      if (const char* v = std::getenv("TG_PR_XLO")) lo = (uint32_t)std::strtoul(v, nullptr, 10);
+      if (const char* v = std::getenv("TG_PR_XHI")) hi = (uint32_t)std::strtoul(v, nullptr, 10);
+      TG_CK(cudaMemcpyToSymbolAsync(c_xlo, &lo, 4, 0, cudaMemcpyHostToDevice, eng.stream));
+      TG_CK(cudaMemcpyToSymbolAsync(c_xhi, &hi, 4, 0, cudaMemcpyHostToDevice, eng.stream));
+      launch_pull_l1<9>(eng, c, contrib, o, concurrent, hub);
+      break;
+    }
+    default: launch_pull_l1<0>(eng, c, contrib, o, concurrent, hub);
   }
+}
+
+// ---------------------------------------------------------------- die split
+constexpr uint32_t kSplitChunk = 2048;  // rows with more half-edges are cut into chunks
+constexpr unsigned kSplitGrab = 8;      // tasks a warp takes from its die's queue at once
+
+__host__ __device__ __forceinline__ uint32_t line_hash(uint32_t l) {
+  l ^= l >> 16;
+  l *= 0x7feb352du;
+  l ^= l >> 15;
+  l *= 0x846ca68bu;
+  l ^= l >> 16;
+  return l;
+}
+// the die whose SMs gather source u: by its 128-byte line of contributions
+__device__ __forceinline__ int src_die(uint32_t u, uint32_t thresh) {
+  return line_hash(u >> 5) >= thresh ? 1 : 0;
+}
+
+__global__ void k_split_count(const uint64_t* off, const uint32_t* col, uint64_t R, uint32_t thresh,
+                              uint64_t* c0, uint64_t* c1) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += stride) {
+    uint64_t n1 = 0;
+    const uint64_t b = off[r], e = off[r + 1];
+    for (uint64_t i = b; i < e; ++i) n1 += src_die(col[i], thresh);
+    c0[r] = (e - b) - n1;
+    c1[r] = n1;
+  }
+}
+
+__global__ void k_split_fill(const uint64_t* off, const uint32_t* col, uint64_t R, uint32_t thresh,
+                             const uint64_t* o0, const uint64_t* o1, uint32_t* d0, uint32_t* d1) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += stride) {
+    uint64_t j0 = o0[r], j1 = o1[r];
+    for (uint64_t i = off[r], e = off[r + 1]; i < e; ++i) {
+      const uint32_t u = col[i];
+      if (src_die(u, thresh)) d1[j1++] = u;
+      else d0[j0++] = u;
+    }
+  }
+}
+
+// per row of one half: warp-row flag, chunked-row flag, chunk count
+__global__ void k_split_class(const uint64_t* off, uint64_t R, uint64_t* wf, uint64_t* cf,
+                              uint64_t* cn) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += stride) {
+    const uint64_t n = off[r + 1] - off[r];
+    wf[r] = n >= 32 && n < kSplitChunk;
+    cf[r] = n >= kSplitChunk;
+    cn[r] = n >= kSplitChunk ? (n + kSplitChunk - 1) / kSplitChunk : 0;
+  }
+}
+
+__global__ void k_split_lists(const uint64_t* off, uint64_t R, const uint64_t* wp, const uint64_t* cp,
+                              const uint64_t* np, uint32_t* wrow, uint32_t* c_list, uint32_t* c_row,
+                              uint32_t* c_k, uint32_t* c_len, uint64_t* c_start) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += stride) {
+    const uint64_t b = off[r], n = off[r + 1] - b;
+    if (n >= 32 && n < kSplitChunk) wrow[wp[r]] = (uint32_t)r;
+    if (n >= kSplitChunk) {
+      const uint64_t k = cp[r];
+      c_list[k] = (uint32_t)r;
+      for (uint64_t j = 0, t = np[r]; j * kSplitChunk < n; ++j, ++t) {
+        c_row[t] = (uint32_t)r;
+        c_k[t] = (uint32_t)k;
+        c_start[t] = b + j * kSplitChunk;
+        c_len[t] = (uint32_t)(n - j * kSplitChunk < kSplitChunk ? n - j * kSplitChunk : kSplitChunk);
+      }
+    }
+  }
+}
+
+struct SplitArgs {
+  const uint64_t* off[2];
+  const uint32_t* col[2];
+  const uint32_t* wrow[2];
+  const uint32_t* c_k[2];
+  const uint32_t* c_len[2];
+  const uint64_t* c_start[2];
+  uint64_t n_w[2], n_c[2];
+  double* cacc[2];
+  float* psum[2];
+  uint64_t R, nT;
+  unsigned long long* qnext;
+  const uint8_t* die_of;
+  uint32_t hot;
+};
+
+__device__ __forceinline__ uint32_t sm_id_pr() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// Persistent warps; each serves the task queue of its own SM's die first
+// (chunks of the long rows, then warp rows, then blocks of 32 short rows, one
+// lane per row), then helps the other die's queue once its own is empty.
+__global__ void __launch_bounds__(256) k_pr_split(SplitArgs a, const float* __restrict__ contrib) {
+  const uint32_t lane = threadIdx.x & 31;
+  const int mine = a.die_of[sm_id_pr()];
+  for (int pass = 0; pass < 2; ++pass) {
+    const int d = pass ? mine ^ 1 : mine;
+    const uint64_t nc = a.n_c[d], nw = a.n_w[d], nt = nc + nw + a.nT;
+    const uint64_t* off = a.off[d];
+    const uint32_t* col = a.col[d];
+    for (;;) {
+      unsigned long long t0 = 0;
+      if (lane == 0) t0 = atomicAdd(&a.qnext[d], (unsigned long long)kSplitGrab);
+      t0 = __shfl_sync(kFull, t0, 0);
+      if (t0 >= nt) break;
+      const uint64_t t1 = t0 + kSplitGrab < nt ? t0 + kSplitGrab : nt;
+      for (uint64_t t = t0; t < t1; ++t) {
+        if (t < nc) {
+          const uint64_t b = a.c_start[d][t];
+          double sum = gather_sum<0>(col, contrib, b + lane, b + a.c_len[d][t], 32, a.hot, 0);
+          sum = warp_sum(sum);
+          if (lane == 0) atomicAdd(&a.cacc[d][a.c_k[d][t]], sum);
+        } else if (t < nc + nw) {
+          const uint32_t r = a.wrow[d][t - nc];
+          const uint64_t b = off[r], e = off[r + 1];
+          double sum = gather_sum<0>(col, contrib, b + lane, e, 32, a.hot, 0);
+          sum = warp_sum(sum);
+          if (lane == 0) a.psum[d][r] = (float)sum;
+        } else {
+          const uint64_t r = (t - nc - nw) * 32 + lane;
+          if (r < a.R) {
+            const uint64_t b = off[r], e = off[r + 1];
+            if (e - b < 32) a.psum[d][r] = (float)gather_sum<0>(col, contrib, b, e, 1, a.hot, 0);
+          }
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_split_cfix(const uint32_t* c_list, const double* cacc, uint64_t n, float* psum) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += stride)
+    psum[c_list[k]] = (float)cacc[k];
+}
+
+__global__ void k_split_finalize(const float* __restrict__ p0, const float* __restrict__ p1,
+                                 uint64_t R, PullOut o) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += stride)
+    o.put(r, (double)p0[r] + (double)p1[r]);
+}
+
+// Die-split layout of the in-CSR `c` (outside the timed region).  Needs a
+// measured two-die map and room for a second copy of the in-CSR; else off.
+void build_pr_split(Engine& eng, PRSplit& sp, const PullCsr& c, cudaStream_t s) {
+  if (sp.built && sp.built_for == c.col) return;
+  sp = PRSplit{};
+  sp.built = true;
+  sp.built_for = c.col;
+  const DieMap& dm = die_map(eng.device);
+  const uint64_t R = c.R;
+  if (!dm.ok || !R) return;
+  uint64_t Ein = 0;
+  TG_CK(cudaMemcpyAsync(&Ein, c.off + R, 8, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+  // room: the split in-CSR (4 B per edge + 2 x 8 B per row) + psum + build scratch
+  size_t fr = 0, tot = 0;
+  TG_CK(cudaMemGetInfo(&fr, &tot));
+  const uint64_t need = Ein * 4 + R * (16 + 8 + 5 * 8) + (1ull << 30);
+  if (need > fr) return;
+  sp.R = R;
+  sp.thresh = (uint32_t)(((uint64_t)dm.n[0] << 32) / (uint64_t)dm.nsm);
+  {
+    DevBuf<uint64_t> c0(R + 1), c1(R + 1);
+    TG_CK(cudaMemsetAsync(c0.get() + R, 0, 8, s));
+    TG_CK(cudaMemsetAsync(c1.get() + R, 0, 8, s));
+    k_split_count<<<grid_for(R, 256), 256, 0, s>>>(c.off, c.col, R, sp.thresh, c0.get(), c1.get());
+    sp.off[0].alloc(R + 1);
+    sp.off[1].alloc(R + 1);
+    scan_u64(c0.get(), sp.off[0].get(), R + 1, s);
+    scan_u64(c1.get(), sp.off[1].get(), R + 1, s);
+  }
+  uint64_t n0 = 0, n1 = 0;
+  TG_CK(cudaMemcpyAsync(&n0, sp.off[0].get() + R, 8, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaMemcpyAsync(&n1, sp.off[1].get() + R, 8, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+  sp.col[0].alloc(std::max<uint64_t>(n0, 1));
+  sp.col[1].alloc(std::max<uint64_t>(n1, 1));
+  k_split_fill<<<grid_for(R, 256), 256, 0, s>>>(c.off, c.col, R, sp.thresh, sp.off[0].get(),
+                                                sp.off[1].get(), sp.col[0].get(), sp.col[1].get());
+  for (int d = 0; d < 2; ++d) {
+    DevBuf<uint64_t> wf(R + 1), cf(R + 1), cn(R + 1), wp(R + 1), cp(R + 1), np(R + 1);
+    TG_CK(cudaMemsetAsync(wf.get() + R, 0, 8, s));
+    TG_CK(cudaMemsetAsync(cf.get() + R, 0, 8, s));
+    TG_CK(cudaMemsetAsync(cn.get() + R, 0, 8, s));
+    k_split_class<<<grid_for(R, 256), 256, 0, s>>>(sp.off[d].get(), R, wf.get(), cf.get(), cn.get());
+    scan_u64(wf.get(), wp.get(), R + 1, s);
+    scan_u64(cf.get(), cp.get(), R + 1, s);
+    scan_u64(cn.get(), np.get(), R + 1, s);
+    uint64_t cnt[3];
+    TG_CK(cudaMemcpyAsync(&cnt[0], wp.get() + R, 8, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaMemcpyAsync(&cnt[1], cp.get() + R, 8, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaMemcpyAsync(&cnt[2], np.get() + R, 8, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaStreamSynchronize(s));
+    sp.n_w[d] = cnt[0];
+    sp.n_ck[d] = cnt[1];
+    sp.n_c[d] = cnt[2];
+    sp.wrow[d].alloc(std::max<uint64_t>(cnt[0], 1));
+    sp.c_list[d].alloc(std::max<uint64_t>(cnt[1], 1));
+    sp.cacc[d].alloc(std::max<uint64_t>(cnt[1], 1));
+    sp.c_row[d].alloc(std::max<uint64_t>(cnt[2], 1));
+    sp.c_k[d].alloc(std::max<uint64_t>(cnt[2], 1));
+    sp.c_len[d].alloc(std::max<uint64_t>(cnt[2], 1));
+    sp.c_start[d].alloc(std::max<uint64_t>(cnt[2], 1));
+    k_split_lists<<<grid_for(R, 256), 256, 0, s>>>(sp.off[d].get(), R, wp.get(), cp.get(), np.get(),
+                                                   sp.wrow[d].get(), sp.c_list[d].get(),
+                                                   sp.c_row[d].get(), sp.c_k[d].get(),
+                                                   sp.c_len[d].get(), sp.c_start[d].get());
+    sp.psum[d].alloc(R);
+  }
+  sp.qnext.alloc(2);
+  TG_CK(cudaGetLastError());
+  TG_CK(cudaStreamSynchronize(s));
+  sp.on = true;
+}
+
+void launch_split(Engine& eng, PRSplit& sp, const float* contrib, const PullOut& o) {
+  cudaStream_t s = eng.stream;
+  const DieMap& dm = die_map(eng.device);
+  SplitArgs a{};
+  for (int d = 0; d < 2; ++d) {
+    a.off[d] = sp.off[d].get();
+    a.col[d] = sp.col[d].get();
+    a.wrow[d] = sp.wrow[d].get();
+    a.c_k[d] = sp.c_k[d].get();
+    a.c_len[d] = sp.c_len[d].get();
+    a.c_start[d] = sp.c_start[d].get();
+    a.n_w[d] = sp.n_w[d];
+    a.n_c[d] = sp.n_c[d];
+    a.cacc[d] = sp.cacc[d].get();
+    a.psum[d] = sp.psum[d].get();
+    if (sp.n_ck[d]) TG_CK(cudaMemsetAsync(sp.cacc[d].get(), 0, sp.n_ck[d] * 8, s));
+  }
+  a.R = sp.R;
+  a.nT = (sp.R + 31) / 32;
+  a.qnext = sp.qnext.get();
+  a.die_of = dm.die_of.get();
+  a.hot = o.hot;
+  TG_CK(cudaMemsetAsync(sp.qnext.get(), 0, 16, s));
+  static int per_sm = 0;
+  if (!per_sm) {
+    TG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pr_split, 256, 0));
+    if (per_sm < 1) per_sm = 1;
+  }
+  k_pr_split<<<(unsigned)(dm.nsm * per_sm), 256, 0, s>>>(a, contrib);
+  eng.launches++;
+  for (int d = 0; d < 2; ++d)
+    if (sp.n_ck[d]) {
+      k_split_cfix<<<grid_for(sp.n_ck[d], 256), 256, 0, s>>>(sp.c_list[d].get(), sp.cacc[d].get(),
+                                                             sp.n_ck[d], sp.psum[d].get());
+      eng.launches++;
+    }
+  k_split_finalize<<<grid_for(sp.R, 256), 256, 0, s>>>(sp.psum[0].get(), sp.psum[1].get(), sp.R, o);
+  eng.launches++;
+  TG_CK(cudaGetLastError());
 }
 
 void* send_obox(Part& p) { return p.pr.obox.get(); }
@@ -406,9 +911,28 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   if (const char* v = std::getenv("TG_PR_L1")) l1 = std::atoi(v);
   uint32_t l1hot = 32768;
   if (const char* v = std::getenv("TG_PR_L1HOT")) l1hot = (uint32_t)std::strtoul(v, nullptr, 10);
+  // L2 policy of the next round's hub contributions (TG_PR_NEXTPOL)
+  int npol = 0;
+  if (const char* v = std::getenv("TG_PR_NEXTPOL")) npol = std::atoi(v);
   // row classes on fork/join streams (TG_PR_CONCURRENT=0: one stream)
   const bool concurrent =
       !(std::getenv("TG_PR_CONCURRENT") && std::getenv("TG_PR_CONCURRENT")[0] == '0');
+  // hub split (PRHub): K hub sources in shared memory (TG_PR_HUB, 0 = off)
+  uint32_t hubk = 0;
+  if (const char* v = std::getenv("TG_PR_HUB")) hubk = (uint32_t)std::strtoul(v, nullptr, 10);
+  if (hubk)
+    for (auto& pp : eng.parts) {
+      Part& p = *pp;
+      build_pr_hub(p.pr.hub, ghost ? ghost_csr(p) : push_csr(p), p.Vp, hubk, s);
+    }
+  // die split (PRSplit): TG_PR_SPLIT=1 (A/B)
+  bool split = false;
+  if (const char* v = std::getenv("TG_PR_SPLIT")) split = v[0] == '1';
+  if (split)
+    for (auto& pp : eng.parts) {
+      Part& p = *pp;
+      build_pr_split(eng, p.pr.split, ghost ? ghost_csr(p) : push_csr(p), s);
+    }
   time_begin(eng);
   for (auto& pp : eng.parts) {
     Part& p = *pp;
@@ -426,9 +950,14 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       PRState& r = p.pr;
       // P == 1 and ghost-pull: every in-edge is in the row, finalize in the pull
       PullOut o{eng.P == 1 || ghost, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
-                r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, l1hot, p.rout(), eng.fused, it & 1};
+                r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, l1hot, npol, p.rout(), eng.fused,
+                it & 1};
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
-      launch_pull(eng, ghost ? ghost_csr(p) : push_csr(p), r.contrib[cur].get(), o, concurrent, l1);
+      if (split && r.split.on)
+        launch_split(eng, r.split, r.contrib[cur].get(), o);
+      else
+        launch_pull(eng, ghost ? ghost_csr(p) : push_csr(p), r.contrib[cur].get(), o, concurrent,
+                    l1, hubk ? &r.hub : nullptr);
     }
     eng.prof_end(TG_K_PR_PULL);
     if (ghost) {  // communication: contributions of boundary sources -> peers' ghosts

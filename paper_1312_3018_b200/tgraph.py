@@ -167,6 +167,7 @@ def lib():
         L.tg_engine_set_profiling.argtypes = [p, i32]
         L.tg_engine_set_exchange.argtypes = [p, i32]
         L.tg_engine_set_pagerank_comm.argtypes = [p, i32]
+        L.tg_device_die_map.argtypes = [i32, p, i32, C.POINTER(i32), C.POINTER(i32)]
         L.tg_engine_kernel_stat.argtypes = [p, i32, C.POINTER(tg_kernel_stat)]
         L.tg_kernel_name.argtypes = [i32]
         L.tg_kernel_name.restype = C.c_char_p
@@ -186,7 +187,7 @@ def lib():
         L.tg_hostcomm_free.restype = None
         for f in ("tg_engine_set_async_collect", "tg_engine_sync", "tg_hostcomm_create", "tg_hostcomm_allreduce_u64", "tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
                   "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc",
-                  "tg_cc", "tg_engine_set_profiling", "tg_engine_set_exchange", "tg_engine_set_pagerank_comm", "tg_engine_kernel_stat", "tg_graph_from_edges",
+                  "tg_cc", "tg_engine_set_profiling", "tg_engine_set_exchange", "tg_engine_set_pagerank_comm", "tg_device_die_map", "tg_engine_kernel_stat", "tg_graph_from_edges",
                   "tg_graph_load_edge_list", "tg_graph_info", "tg_graph_edges", "tg_engine_create",
                   "tg_rmat_edges"):
             getattr(L, f).restype = i32
@@ -428,6 +429,16 @@ TG_PR_PUSH, TG_PR_PULL = 0, 1
 
 def tg_engine_set_pagerank_comm(h, mode: int) -> None:
     _check(lib().tg_engine_set_pagerank_comm(h, int(mode)))
+
+
+def tg_device_die_map(device: int = 0):
+    """-> (ok, die_of numpy u8 per SM id) of the measured two-die map."""
+    nsm, ok = C.c_int(0), C.c_int(0)
+    _check(lib().tg_device_die_map(int(device), None, 0, C.byref(nsm), C.byref(ok)))
+    out = np.zeros(max(nsm.value, 1), np.uint8)
+    _check(lib().tg_device_die_map(int(device), out.ctypes.data_as(C.c_void_p), len(out),
+                                   C.byref(nsm), C.byref(ok)))
+    return bool(ok.value), out[:nsm.value]
 
 
 def tg_engine_set_exchange(h, mode: int) -> None:

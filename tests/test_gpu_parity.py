@@ -225,6 +225,82 @@ def test_pagerank_ghost_pull(tg, P):
     assert_pr(e2.pagerank(5)[0], G2.pagerank(5))
 
 
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_pagerank_hub_split(tg, P, monkeypatch):
+    """Hub split (PRHub, TG_PR_HUB=K): the in-edges from the K hub sources of
+    the CTA- and warp-class rows are summed by a separate pass from a
+    shared-memory replica of the contributions, the class pulls start after
+    each row's hub prefix.  Same oracle result for K from 1 to beyond V, in
+    both PageRank communications, and for a row whose hub prefix spans several
+    tasks (> 4096 hub in-edges)."""
+    scale = 13
+    src, dst, _ = inputs.rmat_edges(scale)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst)
+    eng = tg.Engine.from_edges(V, src, dst, partitions=P, weighted=False)
+    ref = G.pagerank(5)
+    for K in ("1", "256", "3000", "100000", "0"):
+        monkeypatch.setenv("TG_PR_HUB", K)
+        for comm in ((tg.TG_PR_PUSH, tg.TG_PR_PULL) if P > 1 else (None,)):
+            if comm is not None:
+                eng.set_pagerank_comm(comm)
+            assert_pr(eng.pagerank(5)[0], ref)
+    # in-star: 9000 sources of out-degree 1 (ties: all of them lead the
+    # out-degree order) point at one row, plus a sparse background
+    rng = np.random.default_rng(11)
+    n = 10000
+    s2 = np.concatenate([np.arange(9000), rng.integers(0, n, 2000)]).astype(np.uint32)
+    d2 = np.concatenate([np.full(9000, n - 1), rng.integers(0, n, 2000)]).astype(np.uint32)
+    G2 = oracle.Graph(n, s2, d2)
+    e2 = tg.Engine.from_edges(n, s2, d2, partitions=P, weighted=False)
+    ref2 = G2.pagerank(5)
+    for K in ("8192", "5000", "4097"):
+        monkeypatch.setenv("TG_PR_HUB", K)
+        assert_pr(e2.pagerank(5)[0], ref2)
+
+
+def test_die_map(tg):
+    """The measured SM -> die map of a B200: two clusters of pointer-chase
+    latency (each die's L2 caches its own SMs' reads), neither tiny."""
+    ok, die = tg.tg_device_die_map(0)
+    assert len(die) >= 1
+    if ok:
+        n1 = int(die.sum())
+        assert 0 < n1 < len(die) and min(n1, len(die) - n1) * 5 >= len(die)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+def test_pagerank_die_split(tg, P, monkeypatch):
+    """Die split (PRSplit, TG_PR_SPLIT=1): every row's in-edges are split into
+    two CSRs by the die that gathers the source, each die's SMs pull over
+    their own half (stealing from the other die's queue at the end), and a
+    finalize pass adds the two partial sums.  Same oracle result as the class
+    pulls, in both PageRank communications, including rows cut into chunks
+    (> 2048 half-edges)."""
+    ok, _ = tg.tg_device_die_map(0)
+    if not ok:
+        pytest.skip("one-die GPU: no die split")
+    monkeypatch.setenv("TG_PR_SPLIT", "1")
+    scale = 13
+    src, dst, _ = inputs.rmat_edges(scale)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst)
+    eng = tg.Engine.from_edges(V, src, dst, partitions=P, weighted=False)
+    for T in (1, 5):
+        ref = G.pagerank(T)
+        for comm in ((tg.TG_PR_PUSH, tg.TG_PR_PULL) if P > 1 else (None,)):
+            if comm is not None:
+                eng.set_pagerank_comm(comm)
+            assert_pr(eng.pagerank(T)[0], ref)
+    rng = np.random.default_rng(12)
+    n = 20000
+    s2 = np.concatenate([np.arange(15000), rng.integers(0, n, 4000)]).astype(np.uint32)
+    d2 = np.concatenate([np.full(15000, n - 1), rng.integers(0, n, 4000)]).astype(np.uint32)
+    G2 = oracle.Graph(n, s2, d2)
+    e2 = tg.Engine.from_edges(n, s2, d2, partitions=P, weighted=False)
+    assert_pr(e2.pagerank(5)[0], G2.pagerank(5))
+
+
 def test_set_exchange_rejects_unknown_mode(tg):
     from paper_1312_3018_b200 import tgraph
 
@@ -240,7 +316,9 @@ def test_set_exchange_rejects_unknown_mode(tg):
 @pytest.mark.parametrize("variant", [("TG_PR_SEG", "1"), ("TG_PR_L1", "2"), ("TG_PR_L1", "3"),
                                      ("TG_SSSP_DENSE_DIV", "64"), ("TG_BC_HUBPULL", "0"),
                                      ("TG_BC_HUBPULL", "64"), ("TG_STAGE_ROWOFF", "1"),
-                                     ("TG_CC_GHOST_WARP", "1"), ("TG_CC_GHOST_WARP", "0")])
+                                     ("TG_CC_GHOST_WARP", "1"), ("TG_CC_GHOST_WARP", "0"),
+                                     ("TG_PR_REP", "1024"), ("TG_PR_NEXTPOL", "2"),
+                                     ("TG_PR_HUB", "512")])
 @pytest.mark.parametrize("P", [1, 3])
 def test_kernel_variants_same_result(tg, variant, P, monkeypatch):
     """The A/B kernel variants behind run-time switches
