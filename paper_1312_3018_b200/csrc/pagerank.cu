@@ -64,7 +64,9 @@ __device__ __forceinline__ float gather_one(const float* __restrict__ contrib, u
   if constexpr (kRep) {
     if (c < rep.k) return rep.s[c];
   }
-  if constexpr (kL1 == 9) {
+  if constexpr (kL1 == 8) {  // A/B: no L2 policy hints at all
+    return __ldg(contrib + c);
+  } else if constexpr (kL1 == 9) {
     if (c >= c_xlo && c < c_xhi) return 0.0f;
     return ld_f32_hint(contrib + c, c < hot ? keep : stream);
   } else if constexpr (kL1 >= 2) {
@@ -85,7 +87,8 @@ __device__ __forceinline__ double gather_sum(const uint32_t* __restrict__ in_col
                                              uint32_t l1hot, Rep rep = {nullptr, 0}) {
   const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
   auto col = [&](uint64_t j) {
-    if constexpr (kL1 >= 1) return ld_u32_stream(in_col + j, stream);
+    if constexpr (kL1 == 8) return __ldg(in_col + j);
+    else if constexpr (kL1 >= 1 && kL1 <= 3) return ld_u32_stream(in_col + j, stream);
     else return ld_u32_hint(in_col + j, stream);
   };
   auto gather_one = [&](const float* __restrict__ cb, uint32_t c, uint32_t h, uint64_t k,
@@ -210,6 +213,68 @@ __global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_thread(const uint64_
     const uint64_t b = in_off[r], e = in_off[r + 1];
     if (e - b >= 32) continue;
     o.put(r, gather_sum<kL1, kRep>(in_col, contrib, b, e, 1, o.hot, o.l1hot, rep));
+  }
+}
+
+// Software-pipelined class pulls (TG_PR_PIPE=1): the row-setup chain (list
+// entry -> in_off -> in_col -> gathers) is cut by issuing the next row's
+// offsets (and, for the warp class, the list entry two rows ahead) before the
+// current row's gathers, so a warp's gathers no longer wait on its own setup.
+template <int kL1>
+__global__ void __launch_bounds__(256) k_pull_warp_pipe(const uint64_t* in_off,
+                                                        const uint32_t* in_col,
+                                                        const float* contrib, const uint32_t* rows,
+                                                        uint64_t n, PullOut o) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t k0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  uint32_t rA = k0 < n ? rows[k0] : 0u;
+  uint32_t rB = k0 + nwarps < n ? rows[k0 + nwarps] : 0u;
+  uint64_t bA = 0, eA = 0;
+  if (k0 < n) {
+    bA = in_off[rA];
+    eA = in_off[rA + 1];
+  }
+  for (uint64_t k = k0; k < n; k += nwarps) {
+    const uint64_t kC = k + 2 * nwarps;
+    const uint32_t rC = kC < n ? rows[kC] : 0u;
+    uint64_t bB = 0, eB = 0;
+    if (k + nwarps < n) {
+      bB = in_off[rB];
+      eB = in_off[rB + 1];
+    }
+    double sum = gather_sum<kL1>(in_col, contrib, bA + lane, eA, 32, o.hot, o.l1hot);
+    sum = warp_sum(sum);
+    if (lane == 0) o.put(rA, sum);
+    rA = rB;
+    bA = bB;
+    eA = eB;
+    rB = rC;
+  }
+}
+
+template <int kL1>
+__global__ void __launch_bounds__(256) k_pull_thread_pipe(const uint64_t* in_off,
+                                                          const uint32_t* in_col,
+                                                          const float* contrib, uint64_t r0,
+                                                          uint64_t r1, PullOut o) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t b = 0, e = 0;
+  if (r < r1) {
+    b = in_off[r];
+    e = in_off[r + 1];
+  }
+  for (; r < r1; r += stride) {
+    const uint64_t rn = r + stride;
+    uint64_t bn = 0, en = 0;
+    if (rn < r1) {
+      bn = in_off[rn];
+      en = in_off[rn + 1];
+    }
+    if (e - b < 32) o.put(r, gather_sum<kL1>(in_col, contrib, b, e, 1, o.hot, o.l1hot));
+    b = bn;
+    e = en;
   }
 }
 
@@ -395,6 +460,62 @@ void scan_u64(const uint64_t* in, uint64_t* out, uint64_t n, cudaStream_t s) {
   TG_CK(cub::DeviceScan::ExclusiveSum(t.get(), tmp, in, out, (int64_t)n, s));
 }
 
+// rows with in-degree < 32, a warp per group of 32 consecutive rows
+// (TG_PR_GROUP=1): when every row of the group is short, their in-edges are one
+// contiguous range of in_col, walked 128 at a time -- each lane loads 4 columns
+// (coalesced) and gathers their contributions into a per-warp shared-memory
+// window -- and each row's lane then sums its own entries of the window
+// (LDS, fp64).  No per-lane row loops over global memory (a thread per row
+// diverges to the group's longest row and reads in_col one lane at a time);
+// the rank / contribution writes stay coalesced.  Groups holding a row of
+// in-degree >= 32 (left to the warp / CTA classes) take the thread-per-row path.
+constexpr int kGroupWin = 128;
+template <int kL1>
+__global__ void __launch_bounds__(256) k_pull_group(const uint64_t* in_off, const uint32_t* in_col,
+                                                    const float* contrib, uint64_t R, PullOut o) {
+  __shared__ float s_win[256 / 32][kGroupWin];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* win = s_win[w];
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
+  for (uint64_t r0 = ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5) * 32; r0 < R;
+       r0 += nwarps * 32) {
+    const uint64_t r = r0 + lane;
+    const uint64_t rr = r < R ? r : R;
+    const uint64_t b = in_off[rr], e = r < R ? in_off[r + 1] : b;
+    const bool small = e - b < 32;
+    if (__all_sync(kFull, small)) {
+      const uint64_t base = __shfl_sync(kFull, b, 0);
+      const uint32_t T = (uint32_t)(__shfl_sync(kFull, e, 31) - base);
+      const uint32_t lo = (uint32_t)(b - base), hi = (uint32_t)(e - base);
+      double acc = 0.0;
+      for (uint32_t c0 = 0; c0 < T; c0 += kGroupWin) {
+        uint32_t cc[kGroupWin / 32];
+#pragma unroll
+        for (int k = 0; k < kGroupWin / 32; ++k) {
+          const uint32_t idx = c0 + k * 32 + lane;
+          cc[k] = idx < T ? ld_u32_hint(in_col + base + idx, stream) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < kGroupWin / 32; ++k) {
+          const uint32_t idx = c0 + k * 32 + lane;
+          float v = 0.0f;
+          if (idx < T) v = ld_f32_hint(contrib + cc[k], cc[k] < o.hot ? keep : stream);
+          win[k * 32 + lane] = v;
+        }
+        __syncwarp();
+        const uint32_t a0 = lo > c0 ? lo : c0;
+        const uint32_t a1 = hi < c0 + kGroupWin ? hi : c0 + kGroupWin;
+        for (uint32_t k = a0; k < a1; ++k) acc += (double)win[k - c0];
+        __syncwarp();
+      }
+      if (r < R) o.put(r, acc);
+    } else if (r < R && small) {
+      o.put(r, gather_sum<kL1>(in_col, contrib, b, e, 1, o.hot, o.l1hot));
+    }
+  }
+}
+
 __global__ void k_pr_init(const uint32_t* outdeg, uint64_t Vp, double r0, float* contrib, float* rank) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride) {
@@ -557,7 +678,13 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
     TG_CK(cudaFuncSetAttribute(k_pull_thread<kL1, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rep_bytes));
   }
-  if (c.n_warp) {
+  const char* pipe_env = std::getenv("TG_PR_PIPE");
+  const int pipe = pipe_env ? std::atoi(pipe_env) : 0;  // bit 1 warp class, bit 2 thread class
+  if (c.n_warp && (pipe & 1) && !hl) {
+    k_pull_warp_pipe<kL1><<<grid_for(c.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(
+        c.off, c.col, contrib, c.warp, c.n_warp, o);
+    eng.launches++;
+  } else if (c.n_warp) {
     if (rep_k && (rep_cls & 2))
       k_pull_warp<kL1, true><<<148u * rep_ctas, 1024, rep_bytes, s_warp>>>(
           c.off, c.col, contrib, c.warp, c.n_warp, o, rep_k, hl ? hl + c.n_cta : nullptr,
@@ -570,8 +697,14 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
   }
   if (R) {
     const char* seg = std::getenv("TG_PR_SEG");
+    const char* grp = std::getenv("TG_PR_GROUP");
     if (seg && seg[0] == '1')
       k_pull_seg<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, R, o);
+    else if (pipe & 2)
+      k_pull_thread_pipe<kL1><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0,
+                                                                          R, o);
+    else if (grp && grp[0] == '1')
+      k_pull_group<kL1><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, R, o);
     else if (rep_k && (rep_cls & 4))
       k_pull_thread<kL1, true><<<148u * rep_ctas, 1024, rep_bytes, s>>>(c.off, c.col, contrib, 0, R,
                                                                        o, rep_k);
@@ -589,6 +722,7 @@ void launch_pull(Engine& eng, const PullCsr& c, const float* contrib, const Pull
     case 1: launch_pull_l1<1>(eng, c, contrib, o, concurrent, hub); break;
     case 2: launch_pull_l1<2>(eng, c, contrib, o, concurrent, hub); break;
     case 3: launch_pull_l1<3>(eng, c, contrib, o, concurrent, hub); break;
+    case 8: launch_pull_l1<8>(eng, c, contrib, o, concurrent, hub); break;
     case 9: {
       uint32_t lo = 0, hi = 0;
       if (const char* v = std::getenv("TG_PR_XLO")) lo = (uint32_t)std::strtoul(v, nullptr, 10);

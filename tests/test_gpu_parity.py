@@ -259,6 +259,27 @@ def test_pagerank_hub_split(tg, P, monkeypatch):
         assert_pr(e2.pagerank(5)[0], ref2)
 
 
+@pytest.mark.parametrize("P", [1, 2])
+def test_pagerank_short_row_groups(tg, P, monkeypatch):
+    """TG_PR_GROUP=1: rows of in-degree < 32 summed 32 rows at a time through a
+    shared-memory window of 128 in-edges.  Groups whose edges span many
+    windows (every row with 31 in-edges: 992 per group), mixed groups holding
+    a long row, empty rows and a ragged last group."""
+    monkeypatch.setenv("TG_PR_GROUP", "1")
+    rng = np.random.default_rng(13)
+    n = 2000
+    dst = np.repeat(np.arange(n), 31)
+    src = rng.integers(0, n, len(dst))
+    extra_d = np.full(300, 5)                    # one long row inside a group
+    extra_s = rng.integers(0, n, 300)
+    sp = np.concatenate([src, extra_s, [7, 7]]).astype(np.uint32)
+    dp = np.concatenate([dst, extra_d, [n + 10, n + 40]]).astype(np.uint32)
+    V = n + 45                                   # rows n..n+44: 2 edges, mostly empty
+    G = oracle.Graph(V, sp, dp)
+    eng = tg.Engine.from_edges(V, sp, dp, partitions=P, weighted=False)
+    assert_pr(eng.pagerank(5)[0], G.pagerank(5))
+
+
 def test_die_map(tg):
     """The measured SM -> die map of a B200: two clusters of pointer-chase
     latency (each die's L2 caches its own SMs' reads), neither tiny."""
@@ -318,7 +339,8 @@ def test_set_exchange_rejects_unknown_mode(tg):
                                      ("TG_BC_HUBPULL", "64"), ("TG_STAGE_ROWOFF", "1"),
                                      ("TG_CC_GHOST_WARP", "1"), ("TG_CC_GHOST_WARP", "0"),
                                      ("TG_PR_REP", "1024"), ("TG_PR_NEXTPOL", "2"),
-                                     ("TG_PR_HUB", "512")])
+                                     ("TG_PR_HUB", "512"), ("TG_PR_GROUP", "1"),
+                                     ("TG_PR_PIPE", "3")])
 @pytest.mark.parametrize("P", [1, 3])
 def test_kernel_variants_same_result(tg, variant, P, monkeypatch):
     """The A/B kernel variants behind run-time switches
