@@ -363,6 +363,16 @@ int tg_device_die_map(int device, uint8_t* die_of, int cap, int* nsm, int* ok);
 int tg_engine_set_async_collect(tg_engine* eng, int on);
 /* Wait for every pending result copy (and the engine's stream). */
 int tg_engine_sync(tg_engine* eng);
+/* Finer-grained completion of asynchronous host collections: every algorithm
+ * call whose output went to host memory under async collect gets the next
+ * ticket (1, 2, ...); tg_engine_last_ticket returns the latest (0 if none)
+ * and tg_engine_wait_ticket(t) returns once collection t and every earlier
+ * one is complete in host memory (ticket 0: returns at once).  A caller can
+ * so keep two output sets in flight -- wait for call k's ticket while call
+ * k+1 computes (double buffering).  TG_EINVAL for NULL or a ticket not yet
+ * issued. */
+int tg_engine_last_ticket(const tg_engine* eng, uint64_t* ticket);
+int tg_engine_wait_ticket(tg_engine* eng, uint64_t ticket);
 int tg_engine_kernel_stat(const tg_engine* eng, int kernel_id, tg_kernel_stat* out);
 const char* tg_kernel_name(int kernel_id);
 

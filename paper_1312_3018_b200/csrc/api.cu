@@ -35,6 +35,8 @@ Engine::~Engine() {
   for (int i = 0; i < 2; ++i)
     if (stage_free[i]) cudaEventDestroy(stage_free[i]);
   if (chunk_ev) cudaEventDestroy(chunk_ev);
+  for (auto e : ticket_ev)
+    if (e) cudaEventDestroy(e);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (prof_open) cudaEventDestroy(prof_open);
   if (stream) cudaStreamDestroy(stream);
@@ -512,6 +514,11 @@ void collect(Engine& eng, ValsOf vals, size_t elem, void* out, int mem) {
                               (g1 - g0) * elem, cudaMemcpyDeviceToHost, eng.copy_stream));
       }
       TG_CK(cudaEventRecord(eng.stage_free[k], eng.copy_stream));
+      const uint64_t t = ++eng.collect_seq;
+      cudaEvent_t& te = eng.ticket_ev[t % Engine::kTickets];
+      if (!te) TG_CK(cudaEventCreateWithFlags(&te, cudaEventDisableTiming));
+      else TG_CK(cudaEventSynchronize(te));  // ticket t - kTickets is complete
+      TG_CK(cudaEventRecord(te, eng.copy_stream));
       return;
     }
     if (mem == TG_MEM_HOST && mode == 2) {
@@ -908,6 +915,24 @@ int tg_engine_sync(tg_engine* e) {
     TG_CK(cudaSetDevice(eng.device));
     if (eng.copy_stream) TG_CK(cudaStreamSynchronize(eng.copy_stream));
     TG_CK(cudaStreamSynchronize(eng.stream));
+  });
+}
+
+int tg_engine_last_ticket(const tg_engine* e, uint64_t* ticket) {
+  return guard([&] {
+    TG_REQUIRE(e != nullptr && ticket != nullptr, TG_EINVAL, "NULL engine or ticket");
+    *ticket = reinterpret_cast<const Engine*>(e)->collect_seq;
+  });
+}
+
+int tg_engine_wait_ticket(tg_engine* e, uint64_t ticket) {
+  return guard([&] {
+    TG_REQUIRE(e != nullptr, TG_EINVAL, "NULL engine");
+    Engine& eng = *reinterpret_cast<Engine*>(e);
+    TG_REQUIRE(ticket <= eng.collect_seq, TG_EINVAL, "tg_engine_wait_ticket: ticket not issued");
+    if (ticket == 0 || ticket + Engine::kTickets <= eng.collect_seq) return;  // complete
+    TG_CK(cudaSetDevice(eng.device));
+    TG_CK(cudaEventSynchronize(eng.ticket_ev[ticket % Engine::kTickets]));
   });
 }
 

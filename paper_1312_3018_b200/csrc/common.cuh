@@ -116,6 +116,13 @@ __device__ __forceinline__ float ld_f32_cold(const float* p, uint64_t pol) {
                : "=f"(v) : "l"(p), "l"(pol));
   return v;
 }
+// coherent (not .nc) load with an L2 policy: data other threads update with
+// atomics in the same kernel (SSSP distances)
+__device__ __forceinline__ uint32_t ld_u32_hint_coh(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ uint16_t ld_u16_hint(const uint16_t* p, uint64_t pol) {
   uint16_t v;
   asm volatile("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));

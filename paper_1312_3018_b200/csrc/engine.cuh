@@ -183,6 +183,10 @@ struct FrontierState {  // BFS / SSSP / BC-forward (messages arrive in Part::are
   DevBuf<uint32_t> obox_mark, obox_new;           // bitmaps over outbox slots
   DevBuf<uint32_t> obox_u32;                      // SSSP / CC min-combined values
   DevBuf<uint32_t> ibox_u32;                      // CC: owner-packed labels (reverse send)
+  // out-degree class bounds of the local ids (ids in out-degree order): [0,
+  // n_big) >= 2048, [n_big, n_mid) >= 32 (SSSP dense supersteps; lazily)
+  bool cls = false;
+  uint64_t n_big = 0, n_mid = 0;
   // see Vote: 8 counters per partition, a view into Engine::ctr_all (all
   // partitions contiguous, 64 B apart: one strided memset / copy per vote)
   struct {
@@ -324,6 +328,13 @@ struct Engine {
   cudaEvent_t stage_free[2] = {nullptr, nullptr};
   cudaEvent_t chunk_ev = nullptr;
   int stage_next = 0;
+  // collection tickets (tg_engine_last_ticket / tg_engine_wait_ticket): the
+  // n-th asynchronous host collection records ticket_ev[n % kTickets] on
+  // copy_stream after its last copy; a slot is reused only once its previous
+  // event completed, so every ticket <= collect_seq - kTickets is complete
+  static constexpr int kTickets = 16;
+  uint64_t collect_seq = 0;
+  cudaEvent_t ticket_ev[kTickets] = {};
   std::vector<std::unique_ptr<Part>> parts;
   uint64_t build_ms = 0;
   uint64_t launches = 0;     // kernels launched by the current run

@@ -120,6 +120,202 @@ __global__ void k_sssp_scatter(const uint32_t* msg, const uint32_t* lid, uint64_
   }
 }
 
+// Dense supersteps by out-degree class (TG_SSSP_CLASS_DIV): when the frontier's
+// out-edges exceed E / div, the superstep relaxes the active rows with three
+// kernels over the out-degree classes -- local ids are in out-degree order, so
+// the classes are id ranges: [0, n_big) a CTA per row, [n_big, n_mid) a warp
+// per row (a warp takes a frontier word and walks its active rows), the rest a
+// thread per row -- instead of the tile walker, whose per-window scan and
+// shuffles cost more than the load balance they buy once most tiles are busy.
+// Same relaxation, filter and counters as SsspOp.
+template <class W>
+struct Relax {
+  const uint64_t* row_off;
+  const uint32_t* col;
+  const W* w;
+  uint32_t* dist;
+  uint32_t* next;
+  uint32_t* obox;
+  unsigned long long* overflow;
+  RemoteOut rout;
+  bool fused;
+  uint32_t thresh, hub_end;
+  const uint32_t* cur;
+  unsigned long long* edges;
+  __device__ __forceinline__ bool keep(uint32_t v, uint32_t dv) const {
+    return v >= hub_end || dv < thresh;
+  }
+  __device__ __forceinline__ uint32_t target(uint32_t t) const {
+    return (t & kRemote) ? obox[t & ~kRemote] : dist[t];
+  }
+  __device__ __forceinline__ void relax(uint32_t dv, uint32_t t, uint32_t wt, uint32_t cd) const {
+    const uint64_t nd64 = (uint64_t)dv + wt;
+    if (nd64 >= (uint64_t)kInf) {
+      *overflow = 1ull;
+      return;
+    }
+    const uint32_t nd = (uint32_t)nd64;
+    if (!(nd < cd)) return;
+    if (t & kRemote) {
+      const uint32_t sl = t & ~kRemote;
+      atomicMin(&obox[sl], nd);
+      if (fused) atomicMin(rout.slot<uint32_t>(sl), nd);
+    } else {
+      atomicMin(&dist[t], nd);
+      atomicOr(&next[t >> 5], 1u << (t & 31));
+    }
+  }
+  // edges [i, e) of a row with distance dv, stride `step`, 4 in flight
+  __device__ __forceinline__ void row(uint32_t dv, uint64_t i, uint64_t e, uint32_t step) const {
+    for (; i + 3ull * step < e; i += 4ull * step) {
+      uint32_t t[4], wt[4], cd[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        t[k] = __ldcs(col + i + k * step);
+        wt[k] = (uint32_t)__ldcs(w + i + k * step);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cd[k] = target(t[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) relax(dv, t[k], wt[k], cd[k]);
+    }
+    for (; i < e; i += step) {
+      const uint32_t t = __ldcs(col + i);
+      relax(dv, t, (uint32_t)__ldcs(w + i), target(t));
+    }
+  }
+};
+
+__device__ __forceinline__ void add_edges(unsigned long long* ctr, unsigned long long n) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(ctr, n);
+}
+
+template <class W>
+__global__ void __launch_bounds__(256) k_sssp_cls_cta(Relax<W> r, uint64_t n_big) {
+  __shared__ uint32_t s_dv;
+  __shared__ int s_go;
+  unsigned long long ed = 0;
+  for (uint64_t v = blockIdx.x; v < n_big; v += gridDim.x) {
+    if (!((r.cur[v >> 5] >> (v & 31)) & 1u)) continue;  // block-uniform
+    if (threadIdx.x == 0) {
+      const uint32_t dv = r.dist[v];
+      s_dv = dv;
+      s_go = r.keep((uint32_t)v, dv);
+      if (!s_go) bit_set_atomic(r.next, (uint32_t)v);
+    }
+    __syncthreads();
+    const uint32_t dv = s_dv;
+    const int go = s_go;
+    __syncthreads();
+    if (!go) continue;
+    const uint64_t b = r.row_off[v], e = r.row_off[v + 1];
+    r.row(dv, b + threadIdx.x, e, blockDim.x);
+    if (threadIdx.x == 0) ed += e - b;
+  }
+  add_edges(r.edges, ed);
+}
+
+template <class W>
+__global__ void __launch_bounds__(256) k_sssp_cls_warp(Relax<W> r, uint64_t v0, uint64_t v1) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long ed = 0;
+  for (uint64_t wd = (v0 >> 5) + ((blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5);
+       wd * 32 < v1; wd += nwarps) {
+    uint32_t x = r.cur[wd];
+    const uint64_t base = wd * 32;
+    if (base < v0) x &= ~0u << (v0 - base);
+    if (base + 32 > v1) x &= (v1 - base >= 32) ? ~0u : ((1u << (v1 - base)) - 1u);
+    while (x) {
+      const uint32_t v = (uint32_t)base + (uint32_t)(__ffs(x) - 1);
+      x &= x - 1;
+      const uint32_t dv = r.dist[v];
+      if (!r.keep(v, dv)) {
+        if (lane == 0) bit_set_atomic(r.next, v);
+        continue;
+      }
+      const uint64_t b = r.row_off[v], e = r.row_off[v + 1];
+      r.row(dv, b + lane, e, 32);
+      if (lane == 0) ed += e - b;
+    }
+  }
+  add_edges(r.edges, ed);
+}
+
+template <class W>
+__global__ void __launch_bounds__(256) k_sssp_cls_thread(Relax<W> r, uint64_t v0, uint64_t v1) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  unsigned long long ed = 0;
+  for (uint64_t v = (v0 & ~31ull) + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+       v < ((v1 + 31) & ~31ull); v += stride) {
+    const uint32_t x = r.cur[v >> 5];
+    if (!x) continue;  // warp-uniform: one word per warp
+    if (v < v0 || v >= v1 || !((x >> (v & 31)) & 1u)) continue;
+    const uint32_t dv = r.dist[v];
+    if (!r.keep((uint32_t)v, dv)) {
+      bit_set_atomic(r.next, (uint32_t)v);
+      continue;
+    }
+    const uint64_t b = r.row_off[v], e = r.row_off[v + 1];
+    r.row(dv, b, e, 1);
+    ed += e - b;
+  }
+  add_edges(r.edges, ed);
+}
+
+__global__ void k_first_below_u64(const uint64_t* row_off, uint64_t n, uint32_t deg, uint64_t* out) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (row_off[mid + 1] - row_off[mid] >= deg) lo = mid + 1;
+    else hi = mid;
+  }
+  *out = lo;
+}
+
+void out_classes(Engine& eng, Part& p) {
+  FrontierState& f = p.fs;
+  if (f.cls) return;
+  DevBuf<uint64_t> d(2);
+  k_first_below_u64<<<1, 1, 0, eng.stream>>>(p.row_off.get(), p.nz_end, 2048, d.get());
+  k_first_below_u64<<<1, 1, 0, eng.stream>>>(p.row_off.get(), p.nz_end, 32, d.get() + 1);
+  TG_CK(cudaGetLastError());
+  uint64_t h[2];
+  TG_CK(cudaMemcpyAsync(h, d.get(), 16, cudaMemcpyDeviceToHost, eng.stream));
+  TG_CK(cudaStreamSynchronize(eng.stream));
+  f.n_big = h[0];
+  f.n_mid = h[1];
+  f.cls = true;
+}
+
+template <class W>
+void launch_classes(Engine& eng, Part& p, const W* w, uint32_t thresh, uint32_t hubs) {
+  FrontierState& f = p.fs;
+  cudaStream_t s = eng.stream;
+  Relax<W> r{p.row_off.get(), p.col.get(), w, f.vals.get(), f.next.get(), f.obox_u32.get(),
+             f.counters.get() + 4, p.rout(), eng.fused, thresh, hubs, f.cur.get(),
+             f.counters.get() + 1};
+  eng.prof_begin(TG_K_SSSP_EXPAND);
+  if (f.n_big) {
+    k_sssp_cls_cta<W><<<(unsigned)std::min<uint64_t>(f.n_big, 148u * 64u), 256, 0, s>>>(r, f.n_big);
+    eng.launches++;
+  }
+  if (f.n_mid > f.n_big) {
+    k_sssp_cls_warp<W><<<grid_for((f.n_mid - f.n_big), 256, 148u * 16u), 256, 0, s>>>(r, f.n_big,
+                                                                                        f.n_mid);
+    eng.launches++;
+  }
+  if (p.nz_end > f.n_mid) {
+    k_sssp_cls_thread<W><<<grid_for(p.nz_end - f.n_mid, 256, 148u * 16u), 256, 0, s>>>(r, f.n_mid,
+                                                                                         p.nz_end);
+    eng.launches++;
+  }
+  eng.prof_end(TG_K_SSSP_EXPAND);
+  TG_CK(cudaGetLastError());
+}
+
 void* send_obox(Part& p) { return p.fs.obox_u32.get(); }
 void* recv_ibox(Part& p) { return p.arena_fwd.get(); }
 
@@ -177,6 +373,10 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   // frontier by comparing distances afterwards instead of RED.OR per
   // improvement (TG_SSSP_DENSE_DIV, 0 = never)
   const uint32_t dense_div = env_u32("TG_SSSP_DENSE_DIV", 0);  // A/B: profiles/r02_sssp_dense_ab.txt
+  // class kernels when the frontier's out-edges exceed E / class_div (0 = never)
+  const uint32_t class_div = env_u32("TG_SSSP_CLASS_DIV", 0);
+  if (class_div)
+    for (auto& pp : eng.parts) out_classes(eng, *pp);
   if (dense_div)
     for (auto& pp : eng.parts)
       if (pp->fs.prev.n < std::max<uint64_t>(pp->Vp, 1)) pp->fs.prev.alloc(std::max<uint64_t>(pp->Vp, 1));
@@ -209,15 +409,22 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   if (eng.fused && eng.multi()) fused_arrival(eng);  // inboxes at INF before any peer writes
   uint64_t supersteps = 0, frontier = 1, relax = 0, activations = 1;
   uint64_t mind = 0;  // smallest tentative distance among the active vertices
+  uint64_t fr_out = 0;  // out-degree sum of the active vertices (class_div)
   for (;;) {
     reset_vote(eng);
     TG_CK(cudaMemset2DAsync(eng.ctr_all.get() + 5, 64, 0xFF, 8, eng.parts.size(), s));
     const uint64_t th = delta ? mind + delta : (uint64_t)kInf;
     const uint32_t thresh = th >= (uint64_t)kInf ? kInf : (uint32_t)th;
     const bool dense = dense_div && frontier * dense_div > eng.V;
+    const bool cls_step = class_div && fr_out * class_div > eng.E;
     for (size_t i = 0; i < eng.parts.size(); ++i) {
       Part& p = *eng.parts[i];
       FrontierState& f = p.fs;
+      if (cls_step) {
+        if (p.w8.get()) launch_classes(eng, p, p.w8.get(), thresh, hub_deg ? hubs[i] : kInf);
+        else launch_classes(eng, p, p.w.get(), thresh, hub_deg ? hubs[i] : kInf);
+        continue;
+      }
       launch_compact(eng, p.ts);
       if (dense && p.Vp)
         TG_CK(cudaMemcpyAsync(f.prev.get(), f.vals.get(), p.Vp * 4, cudaMemcpyDeviceToDevice, s));
@@ -265,7 +472,8 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
       Part& p = *pp;
       FrontierState& f = p.fs;
       launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get(),
-                     nullptr, nullptr, f.vals.get(), f.counters.get() + 5);
+                     class_div ? f.counters.get() + 2 : nullptr, nullptr, f.vals.get(),
+                     f.counters.get() + 5);
       std::swap(f.cur, f.next);
     }
     const Vote v = read_vote(eng);
@@ -281,6 +489,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     frontier = v.count;
     activations += v.count;
     mind = v.minval;
+    fr_out = v.degsum;
     if (v.count == 0) break;
     TG_REQUIRE(supersteps <= 4 * eng.V + 64, TG_EINTERNAL, "tg_sssp: superstep bound exceeded");
   }

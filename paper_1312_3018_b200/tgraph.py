@@ -168,6 +168,8 @@ def lib():
         L.tg_engine_set_exchange.argtypes = [p, i32]
         L.tg_engine_set_pagerank_comm.argtypes = [p, i32]
         L.tg_device_die_map.argtypes = [i32, p, i32, C.POINTER(i32), C.POINTER(i32)]
+        L.tg_engine_last_ticket.argtypes = [p, C.POINTER(C.c_uint64)]
+        L.tg_engine_wait_ticket.argtypes = [p, u64]
         L.tg_engine_kernel_stat.argtypes = [p, i32, C.POINTER(tg_kernel_stat)]
         L.tg_kernel_name.argtypes = [i32]
         L.tg_kernel_name.restype = C.c_char_p
@@ -187,7 +189,7 @@ def lib():
         L.tg_hostcomm_free.restype = None
         for f in ("tg_engine_set_async_collect", "tg_engine_sync", "tg_hostcomm_create", "tg_hostcomm_allreduce_u64", "tg_engine_create_edges", "tg_engine_create_rmat", "tg_engine_info",
                   "tg_engine_partition_info", "tg_bfs", "tg_sssp", "tg_pagerank", "tg_bc",
-                  "tg_cc", "tg_engine_set_profiling", "tg_engine_set_exchange", "tg_engine_set_pagerank_comm", "tg_device_die_map", "tg_engine_kernel_stat", "tg_graph_from_edges",
+                  "tg_cc", "tg_engine_set_profiling", "tg_engine_set_exchange", "tg_engine_set_pagerank_comm", "tg_device_die_map", "tg_engine_last_ticket", "tg_engine_wait_ticket", "tg_engine_kernel_stat", "tg_graph_from_edges",
                   "tg_graph_load_edge_list", "tg_graph_info", "tg_graph_edges", "tg_engine_create",
                   "tg_rmat_edges"):
             getattr(L, f).restype = i32
@@ -526,6 +528,16 @@ class Engine:
     def sync(self):
         """tg_engine_sync: wait for pending result copies."""
         _check(lib().tg_engine_sync(self.h))
+
+    def last_ticket(self) -> int:
+        """tg_engine_last_ticket: ticket of the latest asynchronous host collection."""
+        t = C.c_uint64(0)
+        _check(lib().tg_engine_last_ticket(self.h, C.byref(t)))
+        return t.value
+
+    def wait_ticket(self, ticket: int) -> None:
+        """tg_engine_wait_ticket: collection `ticket` and all earlier are in host memory."""
+        _check(lib().tg_engine_wait_ticket(self.h, int(ticket)))
 
     def set_exchange(self, mode):
         """TG_EXCHANGE_FUSED (default) or TG_EXCHANGE_COPY (tg_engine_set_exchange)."""

@@ -71,6 +71,8 @@ def test_argument_validation_precedes_cuda(tglib):
     assert tglib.tg_engine_set_exchange(None, tgraph.TG_EXCHANGE_FUSED) == tgraph.TG_EINVAL
     assert tglib.tg_engine_set_pagerank_comm(None, tgraph.TG_PR_PULL) == tgraph.TG_EINVAL
     assert tglib.tg_device_die_map(0, None, 0, None, None) == tgraph.TG_EINVAL
+    assert tglib.tg_engine_last_ticket(None, None) == tgraph.TG_EINVAL
+    assert tglib.tg_engine_wait_ticket(None, 0) == tgraph.TG_EINVAL
     assert b"NULL" in tglib.tg_last_error()
 
 

@@ -340,7 +340,7 @@ def test_set_exchange_rejects_unknown_mode(tg):
                                      ("TG_CC_GHOST_WARP", "1"), ("TG_CC_GHOST_WARP", "0"),
                                      ("TG_PR_REP", "1024"), ("TG_PR_NEXTPOL", "2"),
                                      ("TG_PR_HUB", "512"), ("TG_PR_GROUP", "1"),
-                                     ("TG_PR_PIPE", "3")])
+                                     ("TG_PR_PIPE", "3"), ("TG_SSSP_CLASS_DIV", "1000000")])
 @pytest.mark.parametrize("P", [1, 3])
 def test_kernel_variants_same_result(tg, variant, P, monkeypatch):
     """The A/B kernel variants behind run-time switches
@@ -664,6 +664,31 @@ def test_async_host_collection(tg):
         assert np.array_equal(lv, G.bfs(s)) and np.array_equal(ds, G.sssp(s))
         assert_pr(pr, ref_pr)
         assert_bc(b, G.bc([s]))
+    # collection tickets: double buffering -- after each round of four calls,
+    # the previous round's ticket is waited on and its outputs are exact while
+    # this round's copies may still be in flight; more rounds than ticket slots
+    t0 = eng.last_ticket()
+    assert t0 == 4 * len(srcs)
+    sets = [(np.empty(V, np.uint32), np.empty(V)) for _ in range(2)]
+    prev = t0
+    for k in range(20):
+        s = srcs[k % len(srcs)]
+        lv, b = sets[k % 2]
+        eng.bc([s], out=b)
+        eng.bfs(s, out=lv)
+        eng.wait_ticket(prev)
+        if k:
+            s0 = srcs[(k - 1) % len(srcs)]
+            lv0, b0 = sets[(k - 1) % 2]
+            assert np.array_equal(lv0, G.bfs(s0))
+            assert_bc(b0, G.bc([s0]))
+        prev = eng.last_ticket()
+        assert prev == t0 + 2 * (k + 1)
+    eng.wait_ticket(prev)
+    assert np.array_equal(sets[19 % 2][0], G.bfs(srcs[19 % len(srcs)]))
+    with pytest.raises(tg.TGraphError):
+        eng.wait_ticket(prev + 1)
+    eng.wait_ticket(0)
     eng.set_async_collect(False)
     assert np.array_equal(eng.bfs(srcs[0])[0], G.bfs(srcs[0]))
     eng.close()
