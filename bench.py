@@ -110,14 +110,18 @@ class ClockSampler:
 
 
 def gather_probe_ceiling():
-    """Best random-gather rate (loads/s) in the committed L2 probe table."""
-    path = os.path.join(ROOT, "profiles", "r01_l2_gather_probe.txt")
+    """Best rate (gathers/s) of PageRank's own access pattern -- a coalesced
+    4-byte index stream + dependent random 4-byte gathers from an L2-resident
+    region -- in the committed round-2 probe table (scripts/probes/l2_probe2.cu;
+    its hashed-index columns reach ~290 G/s, the L1TEX one-line-per-clock
+    rate).  The round-1 probe's 230 G/s was bounded by its own index arithmetic."""
+    path = os.path.join(ROOT, "profiles", "r02_l2_probe2.txt")
     best = 0.0
     try:
         for ln in open(path):
             f = ln.split()
-            if len(f) == 3 and not ln.startswith("#"):
-                best = max(best, float(f[1]), float(f[2]))
+            if len(f) == 4 and not ln.startswith("#"):
+                best = max(best, float(f[3]))
     except OSError:
         return None
     return best * 1e9 or None
@@ -427,15 +431,15 @@ def main():
                 "share_of_kernel_time": ks["ms"] / tot_ms if tot_ms else None}
     if dom == "pr_pull":
         # PageRank's pull is bounded by random 4-byte gather requests, not DRAM
-        # bytes: the probe (scripts/probes/l2_probe.cu) measures the B200's rate
-        # for random 4 B loads that all hit in L2 -- the ceiling for this kernel
+        # bytes: the probe (scripts/probes/l2_probe2.cu) measures the B200's rate
+        # for its access pattern when every gather hits in L2 -- the ceiling
         ceil = gather_probe_ceiling()
         gps = E / (roofline["avg_launch_ms"] * 1e-3)
         roofline["gather_bound"] = {
             "gathers_per_s": gps, "probe_ceiling_per_s": ceil,
             "frac": gps / ceil if ceil else None,
-            "source": "profiles/r01_l2_gather_probe.txt (random 4 B loads, L2-resident region, "
-                      "evict_last; 40 G/s when they miss to HBM)"}
+            "source": "profiles/r02_l2_probe2.txt (index stream + random 4 B gathers, "
+                      "L2-resident region, evict_last; ~41 G/s when they miss to HBM)"}
     kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 3),
                    "GBps": (v["algorithmic_bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] else None}
                for k, v in kstats.items() if v["launches"]}
