@@ -259,6 +259,29 @@ __global__ void k_in_fill(const uint64_t* row_off, const uint32_t* col, uint64_t
   }
 }
 
+// In-only single-partition engines (build_in_csr = 2, P = 1): the in-CSR is
+// filled straight from the edge stream (local id = degree position), so the
+// out-CSR's column array never exists -- RMAT-30's two CSRs (2 x 69 GB of
+// columns) would not fit one B200 together.
+__global__ void k_in_count_gen(EdgeGen g, uint64_t E, const uint32_t* rank_of, uint32_t* indeg) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < E; k += stride) {
+    uint32_t sv, dv;
+    g.get(k, sv, dv);
+    atomicAdd(&indeg[rank_of[dv]], 1u);
+  }
+}
+__global__ void k_in_fill_gen(EdgeGen g, uint64_t E, const uint32_t* rank_of, const uint64_t* in_off,
+                              uint32_t* cursor, uint32_t* in_col) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < E; k += stride) {
+    uint32_t sv, dv;
+    g.get(k, sv, dv);
+    const uint32_t r = rank_of[dv];
+    in_col[in_off[r] + atomicAdd(&cursor[r], 1u)] = rank_of[sv];
+  }
+}
+
 __global__ void k_outdeg_local(const uint64_t* row_off, uint64_t Vp, uint32_t* outdeg) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride)
@@ -529,7 +552,9 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
     TG_CK(cudaGetLastError());
   }
 
-  // out-CSR fill
+  // out-CSR fill (skipped by a single-partition in-only engine: stream_in)
+  const bool stream_in = eng.in_only && P == 1 && eng.has_in;
+  if (!stream_in) {
   pt.col.alloc(std::max<uint64_t>(pt.Ep, 1));
   if (eng.weighted) pt.w.alloc(std::max<uint64_t>(pt.Ep, 1));
   {
@@ -566,8 +591,11 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
     }
   }
 
+  }  // !stream_in
+  nloc.release();
+
   // tiles
-  pt.ntiles = (pt.Ep + kTile - 1) / kTile;
+  pt.ntiles = stream_in ? 0 : (pt.Ep + kTile - 1) / kTile;
   pt.tile_vf.alloc(std::max<uint64_t>(pt.ntiles, 1));
   pt.tile_vl.alloc(std::max<uint64_t>(pt.ntiles, 1));
   if (pt.ntiles) {
@@ -582,7 +610,10 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
     const uint64_t R = Vp + pt.S;
     DevBuf<uint32_t> indeg(std::max<uint64_t>(R, 1));
     TG_CK(cudaMemsetAsync(indeg.get(), 0, indeg.bytes(), s));
-    if (pt.Ep) {
+    if (pt.Ep && stream_in) {
+      k_in_count_gen<<<G(eng.E), kB, 0, s>>>(g, eng.E, eng.rank_of.get(), indeg.get());
+      TG_CK(cudaGetLastError());
+    } else if (pt.Ep) {
       k_in_count<<<G(pt.Ep), kB, 0, s>>>(pt.row_off.get(), pt.col.get(), pt.Ep, Vp,
                                          pt.tile_vf.get(), pt.tile_vl.get(), indeg.get());
       TG_CK(cudaGetLastError());
@@ -622,7 +653,11 @@ void build_part(Engine& eng, Part& pt, const EdgeGen& g, const uint32_t* order,
     }
     pt.in_col.alloc(std::max<uint64_t>(pt.Ep, 1));
     TG_CK(cudaMemsetAsync(indeg.get(), 0, indeg.bytes(), s));  // reuse as cursor
-    if (pt.Ep) {
+    if (pt.Ep && stream_in) {
+      k_in_fill_gen<<<G(eng.E), kB, 0, s>>>(g, eng.E, eng.rank_of.get(), pt.in_off.get(),
+                                            indeg.get(), pt.in_col.get());
+      TG_CK(cudaGetLastError());
+    } else if (pt.Ep) {
       k_in_fill<<<G(pt.Ep), kB, 0, s>>>(pt.row_off.get(), pt.col.get(), pt.Ep, Vp, pt.tile_vf.get(),
                                         pt.tile_vl.get(), pt.in_off.get(), indeg.get(),
                                         pt.in_col.get());

@@ -136,6 +136,29 @@ struct PRSplit {
   DevBuf<unsigned long long> qnext;     // [2] task queues' next index
 };
 
+// PageRank cold-tail propagation blocking (pagerank.cu, TG_PR_COLD=T): the
+// in-edges from the cold sources (local ids >= T: out-degree order puts them
+// last, past the L2-resident hub prefix) are not gathered by the pull.  Phase
+// A walks the cold sources in order and writes each contribution into a slot
+// per out-edge, the slots grouped by target bin (2^kb rows) -- random L2
+// gathers that miss to HBM become writes that L2 merges into whole lines;
+// phase B sums each bin's slots into a shared-memory accumulator and writes
+// the rows' cold partial sums, which the pull adds.  Single partition.
+struct PRCold {
+  bool on = false;
+  uint32_t T = 0;
+  int kb = 15;
+  const uint32_t* built_for = nullptr;
+  uint64_t e0 = 0, n = 0;       // cold out-edges: out-CSR [e0, e0 + n), sources [T, nz_end)
+  uint64_t nbins = 0;
+  DevBuf<uint32_t> pos;         // [n] slot of cold out-edge e0 + i
+  DevBuf<uint16_t> binv;        // [n] target row within its bin, per slot
+  DevBuf<float> binval;         // [n] contribution per slot (phase A)
+  DevBuf<uint64_t> bin_off;     // [nbins + 1]
+  DevBuf<uint32_t> hot_len;     // [R] in-edges of row r from sources < T (a prefix: rows ascend)
+  DevBuf<float> csum;           // [R] cold partial sum of row r (phase B)
+};
+
 struct PRState {  // PageRank (local-id order)
   DevBuf<float> contrib[2];
   DevBuf<float> rank;
@@ -143,6 +166,7 @@ struct PRState {  // PageRank (local-id order)
   DevBuf<double> obox;  // partial sums per outbox slot (send)
   PRHub hub;
   PRSplit split;
+  PRCold cold;
 };
 
 // Ghost-pull PageRank (TOTEM_COMM_PULL):

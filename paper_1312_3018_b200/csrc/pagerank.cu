@@ -122,10 +122,16 @@ struct PullOut {
   uint32_t hot;            // sources [0, hot) are gathered evict_last
   uint32_t l1hot;          // kL1 3: sources [0, l1hot) L1::evict_last
   int npol;                // next contributions of rows < hot: 0 evict_last, 1 normal, 2 evict_first
+  const uint32_t* hot_len; // PRCold: row r gathers only its first hot_len[r] in-edges ...
+  const float* csum;       // ... and adds the cold partial sum csum[r] (nullptr: off)
   RemoteOut rout;          // remote: outbox sums go straight into the owner's inbox ...
   bool remote;
   int parity;              // ... double-buffered by round parity (arena slot = 2 x f64)
+  __device__ __forceinline__ uint64_t row_end(uint64_t r, uint64_t b, uint64_t e) const {
+    return hot_len ? b + hot_len[r] : e;
+  }
   __device__ __forceinline__ void put(uint64_t r, double sum) const {
+    if (csum) sum += (double)csum[r];
     if (r < Vp) {
       if (fused) {
         const double rk = base + d * sum;
@@ -159,7 +165,8 @@ __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off
                                                           const double* hsum) {
   __shared__ double s_part[kCtaThreads / 32];
   const uint64_t r = rows[blockIdx.x];
-  const uint64_t b = in_off[r] + (hlen ? hlen[blockIdx.x] : 0u), e = in_off[r + 1];
+  const uint64_t b0 = in_off[r];
+  const uint64_t b = b0 + (hlen ? hlen[blockIdx.x] : 0u), e = o.row_end(r, b0, in_off[r + 1]);
   double sum = gather_sum<kL1>(in_col, contrib, b + threadIdx.x, e, kCtaThreads, o.hot, o.l1hot);
   sum = warp_sum(sum);
   if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = sum;
@@ -195,7 +202,8 @@ __global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_warp(const uint64_t*
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps) {
     const uint64_t r = rows[k];
-    const uint64_t b = in_off[r] + (hlen ? hlen[k] : 0u), e = in_off[r + 1];
+    const uint64_t b0 = in_off[r];
+    const uint64_t b = b0 + (hlen ? hlen[k] : 0u), e = o.row_end(r, b0, in_off[r + 1]);
     double sum = gather_sum<kL1, kRep>(in_col, contrib, b + lane, e, 32, o.hot, o.l1hot, rep);
     sum = warp_sum(sum);
     if (lane == 0) o.put(r, sum + (hsum ? hsum[k] : 0.0));
@@ -212,7 +220,7 @@ __global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_thread(const uint64_
   for (uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < r1; r += stride) {
     const uint64_t b = in_off[r], e = in_off[r + 1];
     if (e - b >= 32) continue;
-    o.put(r, gather_sum<kL1, kRep>(in_col, contrib, b, e, 1, o.hot, o.l1hot, rep));
+    o.put(r, gather_sum<kL1, kRep>(in_col, contrib, b, o.row_end(r, b, e), 1, o.hot, o.l1hot, rep));
   }
 }
 
@@ -642,7 +650,7 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
   // hub pass first: the class pulls of the CTA / warp rows add its sums
   const uint32_t* hl = nullptr;
   const double* hs = nullptr;
-  if (hub && hub->K && hub->ntask) {
+  if (hub && hub->K && hub->ntask && !o.hot_len) {
     const size_t smem = ((size_t)hub->K + 1) * sizeof(float);
     TG_CK(cudaFuncSetAttribute(k_pull_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     TG_CK(cudaMemsetAsync(hub->hsum.get(), 0, hub->n_list * sizeof(double), s));
@@ -679,7 +687,10 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rep_bytes));
   }
   const char* pipe_env = std::getenv("TG_PR_PIPE");
-  const int pipe = pipe_env ? std::atoi(pipe_env) : 0;  // bit 1 warp class, bit 2 thread class
+  // bit 1 warp class, bit 2 thread class; the cold-tail split (o.hot_len) runs
+  // the default class kernels only
+  const int pipe = pipe_env && !o.hot_len ? std::atoi(pipe_env) : 0;
+  if (o.hot_len) rep_k = 0;
   if (c.n_warp && (pipe & 1) && !hl) {
     k_pull_warp_pipe<kL1><<<grid_for(c.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(
         c.off, c.col, contrib, c.warp, c.n_warp, o);
@@ -696,8 +707,8 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
     eng.launches++;
   }
   if (R) {
-    const char* seg = std::getenv("TG_PR_SEG");
-    const char* grp = std::getenv("TG_PR_GROUP");
+    const char* seg = o.hot_len ? nullptr : std::getenv("TG_PR_SEG");
+    const char* grp = o.hot_len ? nullptr : std::getenv("TG_PR_GROUP");
     if (seg && seg[0] == '1')
       k_pull_seg<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, R, o);
     else if (pipe & 2)
@@ -1001,6 +1012,176 @@ void launch_split(Engine& eng, PRSplit& sp, const float* contrib, const PullOut&
   TG_CK(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- cold tail
+// phase A: a thread per cold source, its contribution into the slot of each
+// of its out-edges (slots grouped by target bin, in source order within a bin)
+__global__ void k_cold_bin(const uint64_t* __restrict__ row_off, uint64_t T, uint64_t nz_end,
+                           uint64_t e0, const uint32_t* __restrict__ pos,
+                           const float* __restrict__ contrib, float* binval) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t stream = l2_evict_first();
+  for (uint64_t u = T + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nz_end; u += stride) {
+    const float v = ld_f32_hint(contrib + u, stream);
+    for (uint64_t e = row_off[u], e1 = row_off[u + 1]; e < e1; ++e)
+      binval[ld_u32_hint(pos + (e - e0), stream)] = v;
+  }
+}
+
+// phase B: a CTA per bin sums its slots into 2^kb shared-memory accumulators
+// (fp32: a row's cold part is a few small terms) and writes the rows' sums
+constexpr unsigned kColdThreads = 1024;
+__global__ void __launch_bounds__(kColdThreads) k_cold_acc(const uint64_t* __restrict__ bin_off,
+                                                           const uint16_t* __restrict__ binv,
+                                                           const float* __restrict__ binval,
+                                                           int kb, uint64_t R, float* csum) {
+  extern __shared__ float acc[];
+  const uint32_t Bz = 1u << kb;
+  for (uint32_t j = threadIdx.x; j < Bz; j += blockDim.x) acc[j] = 0.0f;
+  __syncthreads();
+  const uint64_t stream = l2_evict_first();
+  const uint64_t s0 = bin_off[blockIdx.x], s1 = bin_off[blockIdx.x + 1];
+  uint64_t i = s0 + threadIdx.x;
+  constexpr int U = 8;
+  for (; i + (U - 1) * (uint64_t)blockDim.x < s1; i += U * (uint64_t)blockDim.x) {
+    uint32_t t[U];
+    float v[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      t[k] = ld_u16_hint(binv + i + k * blockDim.x, stream);
+      v[k] = ld_f32_hint(binval + i + k * blockDim.x, stream);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) atomicAdd(&acc[t[k]], v[k]);
+  }
+  for (; i < s1; i += blockDim.x) atomicAdd(&acc[ld_u16_hint(binv + i, stream)], ld_f32_hint(binval + i, stream));
+  __syncthreads();
+  const uint64_t r0 = (uint64_t)blockIdx.x << kb;
+  for (uint32_t j = threadIdx.x; j < Bz && r0 + j < R; j += blockDim.x) csum[r0 + j] = acc[j];
+}
+
+__global__ void k_cold_keys(const uint32_t* col, uint64_t e0, uint64_t n, int kb, uint32_t* key,
+                            uint32_t* idx, unsigned long long* bad) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t t = col[e0 + i];
+    if (t & kRemote) *bad = 1ull;
+    key[i] = t >> kb;
+    idx[i] = (uint32_t)i;
+  }
+}
+
+__global__ void k_cold_slots(const uint32_t* skey, const uint32_t* sidx, const uint32_t* col,
+                             uint64_t e0, uint64_t n, int kb, uint32_t* pos, uint16_t* binv) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t e = sidx[i];
+    pos[e] = (uint32_t)i;
+    binv[i] = (uint16_t)(col[e0 + e] & ((1u << kb) - 1u));
+  }
+}
+
+// bin_off[b] = first sorted slot with key >= b
+__global__ void k_cold_binoff(const uint32_t* skey, uint64_t n, uint64_t nbins, uint64_t* bin_off) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b <= nbins; b += stride) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t m = (lo + hi) >> 1;
+      if (skey[m] < b) lo = m + 1;
+      else hi = m;
+    }
+    bin_off[b] = lo;
+  }
+}
+
+__global__ void k_cold_hotlen(const uint64_t* off, const uint32_t* col, uint64_t R, uint32_t T,
+                              uint32_t* hot_len) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < R; r += stride) {
+    uint64_t lo = off[r], hi = off[r + 1];
+    const uint64_t b = lo;
+    while (lo < hi) {
+      const uint64_t m = (lo + hi) >> 1;
+      if (col[m] < T) lo = m + 1;
+      else hi = m;
+    }
+    hot_len[r] = (uint32_t)(lo - b);
+  }
+}
+
+// Cold-tail layout (outside the timed region).  Needs one partition with its
+// out-CSR, and memory for the slots + sort scratch; else stays off.
+void build_pr_cold(Engine& eng, Part& p, PRCold& c, uint32_t T, int kb, cudaStream_t s) {
+  if (c.built_for == p.in_col.get() && c.T == T && c.kb == kb) return;
+  c = PRCold{};
+  c.T = T;
+  c.kb = kb;
+  c.built_for = p.in_col.get();
+  if (eng.P != 1 || eng.in_only || !p.row_off.get() || T >= p.nz_end || kb < 8 || kb > 16) return;
+  uint64_t h[2];
+  TG_CK(cudaMemcpyAsync(&h[0], p.row_off.get() + T, 8, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaMemcpyAsync(&h[1], p.row_off.get() + p.nz_end, 8, cudaMemcpyDeviceToHost, s));
+  TG_CK(cudaStreamSynchronize(s));
+  c.e0 = h[0];
+  c.n = h[1] - h[0];
+  const uint64_t R = p.Vp;
+  if (!c.n || c.n >= (1ull << 32)) return;
+  size_t fr = 0, tot = 0;
+  TG_CK(cudaMemGetInfo(&fr, &tot));
+  if (c.n * 30 + R * 8 + (1ull << 30) > fr) return;
+  c.nbins = (R + (1ull << kb) - 1) >> kb;
+  {
+    DevBuf<uint32_t> key(c.n), idx(c.n), skey(c.n), sidx(c.n);
+    DevBuf<unsigned long long> bad(1);
+    TG_CK(cudaMemsetAsync(bad.get(), 0, 8, s));
+    k_cold_keys<<<grid_for(c.n, 256), 256, 0, s>>>(p.col.get(), c.e0, c.n, kb, key.get(), idx.get(),
+                                                   bad.get());
+    int bits = 1;
+    while ((1ull << bits) < c.nbins) ++bits;
+    size_t tmp = 0;
+    TG_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.get(), skey.get(), idx.get(), sidx.get(),
+                                          (int64_t)c.n, 0, bits, s));
+    DevBuf<uint8_t> t(tmp ? tmp : 1);
+    TG_CK(cub::DeviceRadixSort::SortPairs(t.get(), tmp, key.get(), skey.get(), idx.get(), sidx.get(),
+                                          (int64_t)c.n, 0, bits, s));
+    c.pos.alloc(c.n);
+    c.binv.alloc(c.n);
+    c.bin_off.alloc(c.nbins + 1);
+    k_cold_slots<<<grid_for(c.n, 256), 256, 0, s>>>(skey.get(), sidx.get(), p.col.get(), c.e0, c.n,
+                                                    kb, c.pos.get(), c.binv.get());
+    k_cold_binoff<<<grid_for(c.nbins + 1, 256), 256, 0, s>>>(skey.get(), c.n, c.nbins,
+                                                             c.bin_off.get());
+    unsigned long long hb = 0;
+    TG_CK(cudaMemcpyAsync(&hb, bad.get(), 8, cudaMemcpyDeviceToHost, s));
+    TG_CK(cudaStreamSynchronize(s));
+    if (hb) {  // remote targets: not a single-partition layout
+      c = PRCold{};
+      c.built_for = p.in_col.get();
+      return;
+    }
+  }
+  c.binval.alloc(c.n);
+  c.hot_len.alloc(R);
+  c.csum.alloc(R);
+  k_cold_hotlen<<<grid_for(R, 256), 256, 0, s>>>(p.in_off.get(), p.in_col.get(), R, T,
+                                                 c.hot_len.get());
+  TG_CK(cudaGetLastError());
+  TG_CK(cudaStreamSynchronize(s));
+  c.on = true;
+}
+
+void launch_cold(Engine& eng, Part& p, PRCold& c, const float* contrib) {
+  cudaStream_t s = eng.stream;
+  k_cold_bin<<<grid_for(p.nz_end - c.T, 256, 148u * 16u), 256, 0, s>>>(
+      p.row_off.get(), c.T, p.nz_end, c.e0, c.pos.get(), contrib, c.binval.get());
+  const size_t smem = ((size_t)1 << c.kb) * sizeof(float);
+  TG_CK(cudaFuncSetAttribute(k_cold_acc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_cold_acc<<<(unsigned)c.nbins, kColdThreads, smem, s>>>(c.bin_off.get(), c.binv.get(),
+                                                          c.binval.get(), c.kb, p.Vp, c.csum.get());
+  eng.launches += 2;
+  TG_CK(cudaGetLastError());
+}
+
 void* send_obox(Part& p) { return p.pr.obox.get(); }
 void* recv_ibox(Part& p) { return p.arena_fwd.get(); }
 
@@ -1067,6 +1248,19 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       Part& p = *pp;
       build_pr_split(eng, p.pr.split, ghost ? ghost_csr(p) : push_csr(p), s);
     }
+  // cold-tail propagation blocking (PRCold): sources >= TG_PR_COLD (0 = off),
+  // target bins of 2^TG_PR_COLD_KB rows
+  uint32_t coldT = 0;
+  int coldkb = 15;
+  if (const char* v = std::getenv("TG_PR_COLD")) coldT = (uint32_t)std::strtoul(v, nullptr, 10);
+  if (const char* v = std::getenv("TG_PR_COLD_KB")) coldkb = std::atoi(v);
+  bool cold = false;
+  if (coldT && !ghost && !split && eng.P == 1) {
+    Part& p0 = *eng.parts[0];
+    build_pr_cold(eng, p0, p0.pr.cold, coldT, coldkb, s);
+    cold = p0.pr.cold.on;
+  }
+
   time_begin(eng);
   for (auto& pp : eng.parts) {
     Part& p = *pp;
@@ -1084,8 +1278,10 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       PRState& r = p.pr;
       // P == 1 and ghost-pull: every in-edge is in the row, finalize in the pull
       PullOut o{eng.P == 1 || ghost, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
-                r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, l1hot, npol, p.rout(), eng.fused,
-                it & 1};
+                r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, l1hot, npol,
+                cold ? r.cold.hot_len.get() : nullptr, cold ? r.cold.csum.get() : nullptr,
+                p.rout(), eng.fused, it & 1};
+      if (cold) launch_cold(eng, p, r.cold, r.contrib[cur].get());
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
       if (split && r.split.on)
         launch_split(eng, r.split, r.contrib[cur].get(), o);

@@ -171,7 +171,7 @@ def test_full_cc_local_certificate(full):
 
 
 @pytest.mark.skipif(os.environ.get("TG_RMAT30") != "1",
-                    reason="RMAT-30 (2^34 edges, ~15 min of host certificate work): TG_RMAT30=1")
+                    reason="RMAT-30 (2^34 edges, ~2 min incl. the host certificate): TG_RMAT30=1")
 def test_rmat30_bfs_certificate_one_gpu():
     """BASELINE configs[4]'s graph (RMAT-30, 17.2 G edges) on ONE B200: an
     out-CSR-only engine (no weights, no in-CSR: ~100 GB) runs top-down BFS from
@@ -196,7 +196,7 @@ def test_rmat30_bfs_certificate_one_gpu():
 
 
 @pytest.mark.skipif(os.environ.get("TG_RMAT30") != "1",
-                    reason="RMAT-30 PageRank (2^34 edges, ~20 min of host checks): TG_RMAT30=1")
+                    reason="RMAT-30 PageRank (2^34 edges, ~4 min incl. host checks): TG_RMAT30=1")
 def test_rmat30_pagerank_one_gpu():
     """BASELINE configs[4]'s PageRank on ONE B200: an in-CSR-only engine
     (build_in_csr = 2: the out-CSR is released after the build) runs 5 rounds;

@@ -280,6 +280,41 @@ def test_pagerank_short_row_groups(tg, P, monkeypatch):
     assert_pr(eng.pagerank(5)[0], G.pagerank(5))
 
 
+@pytest.mark.parametrize("kb", ["8", "15"])
+def test_pagerank_cold_tail(tg, kb, monkeypatch):
+    """Cold-tail propagation blocking (PRCold, TG_PR_COLD=T): in-edges from the
+    sources >= T are summed by the two blocking phases (contributions written
+    into per-target-bin slots in source order, then per-bin shared-memory
+    sums), the pull gathers only each row's hot prefix and adds the cold sum.
+    Same oracle result for T from 1 (every source cold) to beyond the last
+    source with out-edges, bins of 2^8 and 2^15 rows; at P = 2 the layout is
+    off and the plain pull runs."""
+    monkeypatch.setenv("TG_PR_COLD_KB", kb)
+    scale = 13
+    src, dst, _ = inputs.rmat_edges(scale)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst)
+    ref = G.pagerank(5)
+    for P in (1, 2):
+        eng = tg.Engine.from_edges(V, src, dst, partitions=P, weighted=False)
+        for T in ("1", "100", "2000", "8000", "100000", "0"):
+            monkeypatch.setenv("TG_PR_COLD", T)
+            assert_pr(eng.pagerank(5)[0], ref)
+            monkeypatch.setenv("TG_PR_GROUP", "1")   # variants fall back to the plain pull
+            assert_pr(eng.pagerank(5)[0], ref)
+            monkeypatch.delenv("TG_PR_GROUP")
+        eng.close()
+    rng = np.random.default_rng(14)
+    n = 3000
+    s2 = np.concatenate([rng.integers(0, n, 20000), [5, 5, 5]]).astype(np.uint32)
+    d2 = np.concatenate([rng.integers(0, n, 20000), [5, 6, 6]]).astype(np.uint32)
+    G2 = oracle.Graph(n + 7, s2, d2)
+    e2 = tg.Engine.from_edges(n + 7, s2, d2, weighted=False)
+    for T in ("1", "1500", "2999"):
+        monkeypatch.setenv("TG_PR_COLD", T)
+        assert_pr(e2.pagerank(5)[0], G2.pagerank(5))
+
+
 def test_die_map(tg):
     """The measured SM -> die map of a B200: two clusters of pointer-chase
     latency (each die's L2 caches its own SMs' reads), neither tiny."""
@@ -711,3 +746,15 @@ def test_in_csr_only_engine(tg):
     assert eng.info["device_bytes"] < full.info["device_bytes"]
     eng.close()
     full.close()
+    # device-generated edges: the in-CSR is filled from the edge stream (no
+    # out-CSR columns at all); multigraph with self-loops and isolated vertices
+    gen = tg.Engine.rmat(scale, weighted=False, in_csr=2)
+    assert_pr(gen.pagerank(5)[0], G.pagerank(5))
+    gen.close()
+    rng = np.random.default_rng(15)
+    s2 = np.concatenate([rng.integers(0, 300, 5000), [7, 7, 9]]).astype(np.uint32)
+    d2 = np.concatenate([rng.integers(0, 300, 5000), [7, 8, 8]]).astype(np.uint32)
+    G2 = oracle.Graph(400, s2, d2)
+    e2 = tg.Engine.from_edges(400, s2, d2, in_csr=2)
+    assert_pr(e2.pagerank(20)[0], G2.pagerank(20))
+    e2.close()
