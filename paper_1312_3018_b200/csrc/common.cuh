@@ -123,6 +123,11 @@ __device__ __forceinline__ uint32_t ld_u32_hint_coh(const uint32_t* p, uint64_t 
   asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
+__device__ __forceinline__ double ld_f64_hint_coh(const double* p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
 __device__ __forceinline__ uint16_t ld_u16_hint(const uint16_t* p, uint64_t pol) {
   uint16_t v;
   asm volatile("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
