@@ -17,6 +17,7 @@
 //             double-buffered by round parity, so the communication phase is
 //             one arrival barrier per round and no copy.
 // No vote: a fixed number of rounds.
+#include <cstdio>
 #include <cstdlib>
 
 #include <cub/cub.cuh>
@@ -110,6 +111,81 @@ __device__ __forceinline__ double gather_sum(const uint32_t* __restrict__ in_col
   return s0 + s1;
 }
 
+// Predicated batches (TG_PR_PRED): U column loads, then U gathers, per lane and
+// iteration, every one predicated on the row end -- no remainder loop.  The
+// plain gather_sum issues a row's last < 4 x step entries one load at a time
+// (a warp-class row of ~214 entries: one 128-entry batch, then three
+// serialized 32-entry steps, each a full memory round trip); here a row of up
+// to U x step entries is one round trip of column loads and one of gathers.
+template <int U>
+__device__ __forceinline__ double gather_sum_pred(const uint32_t* __restrict__ in_col,
+                                                  const float* __restrict__ contrib, uint64_t i,
+                                                  uint64_t e, uint32_t step, uint32_t hot) {
+  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
+  double s0 = 0.0, s1 = 0.0;
+  for (; i < e; i += (uint64_t)U * step) {
+    uint32_t c[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint64_t j = i + (uint64_t)k * step;
+      c[k] = j < e ? ld_u32_hint(in_col + j, stream) : kInf;
+    }
+    float f[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      f[k] = c[k] != kInf ? ld_f32_hint(contrib + c[k], c[k] < hot ? keep : stream) : 0.0f;
+#pragma unroll
+    for (int k = 0; k < U; k += 2) {
+      s0 += (double)f[k];
+      if (k + 1 < U) s1 += (double)f[k + 1];
+    }
+  }
+  return s0 + s1;
+}
+
+// Lean predicated batches (kP < 0 in the class kernels, TG_PR_PRED negative
+// U): the lane's column pointer advances by a compile-time STEP, so the U
+// column loads of a batch are one base register + immediate offsets; each
+// batch's U contributions are summed in fp32 (U <= 8 terms: relative error
+// <= 7 x 2^-24 of the batch) and the batch total accumulated in fp64 (reading
+// A7: fp64 accumulation across the row), which replaces U fp32->fp64
+// conversions + U DADDs by U FADDs + 1 conversion + 1 DADD.
+// kUni (warp / CTA rows, TG_PR_UNIPOL): one L2 policy per warp and batch --
+// the load's policy operand is a uniform register, so a per-lane policy costs
+// a select + two register moves per gather; a row's entries ascend, so the
+// batch is all-hot when its largest column (one REDUX) is below `hot`.
+template <int U, int STEP, bool kUni = false>
+__device__ __forceinline__ double gather_sum_lean(const uint32_t* __restrict__ in_col,
+                                                  const float* __restrict__ contrib, uint64_t i,
+                                                  uint64_t e, uint32_t hot) {
+  const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
+  double s = 0.0;
+  const uint32_t* pc = in_col + i;
+  for (; i < e; i += (uint64_t)U * STEP, pc += U * STEP) {
+    const uint64_t left = e - i;  // > 0
+    uint32_t c[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      c[k] = (uint64_t)k * STEP < left ? ld_u32_hint(pc + k * STEP, stream) : kInf;
+    float f = 0.0f;
+    if constexpr (kUni) {
+      uint32_t mx = 0;
+#pragma unroll
+      for (int k = 0; k < U; ++k) mx = (c[k] != kInf && c[k] > mx) ? c[k] : mx;
+      const uint64_t pol = __reduce_max_sync(__activemask(), mx) < hot ? keep : stream;
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (c[k] != kInf) f += ld_f32_hint(contrib + c[k], pol);
+    } else {
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (c[k] != kInf) f += ld_f32_hint(contrib + c[k], c[k] < hot ? keep : stream);
+    }
+    s += (double)f;
+  }
+  return s;
+}
+
 struct PullOut {
   bool fused;
   uint64_t Vp;
@@ -156,7 +232,7 @@ struct PullOut {
 // one CTA per listed row (in-degree >= kPrCta)
 // Hub split (PRHub): hlen / hsum non-null -> the row's first hlen[k] in-edges
 // (sources < K) were summed by k_pull_hub into hsum[k]; start after them.
-template <int kL1>
+template <int kL1, int kP = 0>
 __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off,
                                                           const uint32_t* in_col,
                                                           const float* contrib,
@@ -167,7 +243,11 @@ __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off
   const uint64_t r = rows[blockIdx.x];
   const uint64_t b0 = in_off[r];
   const uint64_t b = b0 + (hlen ? hlen[blockIdx.x] : 0u), e = o.row_end(r, b0, in_off[r + 1]);
-  double sum = gather_sum<kL1>(in_col, contrib, b + threadIdx.x, e, kCtaThreads, o.hot, o.l1hot);
+  double sum;
+  if constexpr (kP < -100) sum = gather_sum_lean<-kP - 100, kCtaThreads, true>(in_col, contrib, b + threadIdx.x, e, o.hot);
+  else if constexpr (kP < 0) sum = gather_sum_lean<-kP, kCtaThreads>(in_col, contrib, b + threadIdx.x, e, o.hot);
+  else if constexpr (kP > 0) sum = gather_sum_pred<kP>(in_col, contrib, b + threadIdx.x, e, kCtaThreads, o.hot);
+  else sum = gather_sum<kL1>(in_col, contrib, b + threadIdx.x, e, kCtaThreads, o.hot, o.l1hot);
   sum = warp_sum(sum);
   if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = sum;
   __syncthreads();
@@ -192,7 +272,7 @@ __device__ __forceinline__ Rep load_rep(const float* contrib, uint32_t k) {
   }
 }
 
-template <int kL1, bool kRep = false>
+template <int kL1, bool kRep = false, int kP = 0>
 __global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_warp(const uint64_t* in_off, const uint32_t* in_col,
                                                    const float* contrib, const uint32_t* rows,
                                                    uint64_t n, PullOut o, uint32_t rep_k,
@@ -204,14 +284,18 @@ __global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_warp(const uint64_t*
     const uint64_t r = rows[k];
     const uint64_t b0 = in_off[r];
     const uint64_t b = b0 + (hlen ? hlen[k] : 0u), e = o.row_end(r, b0, in_off[r + 1]);
-    double sum = gather_sum<kL1, kRep>(in_col, contrib, b + lane, e, 32, o.hot, o.l1hot, rep);
+    double sum;
+    if constexpr (kP < -100) sum = gather_sum_lean<-kP - 100, 32, true>(in_col, contrib, b + lane, e, o.hot);
+    else if constexpr (kP < 0) sum = gather_sum_lean<-kP, 32>(in_col, contrib, b + lane, e, o.hot);
+    else if constexpr (kP > 0) sum = gather_sum_pred<kP>(in_col, contrib, b + lane, e, 32, o.hot);
+    else sum = gather_sum<kL1, kRep>(in_col, contrib, b + lane, e, 32, o.hot, o.l1hot, rep);
     sum = warp_sum(sum);
     if (lane == 0) o.put(r, sum + (hsum ? hsum[k] : 0.0));
   }
 }
 
 // one thread per row of [r0, r1) with in-degree < 32 (incl. 0); others skipped
-template <int kL1, bool kRep = false>
+template <int kL1, bool kRep = false, int kP = 0>
 __global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_thread(const uint64_t* in_off, const uint32_t* in_col,
                                                      const float* contrib, uint64_t r0, uint64_t r1,
                                                      PullOut o, uint32_t rep_k = 0) {
@@ -220,7 +304,9 @@ __global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_thread(const uint64_
   for (uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < r1; r += stride) {
     const uint64_t b = in_off[r], e = in_off[r + 1];
     if (e - b >= 32) continue;
-    o.put(r, gather_sum<kL1, kRep>(in_col, contrib, b, o.row_end(r, b, e), 1, o.hot, o.l1hot, rep));
+    if constexpr (kP < 0) o.put(r, gather_sum_lean<-kP, 1>(in_col, contrib, b, o.row_end(r, b, e), o.hot));
+    else if constexpr (kP > 0) o.put(r, gather_sum_pred<kP>(in_col, contrib, b, o.row_end(r, b, e), 1, o.hot));
+    else o.put(r, gather_sum<kL1, kRep>(in_col, contrib, b, o.row_end(r, b, e), 1, o.hot, o.l1hot, rep));
   }
 }
 
@@ -667,9 +753,30 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
     s_warp = eng.side[1];
   }
   const uint64_t R = c.R;
+  // batches per class (TG_PR_PRED=Ucta,Uwarp,Uthread): U > 0 predicated batches
+  // (gather_sum_pred), U < 0 lean batches of -U (gather_sum_lean), 0 the plain
+  // loop.  Default -8,-8,-4: RMAT-28 19.2 -> 18.2 ms per round
+  // (profiles/r02_pr_lean_ab.txt)
+  int pu[3] = {-8, -8, -4};
+  if (kL1 != 0 || hl) pu[0] = pu[1] = pu[2] = 0;
+  else if (const char* v = std::getenv("TG_PR_PRED"))
+    std::sscanf(v, "%d,%d,%d", &pu[0], &pu[1], &pu[2]);
   if (c.n_cta) {
-    k_pull_cta<kL1><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o,
-                                                                  hl, hs);
+    if (pu[0] == -108)
+      k_pull_cta<kL1, -108><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o, hl, hs);
+    else if (pu[0] == -16)
+      k_pull_cta<kL1, -16><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o, hl, hs);
+    else if (pu[0] == -8)
+      k_pull_cta<kL1, -8><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o, hl, hs);
+    else if (pu[0] == -4)
+      k_pull_cta<kL1, -4><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o, hl, hs);
+    else if (pu[0] == 2)
+      k_pull_cta<kL1, 2><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o, hl, hs);
+    else if (pu[0] == 4)
+      k_pull_cta<kL1, 4><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o, hl, hs);
+    else
+      k_pull_cta<kL1><<<(unsigned)c.n_cta, kCtaThreads, 0, s_cta>>>(c.off, c.col, contrib, c.cta, o,
+                                                                    hl, hs);
     eng.launches++;
   }
   // TG_PR_REP=k (A/B): warp / thread classes (TG_PR_REP_CLASSES bits 2 / 4) in
@@ -695,6 +802,24 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
     k_pull_warp_pipe<kL1><<<grid_for(c.n_warp * 32, 256, 148u * 16u), 256, 0, s_warp>>>(
         c.off, c.col, contrib, c.warp, c.n_warp, o);
     eng.launches++;
+  } else if (c.n_warp && (pu[1] == 4 || pu[1] == 8 || pu[1] == 6 || pu[1] == -4 || pu[1] == -8 ||
+                           pu[1] == -6 || pu[1] == -108)) {
+    const unsigned g = grid_for(c.n_warp * 32, 256, 148u * 16u);
+    if (pu[1] == -108)
+      k_pull_warp<kL1, false, -108><<<g, 256, 0, s_warp>>>(c.off, c.col, contrib, c.warp, c.n_warp, o, 0u, nullptr, nullptr);
+    else if (pu[1] == -6)
+      k_pull_warp<kL1, false, -6><<<g, 256, 0, s_warp>>>(c.off, c.col, contrib, c.warp, c.n_warp, o, 0u, nullptr, nullptr);
+    else if (pu[1] == -4)
+      k_pull_warp<kL1, false, -4><<<g, 256, 0, s_warp>>>(c.off, c.col, contrib, c.warp, c.n_warp, o, 0u, nullptr, nullptr);
+    else if (pu[1] == -8)
+      k_pull_warp<kL1, false, -8><<<g, 256, 0, s_warp>>>(c.off, c.col, contrib, c.warp, c.n_warp, o, 0u, nullptr, nullptr);
+    else if (pu[1] == 4)
+      k_pull_warp<kL1, false, 4><<<g, 256, 0, s_warp>>>(c.off, c.col, contrib, c.warp, c.n_warp, o, 0u, nullptr, nullptr);
+    else if (pu[1] == 6)
+      k_pull_warp<kL1, false, 6><<<g, 256, 0, s_warp>>>(c.off, c.col, contrib, c.warp, c.n_warp, o, 0u, nullptr, nullptr);
+    else
+      k_pull_warp<kL1, false, 8><<<g, 256, 0, s_warp>>>(c.off, c.col, contrib, c.warp, c.n_warp, o, 0u, nullptr, nullptr);
+    eng.launches++;
   } else if (c.n_warp) {
     if (rep_k && (rep_cls & 2))
       k_pull_warp<kL1, true><<<148u * rep_ctas, 1024, rep_bytes, s_warp>>>(
@@ -711,7 +836,18 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
     const char* grp = o.hot_len ? nullptr : std::getenv("TG_PR_GROUP");
     if (seg && seg[0] == '1')
       k_pull_seg<<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, R, o);
-    else if (pipe & 2)
+    else if (pu[2] == 2 || pu[2] == 4 || pu[2] == -4 || pu[2] == -8 || pu[2] == -2) {
+      if (pu[2] == -8)
+        k_pull_thread<kL1, false, -8><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
+      else if (pu[2] == -2)
+        k_pull_thread<kL1, false, -2><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
+      else if (pu[2] == -4)
+        k_pull_thread<kL1, false, -4><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
+      else if (pu[2] == 2)
+        k_pull_thread<kL1, false, 2><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
+      else
+        k_pull_thread<kL1, false, 4><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0, R, o);
+    } else if (pipe & 2)
       k_pull_thread_pipe<kL1><<<grid_for(R, 256, 148u * 16u), 256, 0, s>>>(c.off, c.col, contrib, 0,
                                                                           R, o);
     else if (grp && grp[0] == '1')

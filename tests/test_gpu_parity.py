@@ -375,7 +375,11 @@ def test_set_exchange_rejects_unknown_mode(tg):
                                      ("TG_CC_GHOST_WARP", "1"), ("TG_CC_GHOST_WARP", "0"),
                                      ("TG_PR_REP", "1024"), ("TG_PR_NEXTPOL", "2"),
                                      ("TG_PR_HUB", "512"), ("TG_PR_GROUP", "1"),
-                                     ("TG_PR_PIPE", "3"), ("TG_SSSP_CLASS_DIV", "1000000")])
+                                     ("TG_PR_PIPE", "3"), ("TG_SSSP_CLASS_DIV", "1000000"),
+                                     ("TG_PR_PRED", "4,8,4"), ("TG_PR_PRED", "2,6,2"),
+                                     ("TG_PR_PRED", "-4,-8,-4"), ("TG_PR_PRED", "0,-4,0"),
+                                     ("TG_PR_PRED", "-8,-6,-8"), ("TG_PR_PRED", "0,0,-2"),
+                                     ("TG_PR_PRED", "-108,-108,-4"), ("TG_PR_PRED", "-16,-8,-4")])
 @pytest.mark.parametrize("P", [1, 3])
 def test_kernel_variants_same_result(tg, variant, P, monkeypatch):
     """The A/B kernel variants behind run-time switches
