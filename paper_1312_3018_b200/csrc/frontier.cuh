@@ -201,8 +201,17 @@ __global__ void __launch_bounds__(kExpandThreads, MB) k_warp_expand(TileArgs a, 
       }
       buf ^= 1;
     }
-    for (uint32_t wv = vf & ~31u; wv <= vl; wv += 32) {
-      const uint32_t x = a.frontier[wv >> 5];
+    // the tile's frontier words, 32 windows per coalesced load: only windows
+    // with an active row are walked (a sparse frontier spread over the id range
+    // leaves most of a low-degree tile's ~16 windows empty)
+    for (uint32_t wb = vf >> 5; wb <= (vl >> 5); wb += 32) {
+      const uint32_t xw = wb + lane <= (vl >> 5) ? a.frontier[wb + lane] : 0u;
+      uint32_t wmask = __ballot_sync(kFull, xw != 0u);
+      while (wmask) {
+      const uint32_t kw = (uint32_t)__ffs(wmask) - 1u;
+      wmask &= wmask - 1u;
+      const uint32_t wv = (wb + kw) << 5;
+      const uint32_t x = __shfl_sync(kFull, xw, (int)kw);
       const uint32_t v = wv + lane;
       const bool act = ((x >> lane) & 1u) && v >= vf && v <= vl;
       if (!__ballot_sync(kFull, act)) continue;
@@ -313,6 +322,7 @@ __global__ void __launch_bounds__(kExpandThreads, MB) k_warp_expand(TileArgs a, 
         if (len > 0) op.vertex_done(v, acc, whole);
       }
       edges += T;
+      }  // windows with an active row
     }
   }
   if constexpr (kStage != 0) {  // drain a copy still in flight (issued past the last tile)
