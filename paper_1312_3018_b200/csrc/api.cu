@@ -31,6 +31,9 @@ Engine::~Engine() {
     if (join_ev[i]) cudaEventDestroy(join_ev[i]);
   }
   if (fork_ev) cudaEventDestroy(fork_ev);
+  for (auto ps : pstream) cudaStreamDestroy(ps);
+  for (auto e : pjoin) cudaEventDestroy(e);
+  if (pfork) cudaEventDestroy(pfork);
   if (copy_stream) cudaStreamSynchronize(copy_stream);
   for (int i = 0; i < 2; ++i)
     if (stage_free[i]) cudaEventDestroy(stage_free[i]);
@@ -309,6 +312,23 @@ void Engine::fork() {
   }
   TG_CK(cudaEventRecord(fork_ev, stream));
   for (int i = 0; i < 2; ++i) TG_CK(cudaStreamWaitEvent(side[i], fork_ev, 0));
+}
+
+bool Engine::part_streams_on() {
+  if (part_streams < 0) {
+    const char* v = std::getenv("TG_PART_STREAMS");
+    part_streams = (v && v[0] == '0') ? 0 : 1;
+    if (part_streams && parts.size() > 1) {
+      TG_CK(cudaEventCreateWithFlags(&pfork, cudaEventDisableTiming));
+      pstream.resize(parts.size());
+      pjoin.resize(parts.size());
+      for (size_t i = 0; i < parts.size(); ++i) {
+        TG_CK(cudaStreamCreateWithFlags(&pstream[i], cudaStreamNonBlocking));
+        TG_CK(cudaEventCreateWithFlags(&pjoin[i], cudaEventDisableTiming));
+      }
+    }
+  }
+  return part_streams == 1;
 }
 
 void Engine::join() {

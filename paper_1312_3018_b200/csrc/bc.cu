@@ -583,8 +583,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     // vote counters: start them from zero (they hold the previous run's values)
     reset_vote(eng);
     // ---------------- forward cycle ----------------
-    for (auto& pp : eng.parts) {
-      Part& p = *pp;
+    eng.each_part([&](Part& p) {
+      cudaStream_t s = eng.stream;
       FrontierState& f = p.fs;
       BCState& b = p.bcs;
       const uint64_t nw = words_for(p.Vp);
@@ -606,7 +606,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       }
       launch_advance(eng, p, p.ts, F0, nullptr, f.visited.get(), nullptr, 0, f.counters.get(),
                      f.counters.get() + 2, f.counters.get() + 3);
-    }
+    });
     uint32_t maxL = 0;
     uint64_t reached = 1;
     std::vector<uint64_t> lvl_count{1};  // |F[L]|
@@ -622,13 +622,14 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
       if (pull && eng.P > 1) {
         // sigma of every published source in F[L] (0 otherwise) -> peers' ghosts
         eng.prof_begin(TG_K_EXCHANGE);
-        for (auto& pp : eng.parts)
-          publish_frontier_sigma(eng, *pp, pp->bcs.level_bm[L].get(), pp->bcs.sigma.get());
+        eng.each_part([&](Part& p) {
+          publish_frontier_sigma(eng, p, p.bcs.level_bm[L].get(), p.bcs.sigma.get());
+        });
         fused_arrival(eng);
         eng.prof_end(TG_K_EXCHANGE);
       }
-      for (auto& pp : eng.parts) {
-        Part& p = *pp;
+      eng.each_part([&](Part& p) {
+        cudaStream_t s = eng.stream;
         FrontierState& f = p.fs;
         BCState& b = p.bcs;
         uint32_t* next = level_bitmap(p, L + 1);
@@ -677,7 +678,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           launch_expand(eng, p, p.ts, b.level_bm[L].get(), op, TG_K_BCF_EXPAND,
                         f.counters.get() + 1);
         }
-      }
+      });
       supersteps++;
       if (eng.P > 1 && !pull) {  // a pull step only sets owned vertices: no messages
         eng.prof_begin(TG_K_EXCHANGE);
@@ -687,8 +688,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         } else {
           exchange(eng, send_osigma, recv_isigma, 8, false);
         }
-        for (auto& pp : eng.parts) {
-          Part& p = *pp;
+        eng.each_part([&](Part& p) {
+          cudaStream_t s = eng.stream;
           FrontierState& f = p.fs;
           BCState& b = p.bcs;
           if (p.S) {
@@ -707,15 +708,15 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
             if (eng.fused) TG_CK(cudaMemsetAsync(p.arena_fwd.get(), 0, p.I * 8, s));
           }
           TG_CK(cudaGetLastError());
-        }
+        });
         eng.prof_end(TG_K_EXCHANGE);
       }
-      for (auto& pp : eng.parts) {
-        Part& p = *pp;
+      eng.each_part([&](Part& p) {
+        cudaStream_t s = eng.stream;
         FrontierState& f = p.fs;
         launch_advance(eng, p, p.ts, p.bcs.level_bm[L + 1].get(), nullptr, f.visited.get(), nullptr,
                        0, f.counters.get(), f.counters.get() + 2, f.counters.get() + 3);
-      }
+      });
       const Vote v = read_vote(eng);
       relax += v.edges;
       mf = v.degsum;
@@ -750,14 +751,14 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     for (uint32_t L = maxL; L >= 1; --L) {
       if (L < maxL) {
         if (eng.P > 1) {
-          for (auto& pp : eng.parts) {
-            Part& p = *pp;
-            if (!p.I) continue;
+          eng.each_part([&](Part& p) {
+            cudaStream_t s = eng.stream;
+            if (!p.I) return;
             k_bc_pack<<<grid_for(p.I, 256), 256, 0, s>>>(
                 p.ibox_lid.get(), p.I, p.bcs.level_bm[L + 1].get(), p.bcs.c.get(),
                 eng.fused ? nullptr : p.bcs.ibox_pack.get(), p.rin(), (int)(L & 1));
             eng.launches++;
-          }
+          });
           TG_CK(cudaGetLastError());
           // fused: the owners stored c into the referencing partitions' ghost
           // slots (buffer L & 1); one arrival barrier, and the next level writes
@@ -777,8 +778,8 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
         const bool push = dir.mode != 1 && pull_ready(eng) &&
                           (eng.P == 1 ? eng.parts[0]->in_ntiles > 0 : true) &&
                           (dir.mode == 2 || 2 * lvl_in[L + 1] < lvl_out[L]);
-        for (auto& pp : eng.parts) {
-          Part& p = *pp;
+        eng.each_part([&](Part& p) {
+          cudaStream_t s = eng.stream;
           const uint32_t hub = push ? (uint32_t)std::min<uint64_t>(bc_hub, p.nz_end) : 0u;
           if (hub) {  // hub rows of F[L]: pull over their out-edges (CTA per row)
             const double* ghost = reinterpret_cast<const double*>(p.arena_rev.get());
@@ -794,7 +795,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           }
           const uint32_t priv = (uint32_t)std::min<uint64_t>(bc_priv, p.Vp - std::min<uint64_t>(hub, p.Vp));
           if (push && eng.P > 1) {
-            if (!p.in_all_ntiles) continue;
+            if (!p.in_all_ntiles) return;
             const uint64_t R = p.Vp + p.S;
             if (p.bcs.ext.n < words_for(R)) p.bcs.ext.alloc(words_for(R));
             const double* ghost = reinterpret_cast<const double*>(p.arena_rev.get());
@@ -820,7 +821,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
           } else if (bwd_classes && lvl_out[L] * 16 > eng.E) {
             // dense level (F[L]'s out-edges > |E|/16): class kernels; sparse
             // levels keep the tile walker, which only visits active tiles
-            if (!p.nz_end) continue;
+            if (!p.nz_end) return;
             const double* ghost = reinterpret_cast<const double*>(p.arena_rev.get());
             PullDelta o{p.row_off.get(), p.col.get(), p.bcs.level_bm[L].get(),
                         p.bcs.level_bm[L + 1].get(), p.bcs.c.get(),
@@ -847,7 +848,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
             eng.prof_end(TG_K_BCB_EXPAND);
             TG_CK(cudaGetLastError());
           } else {
-            if (!p.ntiles) continue;
+            if (!p.ntiles) return;
             launch_mark_tiles(eng, out_tiles(p), p.Vp, p.bcs.level_bm[L].get(), p.ts);
             launch_compact(eng, p.ts);
             const double* ghost = reinterpret_cast<const double*>(p.arena_rev.get());
@@ -857,7 +858,7 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
             launch_expand(eng, p, p.ts, p.bcs.level_bm[L].get(), op, TG_K_BCB_EXPAND,
                           p.fs.counters.get() + 1);
           }
-        }
+        });
         if (dir.trace)
           std::fprintf(stderr, "[tg bc-bwd] L=%u %s out(F[L])=%llu in(F[L+1])=%llu ms=%.3f\n", L,
                        push ? "push" : "pull", (unsigned long long)lvl_out[L],
@@ -868,15 +869,15 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
                        8.0 * lvl_count[L + 1] + 24.0 * lvl_count[L] + 2.0 * bm_bytes);
         supersteps++;
       }
-      for (auto& pp : eng.parts) {
-        Part& p = *pp;
-        if (!p.Vp) continue;
+      eng.each_part([&](Part& p) {
+        cudaStream_t s = eng.stream;
+        if (!p.Vp) return;
         k_bc_level<<<grid_for(words_for(p.Vp), 256, 148u * 16u), 256, 0, s>>>(
             p.bcs.level_bm[L].get(), p.Vp, p.nz_end, p.bcs.sigma.get(), p.bcs.dsum.get(),
             p.bcs.bc.get(), p.bcs.c.get(), p.fs.counters.get() + 4);
         TG_CK(cudaGetLastError());
         eng.launches++;
-      }
+      });
     }
     total_ms += time_end(eng);
     eng.l2_window(nullptr, 0);

@@ -139,7 +139,6 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
   ensure_frontier_state(eng);
   eng.launches = 0;
   eng.comm_bytes = 0;
-  cudaStream_t s = eng.stream;
   uint64_t visited_total = 1;
   uint64_t bm_bytes = 0;  // one pass over every partition's vertex bitmap
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
@@ -149,8 +148,8 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
   if (eng.P > 1 && eng.has_in && direction_policy(eng).mode != 1) build_pr_ghost(eng);
   time_begin(eng);
   reset_vote(eng);
-  for (auto& pp : eng.parts) {
-    Part& p = *pp;
+  eng.each_part([&](Part& p) {
+    cudaStream_t s = eng.stream;
     FrontierState& f = p.fs;
     const uint64_t nw = words_for(p.Vp);
     TG_CK(cudaMemsetAsync(f.vals.get(), 0xFF, p.Vp * 4, s));
@@ -169,7 +168,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
     launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), f.visited.get(), f.vals.get(), 0,
                    f.counters.get(), f.counters.get() + 2);
     std::swap(f.cur, f.next);
-  }
+  });
   // fused: every inbox bitmap is clear before any peer writes into it (the vote
   // below synchronizes the ranks when direction optimization reads it; the
   // barrier covers the forced top-down mode)
@@ -187,12 +186,12 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
     if (bottom_up && eng.P > 1) {
       // the frontier bits of every published source -> the peers' ghost bits
       eng.prof_begin(TG_K_EXCHANGE);
-      for (auto& pp : eng.parts) publish_frontier_bits(eng, *pp, pp->fs.cur.get());
+      eng.each_part([&](Part& p) { publish_frontier_bits(eng, p, p.fs.cur.get()); });
       fused_arrival(eng);
       eng.prof_end(TG_K_EXCHANGE);
     }
-    for (auto& pp : eng.parts) {
-      Part& p = *pp;
+    eng.each_part([&](Part& p) {
+      cudaStream_t s = eng.stream;
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);  // drains the tile marks even when unused
       if (bottom_up) {
@@ -214,7 +213,7 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
                  p.rout(), eng.fused};
         launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_BFS_EXPAND, f.counters.get() + 1);
       }
-    }
+    });
     bu_steps += bottom_up;
     supersteps++;
     if (eng.P > 1 && !bottom_up) {  // a bottom-up step only sets owned vertices: no messages
@@ -225,8 +224,8 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
       } else {
         exchange(eng, send_onew, recv_ibits, 0, false);
       }
-      for (auto& pp : eng.parts) {
-        Part& p = *pp;
+      eng.each_part([&](Part& p) {
+        cudaStream_t s = eng.stream;
         if (p.S && !eng.fused) TG_CK(cudaMemsetAsync(p.fs.obox_new.get(), 0, p.S / 8, s));
         if (p.I) {
           k_bfs_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(
@@ -239,16 +238,15 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
           // (peers write again only after the vote below has synchronized)
           if (eng.fused) TG_CK(cudaMemsetAsync(p.arena_fwd.get(), 0, p.I / 8, s));
         }
-      }
+      });
       eng.prof_end(TG_K_EXCHANGE);
     }
-    for (auto& pp : eng.parts) {
-      Part& p = *pp;
+    eng.each_part([&](Part& p) {
       FrontierState& f = p.fs;
       launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), f.visited.get(), f.vals.get(), L + 1,
                      f.counters.get(), dir.mode == 1 ? nullptr : f.counters.get() + 2);
       std::swap(f.cur, f.next);
-    }
+    });
     const Vote v = read_vote(eng);
     mf = v.degsum;
     explored += mf;

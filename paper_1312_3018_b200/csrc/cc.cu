@@ -232,8 +232,8 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
   // TG_CC_GHOST_WARP=1: the round-1 warp-per-slot ghost pass (A/B)
   const bool ghost_warp = std::getenv("TG_CC_GHOST_WARP") && std::getenv("TG_CC_GHOST_WARP")[0] == '1';
   time_begin(eng);
-  for (auto& pp : eng.parts) {
-    Part& p = *pp;
+  eng.each_part([&](Part& p) {
+    cudaStream_t s = eng.stream;
     FrontierState& f = p.fs;
     const uint64_t nw = words_for(p.Vp);
     TG_CK(cudaMemsetAsync(f.counters.get(), 0, 64, s));
@@ -248,13 +248,13 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
     }
     launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get());
     std::swap(f.cur, f.next);
-  }
+  });
   if (eng.fused && eng.multi()) fused_arrival(eng);  // inboxes at INF before any peer writes
   uint64_t supersteps = 0, frontier = eng.V, processed = 0, activations = eng.V;
   for (;;) {
     reset_vote(eng);
-    for (auto& pp : eng.parts) {
-      Part& p = *pp;
+    eng.each_part([&](Part& p) {
+      cudaStream_t s = eng.stream;
       FrontierState& f = p.fs;
       launch_compact(eng, p.ts);
       CcPushOp op{p.col.get(), f.vals.get(), f.next.get(), f.obox_u32.get(), p.rout(), eng.fused};
@@ -266,19 +266,19 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
         launch_expand_on(eng, in_tiles(p), p.ts_in, f.cur.get(), rop, TG_K_CC_EXPAND,
                          f.counters.get() + 1);
       }
-    }
+    });
     supersteps++;
     if (eng.P > 1) {
       eng.prof_begin(TG_K_EXCHANGE);
-      for (auto& pp : eng.parts) {
-        Part& p = *pp;
-        if (!p.I) continue;
+      eng.each_part([&](Part& p) {
+        cudaStream_t s = eng.stream;
+        if (!p.I) return;
         k_cc_pack<<<grid_for(p.I, 256), 256, 0, s>>>(p.ibox_lid.get(), p.I, p.fs.cur.get(),
                                                      p.fs.vals.get(),
                                                      eng.fused ? nullptr : p.fs.ibox_u32.get(),
                                                      p.rin());
         eng.launches++;
-      }
+      });
       TG_CK(cudaGetLastError());
       // fused: forward minima and reverse ghost labels are already in the
       // receivers' arenas; readers finish before the vote, writers start after it
@@ -289,8 +289,8 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
         exchange(eng, send_obox, recv_ibox, 4, false);
         exchange(eng, send_pack, recv_ghost, 4, true);
       }
-      for (auto& pp : eng.parts) {
-        Part& p = *pp;
+      eng.each_part([&](Part& p) {
+        cudaStream_t s = eng.stream;
         FrontierState& f = p.fs;
         if (p.I) {
           k_cc_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(
@@ -299,12 +299,12 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
           eng.launches++;
         }
         TG_CK(cudaGetLastError());
-      }
+      });
       eng.prof_end(TG_K_EXCHANGE);
       // reverse direction, referencing side: published labels lower the local
       // sources of the outbox rows (compute on the received ghosts)
-      for (auto& pp : eng.parts) {
-        Part& p = *pp;
+      eng.each_part([&](Part& p) {
+        cudaStream_t s = eng.stream;
         FrontierState& f = p.fs;
         if (p.S && p.in_all_ntiles && !ghost_warp) {
           const uint64_t R = p.Vp + p.S;
@@ -325,14 +325,14 @@ void run_cc(Engine& eng, uint32_t* out, int mem, tg_stats* st) {
           eng.launches++;
         }
         TG_CK(cudaGetLastError());
-      }
+      });
     }
-    for (auto& pp : eng.parts) {
-      Part& p = *pp;
+    eng.each_part([&](Part& p) {
+      cudaStream_t s = eng.stream;
       FrontierState& f = p.fs;
       launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get());
       std::swap(f.cur, f.next);
-    }
+    });
     const Vote v = read_vote(eng);
     // both directions: col/in_col 4 + label[target] 4 per edge; offsets 16 +
     // label 4 per active vertex (each CSR); active + next bitmaps per pass

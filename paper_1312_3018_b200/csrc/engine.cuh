@@ -23,6 +23,7 @@
 #pragma once
 
 #include <memory>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -337,6 +338,44 @@ struct Engine {
   cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
   void fork();   // side streams wait for the main stream's work so far
   void join();   // the main stream waits for the side streams' work
+  // Per-partition streams (one process holding several partitions of one GPU):
+  // each_part(f) runs f(p) for every local partition with `stream` switched to
+  // p's own stream, forked from and joined back into the main stream, so the
+  // partitions' kernels of one phase overlap -- as P GPUs' would -- instead of
+  // queueing one partition behind another (launch tails and small grids).
+  // The phases keep their order: each call is one fork ... join.
+  // TG_PART_STREAMS=0: one stream (the round-2 behaviour).
+  std::vector<cudaStream_t> pstream;
+  std::vector<cudaEvent_t> pjoin;
+  cudaEvent_t pfork = nullptr;
+  int part_streams = -1;  // resolved on first use
+  bool part_streams_on();
+  template <class F>
+  void each_part(F&& f) {
+    auto call = [&](size_t i) {
+      if constexpr (std::is_invocable_v<F&, Part&, size_t>) f(*parts[i], i);
+      else f(*parts[i]);
+    };
+    if (parts.size() <= 1 || !part_streams_on()) {
+      for (size_t i = 0; i < parts.size(); ++i) call(i);
+      return;
+    }
+    TG_CK(cudaEventRecord(pfork, stream));
+    cudaStream_t const main = stream;
+    struct Restore {
+      Engine& e;
+      cudaStream_t m;
+      ~Restore() { e.stream = m; }
+    } restore{*this, main};
+    for (size_t i = 0; i < parts.size(); ++i) {
+      TG_CK(cudaStreamWaitEvent(pstream[i], pfork, 0));
+      stream = pstream[i];
+      call(i);
+      TG_CK(cudaEventRecord(pjoin[i], pstream[i]));
+    }
+    stream = main;
+    for (size_t i = 0; i < parts.size(); ++i) TG_CK(cudaStreamWaitEvent(main, pjoin[i], 0));
+  }
   DevBuf<uint32_t> rank_of;  // global id -> degree-order position
   DevBuf<uint8_t> scratch;   // device staging of host-bound results (V x 8 max)
   // Asynchronous host collection (tg_engine_set_async_collect): results bound

@@ -1398,19 +1398,19 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   }
 
   time_begin(eng);
-  for (auto& pp : eng.parts) {
-    Part& p = *pp;
-    if (!p.Vp) continue;
+  eng.each_part([&](Part& p) {
+    cudaStream_t s = eng.stream;
+    if (!p.Vp) return;
     k_pr_init<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.outdeg.get(), p.Vp, r0, p.pr.contrib[0].get(),
                                                   p.pr.rank.get());
     eng.launches++;
-  }
+  });
   if (ghost) publish(eng, 0);
   int cur = 0;
   for (int it = 0; it < iters; ++it) {
     eng.prof_begin(TG_K_PR_PULL);
-    for (auto& pp : eng.parts) {
-      Part& p = *pp;
+    eng.each_part([&](Part& p) {
+      cudaStream_t s = eng.stream;
       PRState& r = p.pr;
       // P == 1 and ghost-pull: every in-edge is in the row, finalize in the pull
       PullOut o{eng.P == 1 || ghost, p.Vp, base, d, r.acc.get(), r.obox.get(), r.rank.get(),
@@ -1424,7 +1424,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       else
         launch_pull(eng, ghost ? ghost_csr(p) : push_csr(p), r.contrib[cur].get(), o, concurrent,
                     l1, hubk ? &r.hub : nullptr);
-    }
+    });
     eng.prof_end(TG_K_PR_PULL);
     if (ghost) {  // communication: contributions of boundary sources -> peers' ghosts
       eng.prof_begin(TG_K_EXCHANGE);
@@ -1446,8 +1446,8 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
       } else {
         exchange(eng, send_obox, recv_ibox, 8, false);
       }
-      for (auto& pp : eng.parts) {
-        Part& p = *pp;
+      eng.each_part([&](Part& p) {
+        cudaStream_t s = eng.stream;
         PRState& r = p.pr;
         if (p.I) {
           const double* msg = reinterpret_cast<const double*>(p.arena_fwd.get());
@@ -1463,7 +1463,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
           eng.launches++;
         }
         TG_CK(cudaGetLastError());
-      }
+      });
       eng.prof_end(TG_K_EXCHANGE);
     }
     cur ^= 1;

@@ -390,8 +390,8 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
   if (eng.P == 1) eng.l2_window(eng.parts[0]->fs.vals.get(), eng.parts[0]->Vp * 4);
   time_begin(eng);
   for (auto& pp : eng.parts) TG_CK(cudaMemsetAsync(pp->fs.counters.get(), 0, 64, s));
-  for (auto& pp : eng.parts) {
-    Part& p = *pp;
+  eng.each_part([&](Part& p) {
+    cudaStream_t s = eng.stream;
     FrontierState& f = p.fs;
     const uint64_t nw = words_for(p.Vp);
     TG_CK(cudaMemsetAsync(f.vals.get(), 0xFF, p.Vp * 4, s));
@@ -405,7 +405,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     }
     launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get());
     std::swap(f.cur, f.next);
-  }
+  });
   if (eng.fused && eng.multi()) fused_arrival(eng);  // inboxes at INF before any peer writes
   uint64_t supersteps = 0, frontier = 1, relax = 0, activations = 1;
   uint64_t mind = 0;  // smallest tentative distance among the active vertices
@@ -417,13 +417,13 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     const uint32_t thresh = th >= (uint64_t)kInf ? kInf : (uint32_t)th;
     const bool dense = dense_div && frontier * dense_div > eng.V;
     const bool cls_step = class_div && fr_out * class_div > eng.E;
-    for (size_t i = 0; i < eng.parts.size(); ++i) {
-      Part& p = *eng.parts[i];
+    eng.each_part([&](Part& p, size_t i) {
+      cudaStream_t s = eng.stream;
       FrontierState& f = p.fs;
       if (cls_step) {
         if (p.w8.get()) launch_classes(eng, p, p.w8.get(), thresh, hub_deg ? hubs[i] : kInf);
         else launch_classes(eng, p, p.w.get(), thresh, hub_deg ? hubs[i] : kInf);
-        continue;
+        return;
       }
       launch_compact(eng, p.ts);
       if (dense && p.Vp)
@@ -447,7 +447,7 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
         TG_CK(cudaGetLastError());
         eng.launches++;
       }
-    }
+    });
     supersteps++;
     if (eng.P > 1) {
       eng.prof_begin(TG_K_EXCHANGE);
@@ -457,25 +457,23 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
       } else {
         exchange(eng, send_obox, recv_ibox, 4, false);
       }
-      for (auto& pp : eng.parts) {
-        Part& p = *pp;
-        if (!p.I) continue;
-        k_sssp_scatter<<<grid_for(p.I, 256), 256, 0, s>>>(
+      eng.each_part([&](Part& p) {
+        if (!p.I) return;
+        k_sssp_scatter<<<grid_for(p.I, 256), 256, 0, eng.stream>>>(
             reinterpret_cast<const uint32_t*>(p.arena_fwd.get()), p.ibox_lid.get(), p.I,
                                                           p.fs.vals.get(), p.fs.next.get());
         TG_CK(cudaGetLastError());
         eng.launches++;
-      }
+      });
       eng.prof_end(TG_K_EXCHANGE);
     }
-    for (auto& pp : eng.parts) {
-      Part& p = *pp;
+    eng.each_part([&](Part& p) {
       FrontierState& f = p.fs;
       launch_advance(eng, p, p.ts, f.next.get(), f.cur.get(), nullptr, nullptr, 0, f.counters.get(),
                      class_div ? f.counters.get() + 2 : nullptr, nullptr, f.vals.get(),
                      f.counters.get() + 5);
       std::swap(f.cur, f.next);
-    }
+    });
     const Vote v = read_vote(eng);
     // relaxation: col 4 + w 4 + dist[t] 4 per edge; offsets 16 + dist[v] 4 per
     // relaxed vertex; active + next bitmaps one pass each
