@@ -1118,10 +1118,11 @@ void build_engine(Engine& eng, const EdgeInput& in) {
     pt->arena_fwd.alloc(std::max<uint64_t>(pt->I, 1) * 16);  // 2 x 8 B: double-buffered PR sums
     pt->arena_rev.alloc(std::max<uint64_t>(pt->S, 1) * 16);  // 2 x 8 B: double-buffered BC ghosts
     pt->staging.alloc(std::max<uint64_t>(pt->Vp, 1) * 8);
-  }
-  TG_CK(cudaStreamSynchronize(s));
-  if (eng.in_only)  // PageRank-only engine: its pull needs the in-CSR and outdeg only
-    for (auto& pt : eng.parts) {
+    // PageRank-only engine: its pull needs the in-CSR and outdeg only; drop
+    // this partition's out-CSR before the next partition is built, so the peak
+    // is the in-CSRs plus ONE out-CSR (RMAT-30 in 8 partitions on one GPU)
+    if (eng.in_only) {
+      TG_CK(cudaStreamSynchronize(s));
       pt->col.release();
       pt->w.release();
       pt->w8.release();
@@ -1131,6 +1132,8 @@ void build_engine(Engine& eng, const EdgeInput& in) {
       pt->in_all_vl.release();
       pt->ntiles = pt->in_all_ntiles = 0;
     }
+  }
+  TG_CK(cudaStreamSynchronize(s));
   setup_peers(eng);
   eng.build_ms = (uint64_t)std::chrono::duration_cast<std::chrono::milliseconds>(
                      std::chrono::steady_clock::now() - t0)

@@ -199,13 +199,52 @@ def test_rmat30_bfs_certificate_one_gpu():
 
 
 @pytest.mark.skipif(os.environ.get("TG_RMAT30") != "1",
+                    reason="RMAT-30 in 8 partitions (2^34 edges, ~3 min incl. the certificate): TG_RMAT30=1")
+def test_rmat30_bfs_certificate_8_partitions():
+    """C5's partitioning at its own scale: RMAT-30 dealt into 8 degree-serpentine
+    partitions (the layout 8 B200s would hold, here all on one B200, out-CSRs
+    only), BFS with the boundary messages of 8 partitions per superstep; the
+    exact streaming certificate over the regenerated 2^34-edge stream proves
+    every level, and the partition layout is checked for balance and for the
+    outbox / inbox identity (every slot one peer sends is one the owner reads)."""
+    import paper_1312_3018_b200 as tg
+
+    scale, P = 30, 8
+    V, E = 1 << scale, 16 << scale
+    eng = tg.Engine.rmat(scale, partitions=P, weighted=False, in_csr=False)
+    info = [eng.partition_info(p) for p in range(P)]
+    s = int(inputs.rmat_sources(scale, 1)[0])
+    lv, st = eng.bfs(s)
+    eng.close()
+    assert sum(pi["Vp"] for pi in info) == V and sum(pi["Ep"] for pi in info) == E
+    emax = max(pi["Ep"] for pi in info)
+    assert emax <= 1.01 * E / P
+    # what p sends to q is exactly what q receives from p
+    for q in range(P):
+        assert info[q]["inbox_slots"] == sum(int(info[p]["slots_to"][q]) for p in range(P))
+    assert sum(pi["outbox_slots"] for pi in info) == sum(pi["inbox_slots"] for pi in info)
+    cert = oracle.StreamingCertificate(V, s, lv, weighted=False)
+    chunk = 1 << 28
+    for first in range(0, E, chunk):
+        src, dst, _ = inputs.rmat_edges(scale, first=first, count=min(chunk, E - first))
+        cert.feed(src, dst)
+    assert cert.holds()
+    slots = sum(pi["outbox_slots"] for pi in info)
+    print(f"RMAT-30 P=8 BFS: {st.device_ms:.1f} ms, supersteps {st.supersteps}, "
+          f"{st.traversed_edges / st.device_ms / 1e6:.1f} GTEPS; boundary slots {slots} "
+          f"(beta_red {slots / E:.4f}), edges max/mean {emax * P / E:.4f}")
+
+
+@pytest.mark.skipif(os.environ.get("TG_RMAT30") != "1",
                     reason="RMAT-30 PageRank (2^34 edges, ~4 min incl. host checks): TG_RMAT30=1")
 def test_rmat30_pagerank_one_gpu():
     """BASELINE configs[4]'s PageRank on ONE B200: an in-CSR-only engine
     (build_in_csr = 2: the out-CSR is released after the build) runs 5 rounds;
     the oracle recomputes round 5 from the GPU's round-4 ranks on a vertex
     sample (the 256 highest in-degrees + 8192 random vertices) over the
-    regenerated 2^34-edge stream (1e-5 relative), plus the mass identity."""
+    regenerated 2^34-edge stream (1e-5 relative), plus the mass identity.
+    (Eight partitions of it do not fit one GPU: ~20 GB of in-CSR, arenas and
+    PageRank state per partition.)"""
     import paper_1312_3018_b200 as tg
 
     scale = 30

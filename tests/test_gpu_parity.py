@@ -764,6 +764,12 @@ def test_in_csr_only_engine(tg):
     assert eng.info["device_bytes"] < full.info["device_bytes"]
     eng.close()
     full.close()
+    # several partitions: each partition's out-CSR is dropped as soon as its
+    # in-CSR and inbox are built
+    for P in (2, 3):
+        part = tg.Engine.from_edges(V, src, dst, in_csr=2, partitions=P)
+        assert_pr(part.pagerank(5)[0], G.pagerank(5))
+        part.close()
     # device-generated edges: the in-CSR is filled from the edge stream (no
     # out-CSR columns at all); multigraph with self-loops and isolated vertices
     gen = tg.Engine.rmat(scale, weighted=False, in_csr=2)
