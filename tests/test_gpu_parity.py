@@ -169,6 +169,29 @@ def test_partition_invariance_rmat12(tg, P):
     check_all(tg, G, eng, bfs_src=srcs, sssp_src=srcs[:3], pr_T=(5,), bc_src=srcs[:4])
 
 
+@pytest.mark.parametrize("streams", ["0", "1"])
+def test_partition_streams_same_result(tg, streams, monkeypatch):
+    """Engine::each_part: the partitions one process hosts launch every phase on
+    their own streams (fork / join per phase; TG_PART_STREAMS=1, the default)
+    or one after another on one stream (0).  Same oracle results, all five
+    algorithms, both transports, forced pull / push directions included."""
+    monkeypatch.setenv("TG_PART_STREAMS", streams)
+    scale = 12
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    srcs = inputs.list_sources(src, 4)
+    cc_ref = G.cc()
+    for direction in ("auto", "bottom", "top"):
+        monkeypatch.setenv("TG_DIRECTION", direction)
+        for mode in ("fused", "copy"):
+            eng = tg.Engine.from_edges(V, src, dst, w, partitions=5)
+            eng.set_exchange(tg.TG_EXCHANGE_FUSED if mode == "fused" else tg.TG_EXCHANGE_COPY)
+            check_all(tg, G, eng, bfs_src=srcs, sssp_src=srcs[:2], pr_T=(5,), bc_src=srcs[:2])
+            assert np.array_equal(eng.cc()[0], cc_ref)
+            eng.close()
+
+
 @pytest.mark.parametrize("P", [2, 3, 8])
 @pytest.mark.parametrize("mode", ["copy", "fused"])
 def test_exchange_modes_rmat13(tg, P, mode):
