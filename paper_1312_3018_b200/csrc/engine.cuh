@@ -22,6 +22,7 @@
 //     local ids of the sources, each row sorted ascending.
 #pragma once
 
+#include <exception>
 #include <memory>
 #include <type_traits>
 #include <vector>
@@ -362,11 +363,18 @@ struct Engine {
     }
     TG_CK(cudaEventRecord(pfork, stream));
     cudaStream_t const main = stream;
+    // an exception in f leaves through here: restore the main stream and drain
+    // the partition streams, so no work is left running unjoined
     struct Restore {
       Engine& e;
       cudaStream_t m;
-      ~Restore() { e.stream = m; }
-    } restore{*this, main};
+      int unwinding;
+      ~Restore() {
+        e.stream = m;
+        if (std::uncaught_exceptions() > unwinding)
+          for (cudaStream_t ps : e.pstream) cudaStreamSynchronize(ps);
+      }
+    } restore{*this, main, std::uncaught_exceptions()};
     for (size_t i = 0; i < parts.size(); ++i) {
       TG_CK(cudaStreamWaitEvent(pstream[i], pfork, 0));
       stream = pstream[i];

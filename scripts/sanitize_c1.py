@@ -1,5 +1,5 @@
 """Small run of all five algorithms for compute-sanitizer (memcheck /
-racecheck / synccheck): SPEC C1 (RMAT-10) at P = 1 and P = 2 in both exchange
+racecheck / synccheck): SPEC C1 (RMAT-10) at P = 1, 2 and 3 (per-partition streams) in both exchange
 transports, direction modes auto; each result is checked against the oracle so
 a sanitizer run is also a parity run.
 
@@ -21,7 +21,7 @@ V = 1 << scale
 G = oracle.Graph(V, src, dst, w)
 s = int(inputs.rmat_sources(scale, 1)[0])
 ref = {"bfs": G.bfs(s), "sssp": G.sssp(s), "pr": G.pagerank(5), "bc": G.bc([s]), "cc": G.cc()}
-for P in (1, 2):
+for P in (1, 2, 3):
     for x in ((None,) if P == 1 else (tg.TG_EXCHANGE_FUSED, tg.TG_EXCHANGE_COPY)):
         eng = tg.Engine.rmat(scale, partitions=P)
         if x is not None:
