@@ -203,6 +203,10 @@ struct PullOut {
   RemoteOut rout;          // remote: outbox sums go straight into the owner's inbox ...
   bool remote;
   int parity;              // ... double-buffered by round parity (arena slot = 2 x f64)
+  // fused: rows >= nz_end have out-degree 0 (ids in out-degree order), so no
+  // pull ever gathers their contribution: neither outdeg nor the next
+  // contribution is touched for them (0: every row writes it)
+  uint64_t nz_end = 0;
   __device__ __forceinline__ uint64_t row_end(uint64_t r, uint64_t b, uint64_t e) const {
     return hot_len ? b + hot_len[r] : e;
   }
@@ -213,6 +217,7 @@ struct PullOut {
         const double rk = base + d * sum;
         const uint64_t stream = l2_evict_first();
         st_f32_hint(rank + r, (float)rk, stream);
+        if (nz_end && r >= nz_end) return;
         const uint32_t od = outdeg[r];
         // next round's contributions: hubs stay evict_last like their gathers
         const float cn = od ? (float)(rk / (double)od) : 0.0f;
@@ -1368,6 +1373,9 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   // row classes on fork/join streams (TG_PR_CONCURRENT=0: one stream)
   const bool concurrent =
       !(std::getenv("TG_PR_CONCURRENT") && std::getenv("TG_PR_CONCURRENT")[0] == '0');
+  // rows of out-degree 0 skip their (never gathered) next contribution
+  // (TG_PR_NZSKIP=0: every row writes it)
+  const bool nzskip = !(std::getenv("TG_PR_NZSKIP") && std::getenv("TG_PR_NZSKIP")[0] == '0');
   // hub split (PRHub): K hub sources in shared memory (TG_PR_HUB, 0 = off)
   uint32_t hubk = 0;
   if (const char* v = std::getenv("TG_PR_HUB")) hubk = (uint32_t)std::strtoul(v, nullptr, 10);
@@ -1417,6 +1425,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
                 r.contrib[cur ^ 1].get(), p.outdeg.get(), hot, l1hot, npol,
                 cold ? r.cold.hot_len.get() : nullptr, cold ? r.cold.csum.get() : nullptr,
                 p.rout(), eng.fused, it & 1};
+      if (nzskip) o.nz_end = p.nz_end;
       if (cold) launch_cold(eng, p, r.cold, r.contrib[cur].get());
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
       if (split && r.split.on)
