@@ -207,6 +207,9 @@ struct PullOut {
   // pull ever gathers their contribution: neither outdeg nor the next
   // contribution is touched for them (0: every row writes it)
   uint64_t nz_end = 0;
+  // fused: rank is the output only after the last round; earlier rounds keep
+  // it in registers for the next contribution (false: no rank store)
+  bool rank_out = true;
   __device__ __forceinline__ uint64_t row_end(uint64_t r, uint64_t b, uint64_t e) const {
     return hot_len ? b + hot_len[r] : e;
   }
@@ -216,7 +219,7 @@ struct PullOut {
       if (fused) {
         const double rk = base + d * sum;
         const uint64_t stream = l2_evict_first();
-        st_f32_hint(rank + r, (float)rk, stream);
+        if (rank_out) st_f32_hint(rank + r, (float)rk, stream);
         if (nz_end && r >= nz_end) return;
         const uint32_t od = outdeg[r];
         // next round's contributions: hubs stay evict_last like their gathers
@@ -1376,6 +1379,8 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   // rows of out-degree 0 skip their (never gathered) next contribution
   // (TG_PR_NZSKIP=0: every row writes it)
   const bool nzskip = !(std::getenv("TG_PR_NZSKIP") && std::getenv("TG_PR_NZSKIP")[0] == '0');
+  // rank stored by the last round only (TG_PR_RANKLAST=0: every round)
+  const bool ranklast = !(std::getenv("TG_PR_RANKLAST") && std::getenv("TG_PR_RANKLAST")[0] == '0');
   // hub split (PRHub): K hub sources in shared memory (TG_PR_HUB, 0 = off)
   uint32_t hubk = 0;
   if (const char* v = std::getenv("TG_PR_HUB")) hubk = (uint32_t)std::strtoul(v, nullptr, 10);
@@ -1426,6 +1431,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
                 cold ? r.cold.hot_len.get() : nullptr, cold ? r.cold.csum.get() : nullptr,
                 p.rout(), eng.fused, it & 1};
       if (nzskip) o.nz_end = p.nz_end;
+      if (ranklast) o.rank_out = it + 1 == iters;
       if (cold) launch_cold(eng, p, r.cold, r.contrib[cur].get());
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
       if (split && r.split.on)
