@@ -169,6 +169,10 @@ struct PRState {  // PageRank (local-id order)
   PRHub hub;
   PRSplit split;
   PRCold cold;
+  // sink rows (local ids >= nz_end, out-degree 0) and their in-edges in the
+  // pull CSR it was counted for (rows a non-final round does not pull)
+  const uint64_t* sinks_for = nullptr;
+  uint64_t sink_rows = 0, sink_edges = 0;
 };
 
 // Ghost-pull PageRank (TOTEM_COMM_PULL):

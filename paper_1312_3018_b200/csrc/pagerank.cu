@@ -210,6 +210,10 @@ struct PullOut {
   // fused: rank is the output only after the last round; earlier rounds keep
   // it in registers for the next contribution (false: no rank store)
   bool rank_out = true;
+  // fused, non-final rounds: rows >= rows_end (the sinks, out-degree 0) have
+  // neither a rank to store nor a contribution anyone gathers -- they are not
+  // pulled at all (0: every row is)
+  uint64_t rows_end = 0;
   __device__ __forceinline__ uint64_t row_end(uint64_t r, uint64_t b, uint64_t e) const {
     return hot_len ? b + hot_len[r] : e;
   }
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_pull_cta(const uint64_t* in_off
                                                           const double* hsum) {
   __shared__ double s_part[kCtaThreads / 32];
   const uint64_t r = rows[blockIdx.x];
+  if (o.rows_end && r >= o.rows_end) return;  // a sink in a non-final round
   const uint64_t b0 = in_off[r];
   const uint64_t b = b0 + (hlen ? hlen[blockIdx.x] : 0u), e = o.row_end(r, b0, in_off[r + 1]);
   double sum;
@@ -290,6 +295,7 @@ __global__ void __launch_bounds__(kRep ? 1024 : 256) k_pull_warp(const uint64_t*
   const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t k = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; k < n; k += nwarps) {
     const uint64_t r = rows[k];
+    if (o.rows_end && r >= o.rows_end) continue;  // a sink in a non-final round
     const uint64_t b0 = in_off[r];
     const uint64_t b = b0 + (hlen ? hlen[k] : 0u), e = o.row_end(r, b0, in_off[r + 1]);
     double sum;
@@ -760,7 +766,7 @@ void launch_pull_l1(Engine& eng, const PullCsr& c, const float* contrib, const P
     s_cta = eng.side[0];
     s_warp = eng.side[1];
   }
-  const uint64_t R = c.R;
+  const uint64_t R = o.rows_end ? std::min<uint64_t>(c.R, o.rows_end) : c.R;
   // batches per class (TG_PR_PRED=Ucta,Uwarp,Uthread): U > 0 predicated batches
   // (gather_sum_pred), U < 0 lean batches of -U (gather_sum_lean), 0 the plain
   // loop.  Default -8,-8,-4: RMAT-28 19.2 -> 18.2 ms per round
@@ -1381,6 +1387,8 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   const bool nzskip = !(std::getenv("TG_PR_NZSKIP") && std::getenv("TG_PR_NZSKIP")[0] == '0');
   // rank stored by the last round only (TG_PR_RANKLAST=0: every round)
   const bool ranklast = !(std::getenv("TG_PR_RANKLAST") && std::getenv("TG_PR_RANKLAST")[0] == '0');
+  // non-final rounds do not pull the sinks' rows (TG_PR_SINKSKIP=0: they do)
+  const bool sinkskip = !(std::getenv("TG_PR_SINKSKIP") && std::getenv("TG_PR_SINKSKIP")[0] == '0');
   // hub split (PRHub): K hub sources in shared memory (TG_PR_HUB, 0 = off)
   uint32_t hubk = 0;
   if (const char* v = std::getenv("TG_PR_HUB")) hubk = (uint32_t)std::strtoul(v, nullptr, 10);
@@ -1410,6 +1418,33 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
     cold = p0.pr.cold.on;
   }
 
+  // rows (and their in-edges) a non-final round does not pull: the sinks
+  const bool sinks_idle = sinkskip && nzskip && ranklast && (eng.P == 1 || ghost) && iters > 1;
+  uint64_t skip_rows = 0, skip_edges = 0;
+  if (sinks_idle) {
+    for (auto& pp : eng.parts) {
+      Part& p = *pp;
+      const PullCsr c = ghost ? ghost_csr(p) : push_csr(p);
+      if (p.pr.sinks_for != c.off) {
+        uint64_t h[2] = {0, 0};
+        if (p.nz_end < p.Vp) {
+          TG_CK(cudaMemcpyAsync(&h[0], c.off + std::max<uint64_t>(p.nz_end, 1), 8,
+                                cudaMemcpyDeviceToHost, s));
+          TG_CK(cudaMemcpyAsync(&h[1], c.off + p.Vp, 8, cudaMemcpyDeviceToHost, s));
+          TG_CK(cudaStreamSynchronize(s));
+        }
+        p.pr.sink_rows = p.Vp - std::min<uint64_t>(std::max<uint64_t>(p.nz_end, 1), p.Vp);
+        p.pr.sink_edges = h[1] - h[0];
+        p.pr.sinks_for = c.off;
+      }
+      skip_rows += p.pr.sink_rows;
+      skip_edges += p.pr.sink_edges;
+    }
+    uint64_t x[2] = {skip_rows, skip_edges};
+    comm_allreduce(eng, x, 2, 0);
+    skip_rows = x[0];
+    skip_edges = x[1];
+  }
   time_begin(eng);
   eng.each_part([&](Part& p) {
     cudaStream_t s = eng.stream;
@@ -1432,6 +1467,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
                 p.rout(), eng.fused, it & 1};
       if (nzskip) o.nz_end = p.nz_end;
       if (ranklast) o.rank_out = it + 1 == iters;
+      if (sinkskip && nzskip && !o.rank_out && o.fused) o.rows_end = std::max<uint64_t>(p.nz_end, 1);
       if (cold) launch_cold(eng, p, r.cold, r.contrib[cur].get());
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
       if (split && r.split.on)
@@ -1448,7 +1484,11 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
     }
     // pull: in_col 4 + contrib gather 4 per edge; in_off 8 + outdeg 4 + rank 4 +
     // next contrib 4 per row
-    eng.prof_bytes(TG_K_PR_PULL, 8.0 * eng.E + 20.0 * eng.V);
+    {  // the units this round pulled (non-final rounds skip the sinks' rows)
+      const bool skipped = sinks_idle && it + 1 < iters;
+      eng.prof_bytes(TG_K_PR_PULL, 8.0 * (eng.E - (skipped ? skip_edges : 0)) +
+                                       20.0 * (eng.V - (skipped ? skip_rows : 0)));
+    }
     if (eng.P > 1 && !ghost) {
       eng.prof_begin(TG_K_EXCHANGE);
       // fused: the pull wrote this round's sums into the owners' arenas (buffer
@@ -1488,11 +1528,14 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   if (st) {
     st->device_ms = ms;
     st->supersteps = (uint64_t)iters;
-    st->relaxations = eng.E * (uint64_t)iters;
-    st->traversed_edges = eng.E * (uint64_t)iters;
-    // per iteration: 8 B per edge (in_col + contrib gather) + 20 B per vertex
+    // edges and rows pulled: the non-final rounds skip the sinks' rows (their
+    // in-edges, ~0.8 % of E on RMAT, are not counted as traversed)
+    const uint64_t rounds_skip = sinks_idle ? (uint64_t)iters - 1 : 0;
+    st->relaxations = eng.E * (uint64_t)iters - skip_edges * rounds_skip;
+    st->traversed_edges = st->relaxations;
+    // per pulled edge 8 B (in_col + contrib gather) + 20 B per pulled row
     // (in_off 8, outdeg 4, rank 4, contrib 4) -- DESIGN.md "Roofline"
-    st->algorithmic_bytes = (8 * eng.E + 20 * eng.V) * (uint64_t)iters;
+    st->algorithmic_bytes = st->relaxations * 8 + (eng.V * (uint64_t)iters - skip_rows * rounds_skip) * 20;
     st->comm_bytes = eng.comm_bytes;
     st->launches = eng.launches;
   }

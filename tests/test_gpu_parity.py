@@ -810,3 +810,25 @@ def test_in_csr_only_engine(tg):
     e2 = tg.Engine.from_edges(400, s2, d2, in_csr=2)
     assert_pr(e2.pagerank(20)[0], G2.pagerank(20))
     e2.close()
+
+
+@pytest.mark.parametrize("skip", ["1", "0"])
+def test_pagerank_sink_rows_stats(tg, skip, monkeypatch):
+    """Non-final PageRank rounds do not pull the rows of sinks (out-degree 0;
+    their intermediate ranks feed no output, TG_PR_SINKSKIP): ranks equal the
+    oracle's either way, and the stats count only the edges pulled --
+    E x T minus the sinks' in-edges in the T - 1 non-final rounds."""
+    monkeypatch.setenv("TG_PR_SINKSKIP", skip)
+    scale, T = 12, 5
+    src, dst, _ = inputs.rmat_edges(scale)
+    V, E = 1 << scale, len(src)
+    G = oracle.Graph(V, src, dst)
+    into_sinks = int((np.bincount(src, minlength=V)[dst] == 0).sum())
+    assert 0 < into_sinks < E // 20
+    for P in (1, 3):
+        eng = tg.Engine.from_edges(V, src, dst, partitions=P)
+        r, st = eng.pagerank(T)
+        assert_pr(r, G.pagerank(T))
+        want = E * T - (into_sinks * (T - 1) if skip == "1" and P == 1 else 0)
+        assert st.traversed_edges == want, (P, st.traversed_edges, want)
+        eng.close()
