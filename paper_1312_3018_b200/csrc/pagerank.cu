@@ -214,6 +214,8 @@ struct PullOut {
   // neither a rank to store nor a contribution anyone gathers -- they are not
   // pulled at all (0: every row is)
   uint64_t rows_end = 0;
+  // fused, last round: no next round gathers a contribution (false: none stored)
+  bool contrib_out = true;
   __device__ __forceinline__ uint64_t row_end(uint64_t r, uint64_t b, uint64_t e) const {
     return hot_len ? b + hot_len[r] : e;
   }
@@ -224,7 +226,7 @@ struct PullOut {
         const double rk = base + d * sum;
         const uint64_t stream = l2_evict_first();
         if (rank_out) st_f32_hint(rank + r, (float)rk, stream);
-        if (nz_end && r >= nz_end) return;
+        if ((nz_end && r >= nz_end) || !contrib_out) return;
         const uint32_t od = outdeg[r];
         // next round's contributions: hubs stay evict_last like their gathers
         const float cn = od ? (float)(rk / (double)od) : 0.0f;
@@ -1467,6 +1469,7 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
                 p.rout(), eng.fused, it & 1};
       if (nzskip) o.nz_end = p.nz_end;
       if (ranklast) o.rank_out = it + 1 == iters;
+      if (ranklast && !ghost) o.contrib_out = it + 1 < iters;  // ghost: published after the pull
       if (sinkskip && nzskip && !o.rank_out && o.fused) o.rows_end = std::max<uint64_t>(p.nz_end, 1);
       if (cold) launch_cold(eng, p, r.cold, r.contrib[cur].get());
       if (eng.P == 1) eng.l2_window(r.contrib[cur].get(), p.Vp * sizeof(float));  // opt-in
