@@ -626,12 +626,14 @@ __global__ void __launch_bounds__(256) k_pull_group(const uint64_t* in_off, cons
   }
 }
 
-__global__ void k_pr_init(const uint32_t* outdeg, uint64_t Vp, double r0, float* contrib, float* rank) {
+// r_0 = 1/|V| as the first round's contributions, for rows [0, n) -- rows past
+// nz_end have out-degree 0 and nothing gathers them (n = nz_end when the sink
+// trims are on).  rank needs no initial value: the last round stores every row.
+__global__ void k_pr_init(const uint32_t* outdeg, uint64_t n, double r0, float* contrib) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < Vp; i += stride) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t od = outdeg[i];
     contrib[i] = od ? (float)(r0 / (double)od) : 0.0f;
-    rank[i] = (float)r0;
   }
 }
 
@@ -1451,8 +1453,8 @@ void run_pagerank(Engine& eng, int iters, double d, float* out, int mem, tg_stat
   eng.each_part([&](Part& p) {
     cudaStream_t s = eng.stream;
     if (!p.Vp) return;
-    k_pr_init<<<grid_for(p.Vp, 256), 256, 0, s>>>(p.outdeg.get(), p.Vp, r0, p.pr.contrib[0].get(),
-                                                  p.pr.rank.get());
+    const uint64_t n = nzskip ? std::min<uint64_t>(p.nz_end, p.Vp) : p.Vp;
+    if (n) k_pr_init<<<grid_for(n, 256), 256, 0, s>>>(p.outdeg.get(), n, r0, p.pr.contrib[0].get());
     eng.launches++;
   });
   if (ghost) publish(eng, 0);
