@@ -425,9 +425,9 @@ def main():
                 "frac": achieved / peak, "traffic": traffic,
                 "traffic_source": "profiles/ncu_traffic.json: dram__bytes_read.sum + "
                                   "dram__bytes_write.sum per launch from a committed ncu "
-                                  "capture (pr_pull: one non-final round of the three class "
-                                  "pulls, profiles/r02_ncu_pr_rounds.csv; not measured inside "
-                                  "this run)",
+                                  "capture (pr_pull: the three class pulls averaged over the 5 "
+                                  "rounds of one call, profiles/r02_ncu_pr_rounds.csv; not "
+                                  "measured inside this run)",
                 "algorithmic_bytes_per_launch": ks["algorithmic_bytes"] / max(ks["launches"], 1),
                 "avg_launch_ms": ks["ms"] / max(ks["launches"], 1), "peak_source": peak_src,
                 "share_of_kernel_time": ks["ms"] / tot_ms if tot_ms else None}
