@@ -50,6 +50,9 @@ struct SsspOp {
   // that dropped (k_mark_dropped), so a relaxation issues one reduction (the
   // RED.MIN) instead of two -- the L2 request rate is what bounds this walk
   bool mark;
+  // local ids >= nz_end have out-degree 0: a sink whose distance drops has
+  // nothing to relax, so it is not activated (its distance is still set)
+  uint32_t nz_end;
   __device__ __forceinline__ Aux aux(uint32_t v) const { return dist[v]; }
   __device__ __forceinline__ bool keep(uint32_t v, const Aux& dv) const {
     return v >= hub_end || dv < thresh;
@@ -89,7 +92,7 @@ struct SsspOp {
       // so t is active next superstep.  Both updates are fire-and-forget
       // reductions (RED.MIN / RED.OR): no round trip on the critical path.
       atomicMin(&dist[t], nd);
-      if (mark) atomicOr(&next[t >> 5], 1u << (t & 31));
+      if (mark && t < nz_end) atomicOr(&next[t >> 5], 1u << (t & 31));
     }
   }
 };
@@ -385,6 +388,9 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
     for (size_t i = 0; i < eng.parts.size(); ++i) hubs[i] = hub_end(eng, *eng.parts[i], hub_deg);
   const bool trace = std::getenv("TG_TRACE") && std::getenv("TG_TRACE")[0] == '1';
   const DirectionPolicy tclock;  // trace lap clock only
+  // sinks (out-degree 0) are not activated when their distance drops
+  // (TG_SSSP_SINKS=1: they are, the round-2 behaviour)
+  const bool sink_idle = !(std::getenv("TG_SSSP_SINKS") && std::getenv("TG_SSSP_SINKS")[0] == '1');
   uint64_t bm_bytes = 0;
   for (auto& pp : eng.parts) bm_bytes += words_for(pp->Vp) * 4;
   if (eng.P == 1) eng.l2_window(eng.parts[0]->fs.vals.get(), eng.parts[0]->Vp * 4);
@@ -431,12 +437,12 @@ void run_sssp(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st
       if (p.w8.get()) {
         SsspOp<uint8_t> op{p.col.get(), p.w8.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
                            f.counters.get() + 4, p.rout(), eng.fused, thresh,
-                           hub_deg ? hubs[i] : kInf, !dense};
+                           hub_deg ? hubs[i] : kInf, !dense, sink_idle ? (uint32_t)p.nz_end : ~0u};
         launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
       } else {
         SsspOp<uint32_t> op{p.col.get(), p.w.get(), f.vals.get(), f.next.get(), f.obox_u32.get(),
                             f.counters.get() + 4, p.rout(), eng.fused, thresh,
-                            hub_deg ? hubs[i] : kInf, !dense};
+                            hub_deg ? hubs[i] : kInf, !dense, sink_idle ? (uint32_t)p.nz_end : ~0u};
         launch_expand(eng, p, p.ts, f.cur.get(), op, TG_K_SSSP_EXPAND, f.counters.get() + 1);
       }
       if (dense && p.Vp) {
