@@ -884,8 +884,11 @@ void run_bc(Engine& eng, const uint64_t* sources, int k, double* out, int mem, t
     const uint64_t bwd_edges = read_vote(eng).edges;
     relax += bwd_edges;
     eng.prof_bytes(TG_K_BCB_EXPAND, 4.0 * bwd_edges);
-    uint64_t nreached = 0;
-    const uint64_t tr = reached_outdeg_bitmap(eng, &nreached);
+    // every reached vertex is in exactly one level: the levels' exact out-degree
+    // sums give the reached out-degree total without another pass
+    const uint64_t nreached = reached;
+    uint64_t tr = 0;
+    for (const uint64_t x : lvl_out) tr += x;
     traversed += 2 * tr;
     // forward: col 4 + visited probe 4 + sigma RMW 8 per edge; backward: col 4 +
     // successor probe 4 + c gather 8 per edge; per reached vertex offsets 16 x2,

@@ -275,7 +275,12 @@ void run_bfs(Engine& eng, uint64_t source, uint32_t* out, int mem, tg_stats* st)
     st->supersteps = supersteps;
     st->relaxations = edges_total;
     uint64_t nreached = 0;
-    st->traversed_edges = reached_outdeg_u32(eng, &nreached);
+    if (dir.mode != 1) {  // the frontiers' exact out-degree sums cover every reached vertex once
+      st->traversed_edges = explored;
+      nreached = visited_total;
+    } else {
+      st->traversed_edges = reached_outdeg_u32(eng, &nreached);
+    }
     TG_REQUIRE(bu_steps || st->traversed_edges == edges_total, TG_EINTERNAL,
                "tg_bfs: expanded edges != sum of reached out-degrees");
     // 4 B per traversed edge (col), 16 B row offsets + 4 B level write per

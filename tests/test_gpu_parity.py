@@ -832,3 +832,23 @@ def test_pagerank_sink_rows_stats(tg, skip, monkeypatch):
         want = E * T - (into_sinks * (T - 1) if skip == "1" and P == 1 else 0)
         assert st.traversed_edges == want, (P, st.traversed_edges, want)
         eng.close()
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_traversed_edge_counts(tg, P):
+    """TEPS bases (reading A14): BFS counts the out-degrees of the reached
+    vertices, BC twice that (forward + backward), taken from the
+    frontiers' exact degree sums -- equal to the oracle's reached set, in every
+    direction mode."""
+    scale = 12
+    src, dst, w = inputs.rmat_edges(scale, weights=True)
+    V = 1 << scale
+    G = oracle.Graph(V, src, dst, w)
+    deg = G.out_degree()
+    eng = tg.Engine.from_edges(V, src, dst, w, partitions=P)
+    for s in inputs.list_sources(src, 3):
+        s = int(s)
+        want = int(deg[G.bfs(s) != 0xFFFFFFFF].sum())
+        assert eng.bfs(s)[1].traversed_edges == want
+        assert eng.bc([s])[1].traversed_edges == 2 * want
+    eng.close()
